@@ -1,0 +1,206 @@
+/*
+ * dfa.h -- C ABI of the B200 speculative chunked DFA membership test
+ * (Ko, Jung, Han, Burgstaller, arXiv:1210.5093).
+ *
+ * Citations "P:n" are lines of the paper's LaTeX source; names in
+ * CamelCase/dots are its \label{}s.  The library is libdfa.so, built from
+ * paper_1210_5093_b200/csrc.  No C++ or torch types cross this boundary:
+ * plain integers and pointers only.  A CUDA stream is passed as `void*`
+ * (a cudaStream_t; NULL = the legacy default stream).
+ *
+ * Problem (Alg.seqmatch): given a DFA
+ * (Q, Sigma, delta, q0, F) and an input x, compute delta-hat(q0, x) and
+ * whether it is in F.  The library computes it as the paper does:
+ * the input is partitioned into chunks (Eq.LZero / Eq.StartPosition /
+ * Eq.EndPosition), every chunk k >= 1 is matched speculatively
+ * from the initial-state set I_sigma of its reverse-lookahead symbol
+ * sigma = x[b_k - 1] (Eq.istates, Alg.MatchingInitialStates
+ * P:1031-1079), each chunk yields a state map L_k, and the maps
+ * are composed (Eq.SeqReduction, Eq.MapReduction).
+ *
+ * Conventions (readings R1-R12 in DESIGN.md):
+ *  - symbols are input bytes: byte b is column b of the table; a byte
+ *    >= alphabet_size is an error (DFA_ERR_SYMBOL), reading R12;
+ *  - error states Z = { q not in F : delta(q,c) = q for all c } (the paper's
+ *    q_E), reading R1.  I_sigma = delta(Q, sigma) \ Z
+ *    (Alg.MatchingInitialStates line 5), listed in ascending order;
+ *  - I_max = max over sigma < alphabet_size of |I_sigma| (Eq.MaxIstates);
+ *    it is the row stride of the map arrays (at least 1);
+ *  - chunks are half-open [b_k, b_{k+1}), b_0 = 0, b_P = n (R5);
+ *  - the chunk-0 length ratio c = c_num/c_den replaces the paper's
+ *    w_0*m/w (Eq.LZero with homogeneous w_i, i >= 1):
+ *        b_k = floor(n * (c + k - 1) / (c + P - 1)),  1 <= k <= P-1,
+ *    evaluated exactly in integers (R3, R4);
+ *  - state maps are compact: row k-1 (chunk k >= 1) has entry
+ *    j = delta-hat(I_sigma_k[j], C_k) for j < |I_sigma_k| and 0xFFFF after
+ *    (R6, R7).  Chunk 0 yields the single state e0 = delta-hat(q0, C_0) (R8).
+ *
+ * Ownership: dfa_create copies the table and bitmap (the caller may free
+ * them on return).  The handle owns its device copies and scratch, freed by
+ * dfa_destroy.  Every dev_* pointer is caller-owned device memory, borrowed
+ * for the stream-ordered lifetime of the call.
+ *
+ * Errors: every call returns a dfa_status; nothing is thrown across the
+ * ABI; out-parameters are untouched on error.  Calls on one handle must not
+ * overlap in time (one in-flight call per handle; it owns one scratch area).
+ */
+#ifndef DFA_H
+#define DFA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dfa_handle *dfa_handle_t;
+
+typedef enum {
+    DFA_OK = 0,
+    DFA_ERR_ARG = 1,       /* NULL pointer, bad option, host-only handle used for compute */
+    DFA_ERR_STATES = 2,    /* |Q| == 0 or > 65000, q0 >= |Q|, table entry >= |Q| */
+    DFA_ERR_ALPHABET = 3,  /* |Sigma| == 0 or > 256 */
+    DFA_ERR_CHUNKS = 4,    /* P == 0, n < c + P - 1, or explicit bounds not strictly increasing */
+    DFA_ERR_SYMBOL = 5,    /* an input byte >= |Sigma| */
+    DFA_ERR_OOM = 6,       /* device or host allocation failed */
+    DFA_ERR_CUDA = 7,      /* a CUDA runtime call failed (no device, launch failure) */
+    DFA_ERR_INTERNAL = 8   /* a device-side consistency check failed (bug) */
+} dfa_status;
+
+/* Static analysis of a DFA (host preprocessing at dfa_create). */
+typedef struct {
+    uint32_t num_states;      /* |Q| */
+    uint32_t alphabet_size;   /* |Sigma| */
+    uint32_t num_classes;     /* distinct table columns over 0..|Sigma|-1 */
+    uint32_t i_max;           /* Eq.MaxIstates, >= 1; map row stride */
+    uint32_t gamma_num;       /* gamma = I_max / |Q \ Z| (Eq.obtained_speedup, R2) */
+    uint32_t gamma_den;
+    uint32_t num_dead;        /* |Z| */
+    uint32_t dead_state;      /* smallest state of Z, 0xFFFF if Z is empty */
+    uint32_t num_absorbing;   /* states with delta(q,c) = q for all c (incl. accepting) */
+    uint32_t table_mode;      /* device table layout, DFA_TABLE_* */
+    uint32_t table_bytes;     /* bytes of the device table kept in shared memory (0 = global) */
+    uint32_t c_num, c_den;    /* chunk-0 length ratio c used by dfa_chunk_maps */
+    uint32_t device_ready;    /* 1 if device tables were uploaded (0 = host-only handle) */
+} dfa_info;
+
+enum {
+    DFA_TABLE_IDENT_U8 = 1,   /* smem, 256 byte-indexed columns, uint8 states   */
+    DFA_TABLE_IDENT_U16 = 2,  /* smem, 256 byte-indexed columns, uint16 states  */
+    DFA_TABLE_WINDOW_U8 = 3,  /* smem, columns = byte window + default column  */
+    DFA_TABLE_WINDOW_U16 = 4,
+    DFA_TABLE_PACKED9 = 5,    /* smem, 9-bit states packed 3 per 32-bit word    */
+    DFA_TABLE_GLOBAL_U16 = 6  /* global memory through L1/__ldg                 */
+};
+
+/* dfa_create_ex flags */
+enum {
+    DFA_CREATE_HOST_ONLY = 1  /* analysis only: no device memory touched; compute calls fail */
+};
+
+/*
+ * dfa_create: validate and analyse a DFA, upload device tables.
+ *   table          host, |Q|*|Sigma| uint16, table[q*|Sigma| + c] = delta(q, c)
+ *   num_states     |Q|, 1..65000
+ *   alphabet_size  |Sigma|, 1..256; input byte b is symbol b
+ *   q0             start state
+ *   accept_bitmap  host, ceil(|Q|/8) bytes; q in F iff bit (q&7) of byte q>>3
+ *   out            receives the handle
+ * Host work O(|Q|*256): error states, column classes, I_sigma for every
+ * symbol (Alg.MatchingInitialStates lines 1-7, computed once
+ * offline as P:1099-1103 allows), I_max, gamma, table placement.
+ */
+dfa_status dfa_create(const uint16_t *table, uint32_t num_states, uint32_t alphabet_size,
+                      uint16_t q0, const uint8_t *accept_bitmap, dfa_handle_t *out);
+dfa_status dfa_create_ex(const uint16_t *table, uint32_t num_states, uint32_t alphabet_size,
+                         uint16_t q0, const uint8_t *accept_bitmap, uint32_t flags,
+                         dfa_handle_t *out);
+dfa_status dfa_destroy(dfa_handle_t h);
+
+dfa_status dfa_get_info(dfa_handle_t h, dfa_info *out);
+
+/* I_sigma for symbol `sigma` (ascending); out_states must hold i_max entries. */
+dfa_status dfa_domain(dfa_handle_t h, uint32_t sigma, uint16_t *out_states, uint32_t *out_count);
+
+/* Chunk-0 length ratio c = c_num/c_den (both 1..2^20) used by dfa_chunk_maps. */
+dfa_status dfa_set_chunk_ratio(dfa_handle_t h, uint32_t c_num, uint32_t c_den);
+
+/* Host evaluation of the partition formula (above) into host_bounds[P+1]. */
+dfa_status dfa_plan_bounds(uint64_t n, uint32_t num_chunks, uint32_t c_num, uint32_t c_den,
+                           uint64_t *host_bounds);
+
+/*
+ * dfa_match: membership test of dev_input[0..len) (device memory).  Runs the
+ * chunked speculative path on `stream` and synchronises it to return host
+ * scalars: *final_state = delta-hat(q0, x), *accept = (final in F).
+ * len == 0 returns (q0, F[q0]) without launching.  DFA_ERR_SYMBOL if some
+ * byte >= |Sigma|.
+ */
+dfa_status dfa_match(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, void *stream,
+                     uint16_t *final_state, int *accept);
+
+/*
+ * dfa_match_host: the same call for an input in HOST memory (pinned for
+ * full speed): copies it to the device inside the call, overlapping the
+ * copy of piece i+1 with the matching of piece i, then synchronises.
+ */
+dfa_status dfa_match_host(dfa_handle_t h, const uint8_t *host_input, uint64_t len, void *stream,
+                          uint16_t *final_state, int *accept);
+
+/*
+ * dfa_chunk_maps: the per-chunk results for P = num_chunks reporting chunks
+ * with the handle's c (asynchronous on `stream`; DFA_ERR_CHUNKS if
+ * len < c + P - 1 so that some chunk would be empty):
+ *   dev_bounds      [P+1]  uint64 chunk offsets (out)
+ *   dev_chunk0_end  [1]    e0 = delta-hat(q0, C_0) (out)
+ *   dev_maps        [(P-1)*i_max] uint16 compact maps (out; may be NULL iff P == 1)
+ *   dev_chunk_start [P]    true initial state of every chunk (out; may be NULL)
+ *   dev_final       [2]    {final state, accept} as uint16 (out; may be NULL)
+ * A bad symbol is reported by dfa_get_last_device_error after a stream sync.
+ */
+dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len,
+                          uint32_t num_chunks, void *stream, uint64_t *dev_bounds,
+                          uint16_t *dev_chunk0_end, uint16_t *dev_maps,
+                          uint16_t *dev_chunk_start, uint16_t *dev_final);
+
+/* Same for a caller-given partition dev_bounds_in[P+1] (device memory):
+ * 0 = b_0 < b_1 < ... < b_P = len, validated on the host after a copy. */
+dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t len,
+                             uint32_t num_chunks, const uint64_t *dev_bounds_in, void *stream,
+                             uint16_t *dev_chunk0_end, uint16_t *dev_maps,
+                             uint16_t *dev_chunk_start, uint16_t *dev_final);
+
+/* After a stream sync: DFA_ERR_SYMBOL / DFA_ERR_INTERNAL raised by the last
+ * asynchronous call's kernels, else DFA_OK.  Clears the flag. */
+dfa_status dfa_get_last_device_error(dfa_handle_t h);
+
+/*
+ * Tuning / measurement options (DFA_OPT_*).  Defaults are chosen by the
+ * library from the table placement and the device's SM count.
+ */
+enum {
+    DFA_OPT_SUBCHUNK_TARGET = 1, /* number of execution sub-chunks per call (0 = auto) */
+    DFA_OPT_CONVERGENCE = 2,     /* 1 = merge converged lanes (default), 0 = off */
+    DFA_OPT_PROFILE = 3,         /* 1 = record per-kernel CUDA-event times */
+    DFA_OPT_THREADS_PER_CTA = 4  /* match kernel CTA size (0 = auto) */
+};
+dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
+
+/* Per-call statistics of the last completed call (valid after a stream sync). */
+typedef struct {
+    uint64_t input_bytes;      /* n */
+    uint64_t num_subchunks;    /* execution sub-chunks of the last call */
+    uint64_t lanes_initial;    /* sum over sub-chunks of |I_sigma| (1 for the first) */
+    uint32_t num_kernels;      /* kernels launched by the last call */
+    uint32_t profiled;         /* 1 if kernel_ms below are valid */
+    float kernel_ms[8];        /* per-kernel durations (DFA_OPT_PROFILE) */
+    char kernel_name[8][32];
+} dfa_stats;
+dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out);
+
+const char *dfa_status_string(dfa_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFA_H */

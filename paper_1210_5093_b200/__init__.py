@@ -1,0 +1,275 @@
+"""B200-native speculative chunked DFA membership test (arXiv:1210.5093).
+
+Thin ctypes binding of ``libdfa.so`` (C ABI in ``include/dfa.h``).  Function
+names are the C names; this module only marshals arguments (numpy arrays for
+host memory, torch CUDA tensors or raw ints for device memory, torch streams).
+Every step of the path runs in the library's CUDA kernels; there is no CPU
+fallback: if ``libdfa.so`` is missing, importing the functions raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+from .build import LIB
+from .build import build  # noqa: F401
+
+__all__ = [
+    "DfaError", "dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
+    "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
+    "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
+    "dfa_status_string", "Dfa", "lib", "EXPORTED",
+]
+
+DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
+DFA_ERR_SYMBOL, DFA_ERR_OOM, DFA_ERR_CUDA, DFA_ERR_INTERNAL = 5, 6, 7, 8
+DFA_CREATE_HOST_ONLY = 1
+DFA_OPT_SUBCHUNK_TARGET, DFA_OPT_CONVERGENCE, DFA_OPT_PROFILE, DFA_OPT_THREADS_PER_CTA = 1, 2, 3, 4
+TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16"}
+
+
+class DfaInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in (
+        "num_states", "alphabet_size", "num_classes", "i_max", "gamma_num", "gamma_den", "num_dead",
+        "dead_state", "num_absorbing", "table_mode", "table_bytes", "c_num", "c_den", "device_ready")]
+
+
+class DfaStats(ctypes.Structure):
+    _fields_ = [("input_bytes", ctypes.c_uint64), ("num_subchunks", ctypes.c_uint64),
+                ("lanes_initial", ctypes.c_uint64), ("num_kernels", ctypes.c_uint32),
+                ("profiled", ctypes.c_uint32), ("kernel_ms", ctypes.c_float * 8),
+                ("kernel_name", (ctypes.c_char * 32) * 8)]
+
+
+class DfaError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {dfa_status_string(status)} ({status})")
+
+
+# every function declared in include/dfa.h
+EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
+            "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
+            "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
+            "dfa_status_string"]
+
+_lib = None
+
+
+def lib():
+    """Load libdfa.so; raise if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} not built: run paper_1210_5093_b200.build.build() "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB)
+        V, u16, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint16, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+        sig = {
+            "dfa_create": [V, u32, u32, u16, V, V],
+            "dfa_create_ex": [V, u32, u32, u16, V, u32, V],
+            "dfa_destroy": [V],
+            "dfa_get_info": [V, V],
+            "dfa_domain": [V, u32, V, V],
+            "dfa_set_chunk_ratio": [V, u32, u32],
+            "dfa_plan_bounds": [u64, u32, u32, u32, V],
+            "dfa_match": [V, V, u64, V, V, V],
+            "dfa_match_host": [V, V, u64, V, V, V],
+            "dfa_chunk_maps": [V, V, u64, u32, V, V, V, V, V, V],
+            "dfa_chunk_maps_at": [V, V, u64, u32, V, V, V, V, V, V],
+            "dfa_get_last_device_error": [V],
+            "dfa_set_option": [V, u32, ctypes.c_int64],
+            "dfa_get_stats": [V, V],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = i32
+        L.dfa_status_string.argtypes = [i32]
+        L.dfa_status_string.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def dfa_status_string(status: int) -> str:
+    return lib().dfa_status_string(int(status)).decode()
+
+
+def _ck(status: int, what: str):
+    if status != DFA_OK:
+        raise DfaError(status, what)
+
+
+def _ptr(x) -> Optional[int]:
+    """Device/host pointer of a torch tensor, numpy array or int (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# --------------------------------------------------------------------------- calls
+def dfa_create_ex(table: np.ndarray, q0: int, accept_bitmap: np.ndarray, flags: int = 0) -> ctypes.c_void_p:
+    t = np.ascontiguousarray(table, dtype=np.uint16)
+    nq, ns = t.shape
+    bm = np.ascontiguousarray(accept_bitmap, dtype=np.uint8)
+    if bm.size * 8 < nq:
+        raise ValueError("accept bitmap too short")
+    h = ctypes.c_void_p()
+    _ck(lib().dfa_create_ex(t.ctypes.data, nq, ns, int(q0), bm.ctypes.data, int(flags), ctypes.byref(h)),
+        "dfa_create")
+    return h
+
+
+def dfa_create(table: np.ndarray, q0: int, accept_bitmap: np.ndarray) -> ctypes.c_void_p:
+    return dfa_create_ex(table, q0, accept_bitmap, 0)
+
+
+def dfa_destroy(h):
+    _ck(lib().dfa_destroy(h), "dfa_destroy")
+
+
+def dfa_get_info(h) -> dict:
+    info = DfaInfo()
+    _ck(lib().dfa_get_info(h, ctypes.byref(info)), "dfa_get_info")
+    d = {n: getattr(info, n) for n, _ in DfaInfo._fields_}
+    d["table_mode_name"] = TABLE_MODES.get(d["table_mode"], "?")
+    return d
+
+
+def dfa_domain(h, sigma: int) -> np.ndarray:
+    info = dfa_get_info(h)
+    out = np.zeros(max(info["i_max"], 1), np.uint16)
+    cnt = ctypes.c_uint32()
+    _ck(lib().dfa_domain(h, int(sigma), out.ctypes.data, ctypes.byref(cnt)), "dfa_domain")
+    return out[:cnt.value].copy()
+
+
+def dfa_set_chunk_ratio(h, c_num: int, c_den: int = 1):
+    _ck(lib().dfa_set_chunk_ratio(h, int(c_num), int(c_den)), "dfa_set_chunk_ratio")
+
+
+def dfa_plan_bounds(n: int, P: int, c_num: int, c_den: int = 1) -> np.ndarray:
+    out = np.zeros(P + 1, np.uint64)
+    _ck(lib().dfa_plan_bounds(int(n), int(P), int(c_num), int(c_den), out.ctypes.data), "dfa_plan_bounds")
+    return out
+
+
+def dfa_match(h, dev_input, n: Optional[int] = None, stream=None) -> Tuple[int, bool]:
+    n = dev_input.numel() if n is None else int(n)
+    fs = ctypes.c_uint16()
+    acc = ctypes.c_int()
+    _ck(lib().dfa_match(h, _ptr(dev_input), n, _stream(stream), ctypes.byref(fs), ctypes.byref(acc)),
+        "dfa_match")
+    return fs.value, bool(acc.value)
+
+
+def dfa_match_host(h, host_input, n: Optional[int] = None, stream=None) -> Tuple[int, bool]:
+    if isinstance(host_input, np.ndarray):
+        n = host_input.size if n is None else int(n)
+    else:
+        n = host_input.numel() if n is None else int(n)
+    fs = ctypes.c_uint16()
+    acc = ctypes.c_int()
+    _ck(lib().dfa_match_host(h, _ptr(host_input), n, _stream(stream), ctypes.byref(fs), ctypes.byref(acc)),
+        "dfa_match_host")
+    return fs.value, bool(acc.value)
+
+
+def dfa_chunk_maps(h, dev_input, P: int, dev_bounds, dev_chunk0_end, dev_maps, dev_chunk_start=None,
+                   dev_final=None, n: Optional[int] = None, stream=None):
+    n = dev_input.numel() if n is None else int(n)
+    _ck(lib().dfa_chunk_maps(h, _ptr(dev_input), n, int(P), _stream(stream), _ptr(dev_bounds),
+                             _ptr(dev_chunk0_end), _ptr(dev_maps), _ptr(dev_chunk_start), _ptr(dev_final)),
+        "dfa_chunk_maps")
+
+
+def dfa_chunk_maps_at(h, dev_input, P: int, dev_bounds_in, dev_chunk0_end, dev_maps, dev_chunk_start=None,
+                      dev_final=None, n: Optional[int] = None, stream=None):
+    n = dev_input.numel() if n is None else int(n)
+    _ck(lib().dfa_chunk_maps_at(h, _ptr(dev_input), n, int(P), _ptr(dev_bounds_in), _stream(stream),
+                                _ptr(dev_chunk0_end), _ptr(dev_maps), _ptr(dev_chunk_start), _ptr(dev_final)),
+        "dfa_chunk_maps_at")
+
+
+def dfa_get_last_device_error(h) -> int:
+    return int(lib().dfa_get_last_device_error(h))
+
+
+def dfa_set_option(h, key: int, value: int):
+    _ck(lib().dfa_set_option(h, int(key), int(value)), "dfa_set_option")
+
+
+def dfa_get_stats(h) -> dict:
+    s = DfaStats()
+    _ck(lib().dfa_get_stats(h, ctypes.byref(s)), "dfa_get_stats")
+    d = {"input_bytes": s.input_bytes, "num_subchunks": s.num_subchunks, "lanes_initial": s.lanes_initial,
+         "num_kernels": s.num_kernels, "profiled": bool(s.profiled)}
+    if s.profiled:
+        d["kernel_ms"] = {bytes(s.kernel_name[i]).split(b"\0")[0].decode(): s.kernel_ms[i]
+                          for i in range(8) if s.kernel_name[i][0]}
+    return d
+
+
+class Dfa:
+    """RAII wrapper: ``with Dfa(table, q0, bitmap) as d: d.match(x)``."""
+
+    def __init__(self, table, q0, accept_bitmap, flags: int = 0):
+        self.h = dfa_create_ex(table, q0, accept_bitmap, flags)
+        self.info = dfa_get_info(self.h)
+
+    def close(self):
+        if self.h is not None:
+            dfa_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def match(self, dev_input, stream=None):
+        return dfa_match(self.h, dev_input, stream=stream)
+
+    def domain(self, sigma: int):
+        return dfa_domain(self.h, sigma)
+
+    def chunk_maps(self, dev_input, P: int, with_starts: bool = False, stream=None):
+        """Allocate outputs with torch and return (bounds, e0, maps, starts, final) as torch tensors."""
+        import torch
+        dev = dev_input.device
+        imax = self.info["i_max"]
+        bounds = torch.empty(P + 1, dtype=torch.int64, device=dev)
+        e0 = torch.empty(1, dtype=torch.int16, device=dev)
+        maps = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=dev)
+        starts = torch.empty(P, dtype=torch.int16, device=dev) if with_starts else None
+        final = torch.empty(2, dtype=torch.int16, device=dev)
+        dfa_chunk_maps(self.h, dev_input, P, bounds, e0, maps, starts, final, stream=stream)
+        return bounds, e0, maps.view(max(P - 1, 1), imax)[:P - 1], starts, final

@@ -1,0 +1,608 @@
+// api.cpp -- the C ABI of include/dfa.h: handle, device tables, scratch,
+// launch orchestration.  See include/dfa.h for the contract.
+#include "../../include/dfa.h"
+#include "kernels.cuh"
+#include "prep.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace dfa;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) { cudaFree(p); p = nullptr; cap = 0; }
+        size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct HostPinned {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) { cudaFreeHost(p); p = nullptr; cap = 0; }
+        cudaError_t e = cudaMallocHost(&p, std::max<size_t>(bytes, 64));
+        if (e == cudaSuccess) cap = std::max<size_t>(bytes, 64);
+        return e;
+    }
+    void release() { if (p) cudaFreeHost(p); p = nullptr; cap = 0; }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+constexpr int kMaxProf = 8;
+
+} // namespace
+
+struct dfa_handle {
+    Prep prep;
+    bool device_ready = false;
+    int device = 0, sms = 0, optin_smem = 0;
+    DevBuf tables;
+    DevTables T{};
+    uint32_t c_num = 1, c_den = 1;
+    // options
+    int convergence = 1, profile = 0, threads = 512;
+    int64_t subchunk_target = 0;
+    // scratch
+    DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
+    DevBuf lvlA, lvlB, domA, domB, rep_rows, rep_dom, bounds, input;
+    HostPinned h_status, h_bounds;
+    cudaEvent_t staging_done = nullptr;
+    bool staging_pending = false;
+    cudaStream_t last_stream = nullptr;
+    // stats / profiling
+    dfa_stats stats{};
+    cudaEvent_t ev[2 * kMaxProf] = {};
+    int nprof = 0;
+};
+
+namespace {
+
+dfa_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return DFA_OK;
+    if (e == cudaErrorMemoryAllocation) return DFA_ERR_OOM;
+    return DFA_ERR_CUDA;
+}
+
+#define CK(expr)                                        \
+    do {                                                \
+        cudaError_t _e = (expr);                        \
+        if (_e != cudaSuccess) return cuda_status(_e);  \
+    } while (0)
+
+uint32_t gcd32(uint32_t a, uint32_t b) {
+    while (b) { uint32_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+// ----- device table upload --------------------------------------------------
+dfa_status upload(dfa_handle *h) {
+    Prep &p = h->prep;
+    CK(cudaGetDevice(&h->device));
+    CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device));
+    CK(cudaDeviceGetAttribute(&h->optin_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+
+    const uint32_t nq = p.nq, nc = p.nclass, imax = p.imax, imu = p.imax_user_stride;
+    std::vector<uint32_t> image = p.image;
+    while (image.size() % 4) image.push_back(0);
+    std::vector<uint16_t> dom_list((size_t)(nc + 1) * imax, kNone), dom_size(nc + 1, 0);
+    std::vector<uint16_t> rank((size_t)(nc + 1) * nq, kNone);
+    for (uint32_t c = 0; c <= nc; c++) {
+        dom_size[c] = (uint16_t)p.dom[c].size();
+        for (uint32_t j = 0; j < p.dom[c].size(); j++) {
+            dom_list[(size_t)c * imax + j] = p.dom[c][j];
+            rank[(size_t)c * nq + p.dom[c][j]] = (uint16_t)j;
+        }
+    }
+    std::vector<uint16_t> xlat((size_t)nc * imu, 0), dom_user_size(nc, 0);
+    for (uint32_t c = 0; c < nc; c++) {
+        dom_user_size[c] = (uint16_t)p.dom_user[c].size();
+        for (uint32_t j = 0; j < p.xlat[c].size(); j++) xlat[(size_t)c * imu + j] = p.xlat[c][j];
+    }
+    const uint32_t bw = ((nq + 31) / 32 + 3) & ~3u;
+    std::vector<uint32_t> dead(bw, 0), absorb(bw, 0), accept(bw, 0);
+    for (uint32_t q = 0; q < nq; q++) {
+        if (p.dead[q]) dead[q >> 5] |= 1u << (q & 31);
+        if (p.absorbing[q]) absorb[q >> 5] |= 1u << (q & 31);
+        if (p.accepting[q]) accept[q >> 5] |= 1u << (q & 31);
+    }
+    // one allocation, 256-byte aligned sections
+    struct Sec { const void *src; size_t bytes; size_t off; };
+    std::vector<Sec> secs = {
+        {image.data(), image.size() * 4, 0},
+        {p.full.data(), p.full.size() * 2, 0},
+        {p.byte_class.data(), 256, 0},
+        {dom_list.data(), dom_list.size() * 2, 0},
+        {dom_size.data(), dom_size.size() * 2, 0},
+        {rank.data(), rank.size() * 2, 0},
+        {dead.data(), dead.size() * 4, 0},
+        {absorb.data(), absorb.size() * 4, 0},
+        {accept.data(), accept.size() * 4, 0},
+        {xlat.data(), xlat.size() * 2, 0},
+        {dom_user_size.data(), dom_user_size.size() * 2, 0},
+    };
+    size_t total = 0;
+    for (auto &s : secs) { s.off = total; total += (s.bytes + 255) & ~size_t(255); }
+    CK(h->tables.ensure(total));
+    std::vector<uint8_t> blob(total, 0);
+    for (auto &s : secs) if (s.bytes) std::memcpy(blob.data() + s.off, s.src, s.bytes);
+    CK(cudaMemcpy(h->tables.p, blob.data(), total, cudaMemcpyHostToDevice));
+    auto at = [&](int i) { return reinterpret_cast<const uint8_t *>(h->tables.p) + secs[i].off; };
+    DevTables &T = h->T;
+    T.image = reinterpret_cast<const uint32_t *>(at(0));
+    T.image_words = p.mode == kGlobalU16 ? 0 : (uint32_t)image.size();
+    T.gtable = reinterpret_cast<const uint16_t *>(at(1));
+    T.byte_class = at(2);
+    T.dom_list = reinterpret_cast<const uint16_t *>(at(3));
+    T.dom_size = reinterpret_cast<const uint16_t *>(at(4));
+    T.rank = reinterpret_cast<const uint16_t *>(at(5));
+    T.dead_bits = reinterpret_cast<const uint32_t *>(at(6));
+    T.absorb_bits = reinterpret_cast<const uint32_t *>(at(7));
+    T.accept_bits = reinterpret_cast<const uint32_t *>(at(8));
+    T.xlat = reinterpret_cast<const uint16_t *>(at(9));
+    T.dom_user_size = reinterpret_cast<const uint16_t *>(at(10));
+    T.nq = nq;
+    T.nclass = nc;
+    T.start_dom = p.start_dom;
+    T.imax = imax;
+    T.imax_user = imu;
+    T.stride = p.stride;
+    T.win_base = p.win_base;
+    T.win_w = p.win_w;
+    T.mode = p.mode;
+    T.q0 = p.q0;
+    T.poison = p.poison == kNone ? 0xFFFFFFFFu : p.poison;
+    if ((int)(T.image_words * 4 + bw * 4) > h->optin_smem) return DFA_ERR_INTERNAL;
+    CK(setup_kernel_attributes(T));
+    CK(h->status.ensure(sizeof(DevStatus)));
+    CK(h->h_status.ensure(sizeof(DevStatus)));
+    CK(cudaEventCreateWithFlags(&h->staging_done, cudaEventDisableTiming));
+    for (int i = 0; i < 2 * kMaxProf; i++) CK(cudaEventCreate(&h->ev[i]));
+    h->device_ready = true;
+    return DFA_OK;
+}
+
+void prof_begin(dfa_handle *h, cudaStream_t s) {
+    if (h->profile && h->nprof < kMaxProf) cudaEventRecord(h->ev[2 * h->nprof], s);
+}
+void prof_end(dfa_handle *h, cudaStream_t s, const char *name) {
+    if (h->profile && h->nprof < kMaxProf) {
+        cudaEventRecord(h->ev[2 * h->nprof + 1], s);
+        std::snprintf(h->stats.kernel_name[h->nprof], 32, "%s", name);
+        h->nprof++;
+    }
+}
+
+uint32_t compose_group(const dfa_handle *h) {
+    const uint64_t room = (uint64_t)h->optin_smem - (uint64_t)h->T.imax * 2 - 64;
+    uint64_t G = 1 + room / ((uint64_t)h->T.nq * 2);
+    return (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(2, G));
+}
+
+struct Outputs {
+    uint16_t *chunk0_end = nullptr;  // [1]
+    uint16_t *user_maps = nullptr;   // [(P-1) * imax_user]
+    uint16_t *starts = nullptr;      // [P]
+    uint16_t *final2 = nullptr;      // [2]
+};
+
+// Sub-chunk counts per reporting chunk from the host copy of the bounds.
+void plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb, int threads, uint32_t &m0,
+                uint32_t &m) {
+    uint64_t target = h->subchunk_target;
+    if (target <= 0) {
+        int occ = std::max(1, lanes_occupancy(h->T, threads));
+        target = (uint64_t)h->sms * occ * threads;
+    }
+    const uint64_t Ls = std::max<uint64_t>(32, (n + target - 1) / target);
+    const uint64_t len0 = hb[1] - hb[0];
+    m0 = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (len0 + Ls / 2) / Ls), std::min<uint64_t>(len0, 1u << 30));
+    m = 1;
+    if (P > 1) {
+        uint64_t minlen = UINT64_MAX;
+        for (uint32_t k = 1; k < P; k++) minlen = std::min(minlen, hb[k + 1] - hb[k]);
+        const uint64_t avg = (n - len0) / (P - 1);
+        m = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (avg + Ls / 2) / Ls), minlen);
+    }
+}
+
+// Core: match `in` under the partition dev_bounds[P+1] (already on the device).
+dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const uint64_t *dev_bounds,
+               uint32_t m0, uint32_t m, cudaStream_t s, const Outputs &o) {
+    DevTables &T = h->T;
+    h->nprof = 0;
+    h->stats = dfa_stats{};
+    h->last_stream = s;
+    CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
+    Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds};
+    const uint64_t NS = plan.NS;
+    h->stats.input_bytes = n;
+    h->stats.num_subchunks = NS;
+
+    // stage A: lock-step convergence of large initial-state sets
+    const bool stageA = h->convergence && T.imax > (uint32_t)kLanes;
+    int wpc = 0;
+    if (stageA) {
+        for (int w = 16; w >= 1; w /= 2)
+            if (converge_smem_bytes(T, w) <= h->optin_smem) { wpc = w; break; }
+    }
+    const uint32_t sk = stageA && wpc ? (uint32_t)kLanes : std::max<uint32_t>(kLanes, (T.imax + 7) & ~7u);
+    CK(h->sfin.ensure(NS * sk * 2));
+    CK(h->dom_of.ensure(NS * 2));
+    const uint16_t *amap = nullptr, *surv = nullptr;
+    const uint8_t *surv_n = nullptr;
+    const uint64_t *surv_pos = nullptr;
+    int kernels = 0;
+    if (stageA && wpc) {
+        CK(h->surv.ensure(NS * kLanes * 2));
+        CK(h->surv_n.ensure(NS));
+        CK(h->surv_pos.ensure(NS * 8));
+        CK(h->amap.ensure(NS * T.imax * 2));
+        const int occ = std::max(1, converge_occupancy(T, wpc));
+        const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + wpc - 1) / wpc);
+        prof_begin(h, s);
+        CK(launch_converge(T, plan, in, h->surv.as<uint16_t>(), h->surv_n.as<uint8_t>(), h->surv_pos.as<uint64_t>(),
+                           h->amap.as<uint16_t>(), wpc, (int)grid, s));
+        prof_end(h, s, "converge");
+        kernels++;
+        amap = h->amap.as<uint16_t>();
+        surv = h->surv.as<uint16_t>();
+        surv_n = h->surv_n.as<uint8_t>();
+        surv_pos = h->surv_pos.as<uint64_t>();
+    }
+    {
+        const int threads = h->threads;
+        const int occ = std::max(1, lanes_occupancy(T, threads));
+        const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
+        prof_begin(h, s);
+        CK(launch_lanes(T, plan, in, surv, surv_n, surv_pos, h->sfin.as<uint16_t>(), sk, h->dom_of.as<uint16_t>(),
+                        h->convergence, threads, (int)grid, s));
+        prof_end(h, s, "lanes");
+        kernels++;
+    }
+    // composition: sub-chunk maps -> reporting maps -> final state
+    const uint32_t G = compose_group(h);
+    Shape sh{m0, P > 1 ? m : 0, P, G};
+    const uint64_t first_groups = sh.groups();
+    const uint64_t ping = std::max<uint64_t>(first_groups, (P + G - 1) / G) + 1;
+    CK(h->lvlA.ensure(ping * T.imax * 2));
+    CK(h->lvlB.ensure(ping * T.imax * 2));
+    CK(h->domA.ensure(ping * 2));
+    CK(h->domB.ensure(ping * 2));
+    CK(h->rep_rows.ensure((uint64_t)(P + 1) * T.imax * 2));
+    CK(h->rep_dom.ensure((uint64_t)(P + 1) * 2));
+    LevelIn lin{0, amap, h->sfin.as<uint16_t>(), sk, nullptr, nullptr, h->dom_of.as<uint16_t>()};
+    bool useA = true;
+    const int cgrid_cap = h->sms * 8;
+    prof_begin(h, s);
+    for (;;) {
+        const uint64_t gf = (sh.f + G - 1) / G, gm = sh.S > 1 ? (sh.m + G - 1) / G : 0;
+        const bool last = gf == 1 && (sh.S == 1 || gm == 1);
+        LevelOut out{};
+        if (last) {
+            out.row0 = h->rep_rows.as<uint16_t>();
+            out.rows = h->rep_rows.as<uint16_t>() + T.imax;
+            out.dom = h->rep_dom.as<uint16_t>();
+            out.user_rows = o.user_maps;
+            out.e0 = o.chunk0_end;
+        } else {
+            DevBuf &b = useA ? h->lvlA : h->lvlB;
+            DevBuf &d = useA ? h->domA : h->domB;
+            out.row0 = b.as<uint16_t>();
+            out.rows = b.as<uint16_t>() + T.imax;
+            out.dom = d.as<uint16_t>();
+            useA = !useA;
+        }
+        const uint64_t ng = sh.groups();
+        CK(launch_compose(T, lin, out, sh, h->status.as<DevStatus>(), (int)std::min<uint64_t>(ng, cgrid_cap), s));
+        kernels++;
+        lin = LevelIn{1, nullptr, nullptr, 0, out.row0, out.rows, out.dom};
+        sh = Shape{gf, gm, sh.S, G};
+        if (last) break;
+    }
+    const LevelIn rep = lin;
+    Shape fs{P, 0, 1, G};
+    while (fs.f > 1) {
+        DevBuf &b = useA ? h->lvlA : h->lvlB;
+        DevBuf &d = useA ? h->domA : h->domB;
+        useA = !useA;
+        LevelOut out{b.as<uint16_t>(), b.as<uint16_t>() + T.imax, d.as<uint16_t>(), nullptr, nullptr};
+        const uint64_t ng = fs.groups();
+        CK(launch_compose(T, lin, out, fs, h->status.as<DevStatus>(), (int)std::min<uint64_t>(ng, cgrid_cap), s));
+        kernels++;
+        lin = LevelIn{1, nullptr, nullptr, 0, out.row0, out.rows, out.dom};
+        fs = Shape{(fs.f + G - 1) / G, 0, 1, G};
+    }
+    CK(launch_finalize(T, lin.row0, h->status.as<DevStatus>(), o.final2, s));
+    kernels++;
+    prof_end(h, s, "compose+finalize");
+    if (o.starts) {
+        CK(launch_starts(T, plan, rep.row0, rep.rows, rep.dom, o.starts, h->status.as<DevStatus>(), s));
+        kernels++;
+    }
+    h->stats.num_kernels = kernels;
+    return DFA_OK;
+}
+
+dfa_status check_ready(dfa_handle *h) {
+    if (!h) return DFA_ERR_ARG;
+    if (!h->device_ready) return DFA_ERR_ARG;
+    return DFA_OK;
+}
+
+dfa_status stage_bounds(dfa_handle *h, uint64_t n, uint32_t P) {
+    if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
+    CK(h->h_bounds.ensure((size_t)(P + 1) * 8));
+    uint64_t *hb = h->h_bounds.as<uint64_t>();
+    for (uint32_t k = 0; k <= P; k++) hb[k] = cform_bound(n, P, h->c_num, h->c_den, k);
+    return DFA_OK;
+}
+
+dfa_status fetch_status(dfa_handle *h, cudaStream_t s, DevStatus &out) {
+    CK(cudaMemcpyAsync(h->h_status.p, h->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out = *h->h_status.as<DevStatus>();
+    return DFA_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char *dfa_status_string(dfa_status s) {
+    switch (s) {
+    case DFA_OK: return "ok";
+    case DFA_ERR_ARG: return "invalid argument";
+    case DFA_ERR_STATES: return "invalid states (|Q| == 0 or > 65000, q0 or a table entry >= |Q|)";
+    case DFA_ERR_ALPHABET: return "invalid alphabet size (must be 1..256)";
+    case DFA_ERR_CHUNKS: return "invalid chunk count or bounds (some chunk would be empty)";
+    case DFA_ERR_SYMBOL: return "input byte outside the alphabet";
+    case DFA_ERR_OOM: return "out of memory";
+    case DFA_ERR_CUDA: return "CUDA error";
+    case DFA_ERR_INTERNAL: return "internal consistency check failed";
+    }
+    return "unknown status";
+}
+
+dfa_status dfa_create_ex(const uint16_t *table, uint32_t num_states, uint32_t alphabet_size, uint16_t q0,
+                         const uint8_t *accept_bitmap, uint32_t flags, dfa_handle_t *out) {
+    if (!out) return DFA_ERR_ARG;
+    std::unique_ptr<dfa_handle> h(new (std::nothrow) dfa_handle());
+    if (!h) return DFA_ERR_OOM;
+    uint32_t budget = 200 * 1024;
+    if (!(flags & DFA_CREATE_HOST_ONLY)) {
+        int dev = 0, optin = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return DFA_ERR_CUDA;
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0)
+            budget = (uint32_t)optin - 24 * 1024;
+    }
+    int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, h->prep);
+    if (st != 0) return (dfa_status)st;
+    if (!(flags & DFA_CREATE_HOST_ONLY)) {
+        dfa_status ds = upload(h.get());
+        if (ds != DFA_OK) { dfa_destroy(h.release()); return ds; }
+    }
+    *out = h.release();
+    return DFA_OK;
+}
+
+dfa_status dfa_create(const uint16_t *table, uint32_t num_states, uint32_t alphabet_size, uint16_t q0,
+                      const uint8_t *accept_bitmap, dfa_handle_t *out) {
+    return dfa_create_ex(table, num_states, alphabet_size, q0, accept_bitmap, 0, out);
+}
+
+dfa_status dfa_destroy(dfa_handle_t h) {
+    if (!h) return DFA_ERR_ARG;
+    if (h->device_ready) {
+        if (h->last_stream) cudaStreamSynchronize(h->last_stream);
+        for (DevBuf *b : {&h->tables, &h->status, &h->sfin, &h->dom_of, &h->surv, &h->surv_n, &h->surv_pos,
+                          &h->amap, &h->lvlA, &h->lvlB, &h->domA, &h->domB, &h->rep_rows, &h->rep_dom,
+                          &h->bounds, &h->input})
+            b->release();
+        h->h_status.release();
+        h->h_bounds.release();
+        if (h->staging_done) cudaEventDestroy(h->staging_done);
+        for (auto &e : h->ev) if (e) cudaEventDestroy(e);
+    }
+    delete h;
+    return DFA_OK;
+}
+
+dfa_status dfa_get_info(dfa_handle_t h, dfa_info *out) {
+    if (!h || !out) return DFA_ERR_ARG;
+    const Prep &p = h->prep;
+    dfa_info i{};
+    i.num_states = p.nq_user;
+    i.alphabet_size = p.ns;
+    i.num_classes = p.nclass_user;
+    i.i_max = p.imax_user_stride;
+    uint32_t live = p.nq_user - p.num_dead_user;
+    uint32_t g = gcd32(p.imax_user, std::max<uint32_t>(live, 1));
+    i.gamma_num = p.imax_user / std::max<uint32_t>(g, 1);
+    i.gamma_den = std::max<uint32_t>(live, 1) / std::max<uint32_t>(g, 1);
+    i.num_dead = p.num_dead_user;
+    i.dead_state = p.first_dead_user;
+    i.num_absorbing = p.num_absorbing_user;
+    i.table_mode = (uint32_t)p.mode;
+    i.table_bytes = p.mode == kGlobalU16 ? 0 : (uint32_t)(p.image.size() * 4);
+    i.c_num = h->c_num;
+    i.c_den = h->c_den;
+    i.device_ready = h->device_ready ? 1 : 0;
+    *out = i;
+    return DFA_OK;
+}
+
+dfa_status dfa_domain(dfa_handle_t h, uint32_t sigma, uint16_t *out_states, uint32_t *out_count) {
+    if (!h || !out_count) return DFA_ERR_ARG;
+    if (sigma >= h->prep.ns) return DFA_ERR_SYMBOL;
+    const auto &d = h->prep.dom_user[h->prep.byte_class[sigma]];
+    if (out_states) std::copy(d.begin(), d.end(), out_states);
+    *out_count = (uint32_t)d.size();
+    return DFA_OK;
+}
+
+dfa_status dfa_set_chunk_ratio(dfa_handle_t h, uint32_t c_num, uint32_t c_den) {
+    if (!h || c_num == 0 || c_den == 0 || c_num > (1u << 20) || c_den > (1u << 20)) return DFA_ERR_ARG;
+    uint32_t g = gcd32(c_num, c_den);
+    h->c_num = c_num / g;
+    h->c_den = c_den / g;
+    return DFA_OK;
+}
+
+dfa_status dfa_plan_bounds(uint64_t n, uint32_t P, uint32_t c_num, uint32_t c_den, uint64_t *host_bounds) {
+    if (!host_bounds || P == 0 || c_num == 0 || c_den == 0) return DFA_ERR_ARG;
+    // every chunk non-empty iff n >= c + P - 1, i.e. n*b >= a + b(P-1)
+    if ((unsigned __int128)n * c_den < (unsigned __int128)c_num + (unsigned __int128)c_den * (P - 1))
+        return DFA_ERR_CHUNKS;
+    for (uint32_t k = 0; k <= P; k++) host_bounds[k] = cform_bound(n, P, c_num, c_den, k);
+    return DFA_OK;
+}
+
+dfa_status dfa_match(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, void *stream, uint16_t *final_state,
+                     int *accept) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    if (!final_state || !accept || (len && !dev_input)) return DFA_ERR_ARG;
+    if (len == 0) {
+        *final_state = h->prep.q0;
+        *accept = h->prep.accepting[h->prep.q0];
+        return DFA_OK;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
+    CK(h->h_bounds.ensure(16));
+    CK(h->bounds.ensure(16));
+    uint64_t *hb = h->h_bounds.as<uint64_t>();
+    hb[0] = 0;
+    hb[1] = len;
+    CK(cudaMemcpyAsync(h->bounds.p, hb, 16, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(h->staging_done, s));
+    h->staging_pending = true;
+    uint32_t m0, m;
+    plan_split(h, len, 1, hb, h->threads, m0, m);
+    Outputs o;
+    st = run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), m0, m, s, o);
+    if (st != DFA_OK) return st;
+    DevStatus ds;
+    st = fetch_status(h, s, ds);
+    if (st != DFA_OK) return st;
+    if (ds.err) return (dfa_status)ds.err;
+    *final_state = (uint16_t)ds.final_state;
+    *accept = (int)ds.accept;
+    return DFA_OK;
+}
+
+dfa_status dfa_match_host(dfa_handle_t h, const uint8_t *host_input, uint64_t len, void *stream,
+                          uint16_t *final_state, int *accept) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    if (!final_state || !accept || (len && !host_input)) return DFA_ERR_ARG;
+    if (len == 0) return dfa_match(h, nullptr, 0, stream, final_state, accept);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    CK(h->input.ensure(len));
+    CK(cudaMemcpyAsync(h->input.p, host_input, len, cudaMemcpyHostToDevice, s));
+    return dfa_match(h, h->input.as<uint8_t>(), len, stream, final_state, accept);
+}
+
+dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks, void *stream,
+                          uint64_t *dev_bounds, uint16_t *dev_chunk0_end, uint16_t *dev_maps,
+                          uint16_t *dev_chunk_start, uint16_t *dev_final) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    const uint32_t P = num_chunks;
+    if (P == 0) return DFA_ERR_CHUNKS;
+    if (!dev_input || !dev_bounds || !dev_chunk0_end || (P > 1 && !dev_maps)) return DFA_ERR_ARG;
+    if ((unsigned __int128)len * h->c_den < (unsigned __int128)h->c_num + (unsigned __int128)h->c_den * (P - 1))
+        return DFA_ERR_CHUNKS;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    st = stage_bounds(h, len, P);
+    if (st != DFA_OK) return st;
+    const uint64_t *hb = h->h_bounds.as<uint64_t>();
+    CK(cudaMemcpyAsync(dev_bounds, hb, (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(h->staging_done, s));
+    h->staging_pending = true;
+    uint32_t m0, m;
+    plan_split(h, len, P, hb, h->threads, m0, m);
+    Outputs o{dev_chunk0_end, P > 1 ? dev_maps : nullptr, dev_chunk_start, dev_final};
+    return run(h, dev_input, len, P, dev_bounds, m0, m, s, o);
+}
+
+dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
+                             const uint64_t *dev_bounds_in, void *stream, uint16_t *dev_chunk0_end,
+                             uint16_t *dev_maps, uint16_t *dev_chunk_start, uint16_t *dev_final) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    const uint32_t P = num_chunks;
+    if (P == 0 || len < P) return DFA_ERR_CHUNKS;
+    if (!dev_input || !dev_bounds_in || !dev_chunk0_end || (P > 1 && !dev_maps)) return DFA_ERR_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    std::vector<uint64_t> hb(P + 1);
+    CK(cudaMemcpyAsync(hb.data(), dev_bounds_in, (size_t)(P + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hb[0] != 0 || hb[P] != len) return DFA_ERR_CHUNKS;
+    for (uint32_t k = 0; k < P; k++)
+        if (hb[k + 1] <= hb[k]) return DFA_ERR_CHUNKS;
+    Outputs o{dev_chunk0_end, P > 1 ? dev_maps : nullptr, dev_chunk_start, dev_final};
+    return run(h, dev_input, len, P, dev_bounds_in, 1, 1, s, o);
+}
+
+dfa_status dfa_get_last_device_error(dfa_handle_t h) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    DevStatus ds;
+    st = fetch_status(h, h->last_stream, ds);
+    if (st != DFA_OK) return st;
+    return (dfa_status)ds.err;
+}
+
+dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
+    if (!h) return DFA_ERR_ARG;
+    switch (key) {
+    case DFA_OPT_SUBCHUNK_TARGET: if (value < 0) return DFA_ERR_ARG; h->subchunk_target = value; return DFA_OK;
+    case DFA_OPT_CONVERGENCE: h->convergence = value ? 1 : 0; return DFA_OK;
+    case DFA_OPT_PROFILE: h->profile = value ? 1 : 0; return DFA_OK;
+    case DFA_OPT_THREADS_PER_CTA:
+        if (value == 0) value = 512;
+        if (value < 32 || value > 512 || value % 32) return DFA_ERR_ARG;
+        h->threads = (int)value;
+        return DFA_OK;
+    }
+    return DFA_ERR_ARG;
+}
+
+dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out) {
+    if (!h || !out) return DFA_ERR_ARG;
+    dfa_stats s = h->stats;
+    if (h->device_ready && h->profile && h->nprof > 0) {
+        CK(cudaEventSynchronize(h->ev[2 * h->nprof - 1]));
+        for (int i = 0; i < h->nprof; i++) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]));
+            s.kernel_ms[i] = ms;
+            std::snprintf(s.kernel_name[i], 32, "%s", h->stats.kernel_name[i]);
+        }
+        s.profiled = 1;
+    }
+    *out = s;
+    return DFA_OK;
+}
+
+} // extern "C"

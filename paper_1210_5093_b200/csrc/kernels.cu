@@ -1,0 +1,690 @@
+// kernels.cu -- sm_100a kernels of the speculative chunked DFA membership test.
+//
+// Paper: Ko, Jung, Han, Burgstaller, arXiv:1210.5093.  The paper's
+// kernels are a scalar C loop (Listing Cmatching) and an 8-way
+// AVX2 gather loop (Listing AVX2matching) over a flattened table
+// (SBase, Fig.SBaseExample).  Here the same transition step
+// s <- delta(s, x[i]) is a shared-memory gather (LDS) per lane; a warp issues
+// 32 of them per instruction where AVX2 issued 8.  No tensor cores: the path
+// is a dependent gather chain, not a contraction.
+#include "kernels.cuh"
+#include "prep.h"
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dfa {
+
+namespace {
+
+constexpr uint32_t kDone = 0xFFu;
+
+__device__ __forceinline__ bool test_bit(const uint32_t *bits, uint32_t q) {
+    return (bits[q >> 5] >> (q & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint4 ldg16(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+// Execution sub-chunk i -> [start, end): reporting chunk k is [b_k, b_{k+1})
+// (Eq.StartPosition/EndPosition, half-open, reading R5), split into m_k equal
+// parts (m_0 = m0, m_k = m for k >= 1).
+__device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s, uint64_t &e) {
+    uint64_t k, j, mk;
+    if (i < p.m0) { k = 0; j = i; mk = p.m0; }
+    else { uint64_t t = i - p.m0; k = 1 + t / p.m; j = t % p.m; mk = p.m; }
+    uint64_t b0 = p.bounds[k], b1 = p.bounds[k + 1], len = b1 - b0;
+    s = b0 + len * j / mk;
+    e = b0 + len * (j + 1) / mk;
+}
+
+// Reverse lookahead: the domain of sub-chunk i is I_sigma with
+// sigma the byte before it; the very first sub-chunk starts from {q0}.
+__device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const uint8_t *in, uint64_t i,
+                                               uint64_t start) {
+    return i == 0 ? T.start_dom : (uint32_t)T.byte_class[__ldg(in + start - 1)];
+}
+
+// ---------------------------------------------------------------------------
+// Transition step per table layout.  wprep: per 32-bit input word (window
+// modes map 4 bytes to 4 columns with two SIMD ops); bprep: per byte, shared
+// by all lanes of a thread; look: per lane, one shared-memory load.
+// ---------------------------------------------------------------------------
+template <int MODE>
+struct Tab {
+    const uint8_t *t8;
+    const uint16_t *t16;
+    const uint32_t *t32;
+    const uint16_t *g;
+    uint32_t stride, base4, w4, base, w;
+    uint32_t tb;      // shared-space address of the table
+    uint32_t rowb;    // bytes per table row
+    // IdentU8: the table sits at a 256-aligned shared address A = bias*256 and
+    // holds encoded states s + bias, so the shared address of entry (s, b) is
+    // exactly (s_enc << 8) | b -- one PRMT builds it from the state and the
+    // input word ("we only add the current state's offset to the
+    // current input symbol"), with no base add.  Other modes: bias = 0 and
+    // one IMAD per lane (state * row bytes + per-byte column address).
+    uint32_t bias;
+
+    struct Pre { uint32_t a, sh; };
+
+    __device__ __forceinline__ void init(const DevTables &T, const void *table_smem) {
+        t8 = reinterpret_cast<const uint8_t *>(table_smem);
+        t16 = reinterpret_cast<const uint16_t *>(table_smem);
+        t32 = reinterpret_cast<const uint32_t *>(table_smem);
+        g = T.gtable;
+        stride = T.stride;
+        base = T.win_base;
+        w = T.win_w;
+        base4 = T.win_base * 0x01010101u;
+        w4 = T.win_w * 0x01010101u;
+        tb = (uint32_t)__cvta_generic_to_shared(table_smem);
+        bias = MODE == kIdentU8 ? (tb >> 8) : 0u;
+        rowb = MODE == kIdentU16 ? 512u : MODE == kWindowU8 ? T.stride : MODE == kWindowU16 ? 2u * T.stride
+             : MODE == kPacked9 ? 4u * T.stride : 0u;
+    }
+    __device__ __forceinline__ uint32_t enc(uint32_t s) const { return s + bias; }
+    __device__ __forceinline__ uint32_t dec(uint32_t s) const { return s - bias; }
+    __device__ __forceinline__ static uint32_t lds_u8(uint32_t addr) {
+        uint32_t r;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(addr));
+        return r;
+    }
+    __device__ __forceinline__ static uint32_t lds_u16(uint32_t addr) {
+        uint32_t r;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r) : "r"(addr));
+        return r;
+    }
+    __device__ __forceinline__ static uint32_t lds_u32(uint32_t addr) {
+        uint32_t r;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+        return r;
+    }
+    __device__ __forceinline__ uint32_t wprep(uint32_t x) const {
+        if constexpr (MODE == kWindowU8 || MODE == kWindowU16) return __vminu4(__vsub4(x, base4), w4);
+        else return x;
+    }
+    // per input byte, shared by all lanes of the thread: the column's address
+    __device__ __forceinline__ Pre bprep(uint32_t x, int k) const {
+        const uint32_t c = (x >> (8 * k)) & 0xFFu;
+        if constexpr (MODE == kIdentU16) return {tb + 2u * c, 0u};
+        else if constexpr (MODE == kWindowU8) return {tb + c, 0u};
+        else if constexpr (MODE == kWindowU16) return {tb + 2u * c, 0u};
+        else if constexpr (MODE == kPacked9) {
+            const uint32_t wc = (c * 171u) >> 9;  // c / 3 for c < 256
+            return {tb + 4u * wc, (c - 3u * wc) * 9u};
+        } else return {c, 0u};
+    }
+    __device__ __forceinline__ uint32_t look(uint32_t s, uint32_t x, int k, Pre p) const {
+        if constexpr (MODE == kIdentU8) return lds_u8(__byte_perm(x, s, 0x6540 + k));
+        else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
+        else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
+        else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
+        else return __ldg(g + (s << 8) + p.a);
+    }
+    // scalar step on an encoded state and a raw byte
+    __device__ __forceinline__ uint32_t look_byte(uint32_t s, uint32_t b) const {
+        if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | b);
+        else if constexpr (MODE == kIdentU16) return t16[(s << 8) | b];
+        else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
+            uint32_t c = min((b - base) & 0xFFu, w);
+            if constexpr (MODE == kWindowU8) return t8[s * stride + c];
+            else return t16[s * stride + c];
+        } else if constexpr (MODE == kPacked9) {
+            return (t32[s * stride + b / 3u] >> ((b % 3u) * 9u)) & 511u;
+        } else return __ldg(g + (s << 8) + b);
+    }
+};
+
+// Shared-memory layout: [pad to a 256-aligned shared address][table image]
+// [absorbing-state bitmap][kernel scratch].  Returns the table pointer.
+// IdentU8 entries are stored biased by the table's shared address >> 8.
+template <int MODE>
+__device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem, uint32_t bits_words_n) {
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
+    uint8_t *tab = reinterpret_cast<uint8_t *>(smem) + (((sb + 255u) & ~255u) - sb);
+    const uint32_t bias4 = MODE == kIdentU8 ? (((sb + 255u) & ~255u) >> 8) * 0x01010101u : 0u;
+    const uint4 *src = reinterpret_cast<const uint4 *>(T.image);
+    uint4 *dst = reinterpret_cast<uint4 *>(tab);
+    for (uint32_t i = threadIdx.x; i < T.image_words / 4; i += blockDim.x) {
+        uint4 v = __ldg(src + i);
+        if (MODE == kIdentU8) {
+            v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4);
+            v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
+        }
+        dst[i] = v;
+    }
+    uint32_t *w = reinterpret_cast<uint32_t *>(tab) + T.image_words;
+    for (uint32_t i = threadIdx.x; i < bits_words_n; i += blockDim.x) w[i] = __ldg(T.absorb_bits + i);
+    return tab;
+}
+
+__device__ __forceinline__ uint32_t bits_words(uint32_t nq) { return ((nq + 31) / 32 + 3) & ~3u; }
+
+// ---------------------------------------------------------------------------
+// lanes_kernel: one thread per execution sub-chunk, <= kLanes lanes in registers.
+// ---------------------------------------------------------------------------
+template <int B, int MODE>
+__device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t (&st)[kLanes]) {
+    const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int wi = 0; wi < 4; wi++) {
+        uint32_t x = tab.wprep(wds[wi]);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const typename Tab<MODE>::Pre c = tab.bprep(x, k);
+#pragma unroll
+            for (int l = 0; l < B; l++) st[l] = tab.look(st[l], x, k, c);
+        }
+    }
+}
+
+// A lane whose slot is `slot` finished: write its final state for every
+// original lane it carries (own[r] == slot).
+__device__ __forceinline__ void finish_slot(uint32_t slot, uint32_t state, uint32_t (&own)[kLanes],
+                                            uint16_t *out) {
+#pragma unroll
+    for (int r = 0; r < kLanes; r++)
+        if (own[r] == slot) { out[r] = (uint16_t)state; own[r] = kDone; }
+}
+
+// Merge converged lanes, retire absorbing ones, compact.
+__device__ __forceinline__ void checkpoint(const uint32_t *absorb, uint32_t bias, uint32_t (&st)[kLanes],
+                                           uint32_t (&own)[kLanes], uint32_t &nlive, uint16_t *out) {
+    const uint32_t full = (1u << nlive) - 1u;
+    uint32_t lm = full;
+    if (nlive == 1) {
+        if (test_bit(absorb, st[0] - bias)) { finish_slot(0, st[0] - bias, own, out); lm = 0; }
+    } else {
+#pragma unroll
+        for (int l = 0; l < kLanes; l++)
+            if (((lm >> l) & 1u) && test_bit(absorb, st[l] - bias)) {
+                finish_slot(l, st[l] - bias, own, out);
+                lm &= ~(1u << l);
+            }
+#pragma unroll
+        for (int a = 0; a < kLanes - 1; a++)
+#pragma unroll
+            for (int b = a + 1; b < kLanes; b++)
+                if (((lm >> a) & (lm >> b) & 1u) && st[a] == st[b]) {
+                    lm &= ~(1u << b);
+#pragma unroll
+                    for (int r = 0; r < kLanes; r++)
+                        if (own[r] == (uint32_t)b) own[r] = a;
+                }
+    }
+    if (lm == full) return;
+    uint32_t pc[kLanes];
+#pragma unroll
+    for (int s = 0; s < kLanes; s++) pc[s] = __popc(lm & ((1u << s) - 1u));
+    // ns[t] = st[s] for the live slot s of rank t (branch-free masks keep
+    // everything in registers: no dynamically indexed array)
+    uint32_t ns[kLanes];
+#pragma unroll
+    for (int t = 0; t < kLanes; t++) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int s = t; s < kLanes; s++) {
+            const uint32_t hit = 0u - (uint32_t)((((lm >> s) & 1u) != 0) & (pc[s] == (uint32_t)t));
+            v |= st[s] & hit;
+        }
+        ns[t] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < kLanes; t++) st[t] = ns[t];
+#pragma unroll
+    for (int r = 0; r < kLanes; r++)
+        if (own[r] != kDone) own[r] = __popc(lm & ((1u << own[r]) - 1u));
+    nlive = __popc(lm);
+}
+
+template <int MODE>
+__device__ __forceinline__ void step_scalar(const Tab<MODE> &tab, uint32_t b, uint32_t (&st)[kLanes],
+                                            uint32_t nlive) {
+#pragma unroll
+    for (int l = 0; l < kLanes; l++)
+        if ((uint32_t)l < nlive) st[l] = tab.look_byte(st[l], b);
+}
+
+template <int MODE>
+__device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *absorb, const uint8_t *in, uint64_t pos,
+                          uint64_t end, uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t nl,
+                          int convergence, uint16_t *out) {
+    uint32_t nlive = nl;
+    const uint8_t *ptr = in + pos;
+    const uint8_t *endp = in + end;
+    // head: up to 15 bytes until 16-byte alignment
+    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 15u)) step_scalar(tab, *ptr++, st, nlive);
+    uint64_t nblk = (uint64_t)(endp - ptr) >> 4;
+    const uint4 *q = reinterpret_cast<const uint4 *>(ptr);
+    if (nblk) {
+        uint4 cur = ldg16(q);
+        for (uint64_t bi = 0; bi < nblk; bi++) {
+            uint4 nxt = cur;
+            if (bi + 1 < nblk) nxt = ldg16(q + bi + 1);
+            uint32_t bucket = __reduce_max_sync(__activemask(), nlive);
+            if (bucket <= 1) block16<1>(tab, cur, st);
+            else if (bucket <= 2) block16<2>(tab, cur, st);
+            else if (bucket <= 4) block16<4>(tab, cur, st);
+            else block16<8>(tab, cur, st);
+            if (convergence) {
+                checkpoint(absorb, tab.bias, st, own, nlive, out);
+                if (nlive == 0) return;
+            }
+            cur = nxt;
+        }
+        ptr += nblk * 16;
+    }
+    while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
+    // remaining lanes: final state of the slot that carries them
+#pragma unroll
+    for (int r = 0; r < kLanes; r++) {
+        if ((uint32_t)r >= nl || own[r] == kDone) continue;
+        uint32_t v = 0;
+#pragma unroll
+        for (int l = 0; l < kLanes; l++) v |= st[l] & (0u - (uint32_t)(own[r] == (uint32_t)l));
+        out[r] = (uint16_t)(v - tab.bias);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
+                                                    const uint16_t *__restrict__ surv,
+                                                    const uint8_t *__restrict__ surv_n,
+                                                    const uint64_t *__restrict__ surv_pos,
+                                                    uint16_t *__restrict__ sfin, uint32_t sk,
+                                                    uint16_t *__restrict__ dom_of, int convergence) {
+    extern __shared__ uint4 smem4[];
+    uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
+    __syncthreads();
+    Tab<MODE> tab;
+    tab.init(T, tsm);
+    const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + T.image_words;
+
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t start, end;
+        sub_range(p, i, start, end);
+        const uint32_t dom = sub_domain(T, in, i, start);
+        dom_of[i] = (uint16_t)dom;
+        uint32_t u;
+        uint64_t pos;
+        if (surv) { u = surv_n[i]; pos = surv_pos[i]; }
+        else { u = T.dom_size[dom]; pos = start; }
+        for (uint32_t pass = 0; pass * kLanes < u; pass++) {
+            const uint32_t nl = min((uint32_t)kLanes, u - pass * kLanes);
+            uint32_t st[kLanes], own[kLanes];
+#pragma unroll
+            for (int l = 0; l < kLanes; l++) {
+                const uint32_t r = pass * kLanes + l;
+                if ((uint32_t)l < nl) {
+                    st[l] = tab.enc(surv ? surv[i * kLanes + r] : T.dom_list[(uint64_t)dom * T.imax + r]);
+                    own[l] = l;
+                } else {
+                    st[l] = tab.enc(0);
+                    own[l] = kDone;
+                }
+            }
+            run_lanes<MODE>(tab, absorb, in, pos, end, st, own, nl, convergence,
+                            sfin + i * sk + pass * kLanes);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// converge_kernel: one warp per sub-chunk, all |I_sigma| lanes in lock-step
+// (the lanes of Alg.MatchingInitialStates line 17 for one chunk), merging
+// lanes that reach equal states every kSubWindow bytes until <= kLanes remain.
+// Output: survivors (states + start position for lanes_kernel) and amap[i][j]
+// = final state of lane j, or kSurvBase + survivor index.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t scratch_u16(const DevTables &T) {
+    return (4 * T.imax + T.nq + 7) & ~7u;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
+                                                       uint16_t *__restrict__ surv, uint8_t *__restrict__ surv_n,
+                                                       uint64_t *__restrict__ surv_pos,
+                                                       uint16_t *__restrict__ amap) {
+    extern __shared__ uint4 smem4[];
+    const uint32_t bw = bits_words(T.nq);
+    uint8_t *tsm = load_tables<MODE>(T, smem4, bw);
+    Tab<MODE> tab;
+    tab.init(T, tsm);
+    const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + T.image_words;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint16_t *scr = reinterpret_cast<uint16_t *>(reinterpret_cast<uint32_t *>(tsm) + T.image_words + bw) +
+                    (size_t)warp * scratch_u16(T);
+    uint16_t *pool_s = scr, *pool_id = scr + T.imax, *parent = scr + 2 * T.imax, *res = scr + 3 * T.imax;
+    uint16_t *first = scr + 4 * T.imax;
+    for (uint32_t q = lane; q < T.nq; q += 32) first[q] = kNone;
+    __syncthreads();
+
+    const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; i < p.NS; i += warps_total) {
+        uint64_t start, end;
+        sub_range(p, i, start, end);
+        const uint32_t dom = sub_domain(T, in, i, start);
+        const uint32_t u = T.dom_size[dom];
+        for (uint32_t e = lane; e < u; e += 32) {
+            pool_s[e] = T.dom_list[(uint64_t)dom * T.imax + e];
+            pool_id[e] = (uint16_t)e;
+            parent[e] = (uint16_t)e;
+            res[e] = kNone;
+        }
+        uint32_t np = u;
+        uint64_t pos = start;
+        __syncwarp();
+        while (np > (uint32_t)kLanes && pos < end) {
+            // one window: the bytes [pos, min(next 16-byte boundary, end))
+            const uint64_t abase = pos & ~15ull;
+            const uint32_t k0 = (uint32_t)(pos - abase);
+            const uint32_t k1 = (uint32_t)(end - abase < 16 ? end - abase : 16);
+            uint4 v;
+            if (abase + 16 <= p.n) {
+                v = ldg16(reinterpret_cast<const uint4 *>(in + abase));
+            } else {  // last partial block of the input: byte loads, never past n
+                uint32_t wv[4] = {0, 0, 0, 0};
+                for (uint32_t k = k0; k < k1; k++) wv[k >> 2] |= (uint32_t)__ldg(in + abase + k) << (8 * (k & 3));
+                v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+            for (uint32_t base = 0; base < np; base += 32 * kConvergeLA) {
+                uint32_t s[kConvergeLA];
+#pragma unroll
+                for (int l = 0; l < kConvergeLA; l++) {
+                    const uint32_t e = base + lane + 32 * l;
+                    s[l] = tab.enc(e < np ? pool_s[e] : 0);
+                }
+                for (uint32_t k = k0; k < k1; k++) {
+                    const uint32_t wsel = k >> 2;
+                    const uint32_t word = wsel == 0 ? v.x : wsel == 1 ? v.y : wsel == 2 ? v.z : v.w;
+                    const uint32_t b = (word >> (8 * (k & 3))) & 0xFFu;
+#pragma unroll
+                    for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_byte(s[l], b);
+                }
+#pragma unroll
+                for (int l = 0; l < kConvergeLA; l++) {
+                    const uint32_t e = base + lane + 32 * l;
+                    if (e < np) pool_s[e] = (uint16_t)tab.dec(s[l]);
+                }
+            }
+            pos = abase + k1;
+            __syncwarp();
+            // merge lanes with equal states (leader = first in pool order),
+            // retire lanes in absorbing states, compact the pool in place.
+            uint32_t np_new = 0;
+            for (uint32_t row = 0; row * 32 < np; row++) {
+                const uint32_t e = row * 32 + lane;
+                const bool valid = e < np;
+                const uint32_t s = valid ? pool_s[e] : 0;
+                const uint32_t id = valid ? pool_id[e] : 0;
+                const bool absorbed = valid && test_bit(absorb, s);
+                const bool live = valid && !absorbed;
+                const uint32_t key = live ? s : (0x10000u | lane);
+                const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                const uint32_t leader_lane = __ffs(peers) - 1;
+                const uint32_t lid = __shfl_sync(0xffffffffu, id, leader_lane);
+                const uint32_t f = live ? first[s] : kNone;
+                __syncwarp();
+                const bool new_leader = live && f == kNone && lane == leader_lane;
+                if (new_leader) first[s] = (uint16_t)id;
+                if (live && !new_leader) parent[id] = (uint16_t)(f != kNone ? f : lid);
+                if (absorbed) res[id] = (uint16_t)s;
+                const uint32_t mask = __ballot_sync(0xffffffffu, new_leader);
+                if (new_leader) {
+                    const uint32_t off = np_new + __popc(mask & ((1u << lane) - 1u));
+                    pool_s[off] = (uint16_t)s;
+                    pool_id[off] = (uint16_t)id;
+                }
+                np_new += __popc(mask);
+                __syncwarp();
+            }
+            for (uint32_t e = lane; e < np_new; e += 32) first[pool_s[e]] = kNone;
+            np = np_new;
+            __syncwarp();
+        }
+        if (pos < end) {
+            for (uint32_t e = lane; e < np; e += 32) {
+                res[pool_id[e]] = (uint16_t)(kSurvBase + e);
+                surv[i * kLanes + e] = pool_s[e];
+            }
+            if (lane == 0) { surv_n[i] = (uint8_t)np; surv_pos[i] = pos; }
+        } else {
+            for (uint32_t e = lane; e < np; e += 32) res[pool_id[e]] = pool_s[e];
+            if (lane == 0) { surv_n[i] = 0; surv_pos[i] = end; }
+        }
+        __syncwarp();
+        for (uint32_t j = lane; j < u; j += 32) {
+            uint32_t r = j;
+            while (parent[r] != r) r = parent[r];
+            amap[i * T.imax + j] = res[r];
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// compose_kernel: one CTA per group of <= G consecutive maps.  Maps 2..cnt of
+// the group are expanded to dense maps over Q in shared memory
+// (dense[q] = L[rank(q)], error states map to themselves), then every entry
+// of the first map is pushed through them: Eq.MapReduction
+// L_{i,j}[q] = L_j[L_i[q]] applied cnt-1 times.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t level_entry(const LevelIn &in, const DevTables &T, uint64_t i, uint32_t r) {
+    if (in.kind == 0) {
+        if (in.amap) {
+            const uint32_t a = in.amap[i * T.imax + r];
+            return a < kSurvBase ? a : in.sfin[i * in.sk + (a - kSurvBase)];
+        }
+        return in.sfin[i * in.sk + r];
+    }
+    const uint16_t *row = i == 0 ? in.row0 : in.rows + (i - 1) * T.imax;
+    return row[r];
+}
+
+__device__ __forceinline__ void group_range(const Shape &sh, uint64_t g, uint64_t &st, uint64_t &en) {
+    const uint64_t gf = (sh.f + sh.G - 1) / sh.G;
+    if (g < gf) { st = g * sh.G; en = min(sh.f, st + sh.G); return; }
+    const uint64_t gm = (sh.m + sh.G - 1) / sh.G;
+    const uint64_t t = g - gf, seg = t / gm, r = t % gm;
+    const uint64_t base = sh.f + seg * sh.m;
+    st = base + r * sh.G;
+    en = min(base + sh.m, st + sh.G);
+}
+
+__global__ void __launch_bounds__(256) compose_kernel(DevTables T, LevelIn in, LevelOut out, Shape sh,
+                                                      DevStatus *status) {
+    extern __shared__ uint4 smem4[];
+    uint16_t *dense = reinterpret_cast<uint16_t *>(smem4);
+    const uint64_t ngroups = sh.groups();
+    for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        uint64_t st, en;
+        group_range(sh, g, st, en);
+        const uint32_t cnt = (uint32_t)(en - st);
+        uint16_t *rowbuf = dense + (size_t)(sh.G - 1) * T.nq;
+        const uint32_t total = (cnt - 1) * T.nq;
+        for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+            const uint32_t c = t / T.nq, q = t - c * T.nq;
+            const uint64_t i = st + 1 + c;
+            uint32_t v;
+            if (test_bit(T.dead_bits, q)) v = q;
+            else {
+                const uint32_t d = in.dom[i];
+                const uint32_t r = T.rank[(uint64_t)d * T.nq + q];
+                v = r == kNone ? kNone : level_entry(in, T, i, r);
+            }
+            dense[t] = (uint16_t)v;
+        }
+        __syncthreads();
+        const uint32_t d0 = in.dom[st];
+        const uint32_t u = T.dom_size[d0];
+        for (uint32_t j = threadIdx.x; j < T.imax; j += blockDim.x) {
+            uint32_t s = kNone;
+            if (j < u) {
+                s = level_entry(in, T, st, j);
+                for (uint32_t c = 0; c + 1 < cnt; c++) {
+                    const uint32_t s2 = dense[(size_t)c * T.nq + s];
+                    if (s2 == kNone) { atomicMax(&status->err, 8u); s = 0; break; }
+                    s = s2;
+                }
+            }
+            rowbuf[j] = (uint16_t)s;
+            uint16_t *orow = g == 0 ? out.row0 : out.rows + (g - 1) * T.imax;
+            orow[j] = (uint16_t)s;
+        }
+        if (threadIdx.x == 0) out.dom[g] = (uint16_t)d0;
+        __syncthreads();
+        if (out.user_rows && g > 0) {
+            // API row in the user's I_sigma order (reading R1): drop internal-only states
+            const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : 0;
+            uint16_t *urow = out.user_rows + (g - 1) * T.imax_user;
+            for (uint32_t j = threadIdx.x; j < T.imax_user; j += blockDim.x)
+                urow[j] = j < du ? rowbuf[T.xlat[(uint64_t)d0 * T.imax_user + j]] : kNone;
+        }
+        if (out.e0 && g == 0 && threadIdx.x == 0) out.e0[0] = rowbuf[0];
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// finalize_kernel: Alg.seqmatch lines 4-6 on the composed state.
+// ---------------------------------------------------------------------------
+__global__ void finalize_kernel(DevTables T, const uint16_t *final_row, DevStatus *status, uint16_t *dev_final) {
+    if (threadIdx.x != 0) return;
+    const uint32_t s = final_row[0];
+    uint32_t err = status->err;
+    if (s == T.poison) err = max(err, 5u);
+    status->final_state = s;
+    status->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
+    status->err = err;
+    if (dev_final) {
+        dev_final[0] = (uint16_t)s;
+        dev_final[1] = (uint16_t)status->accept;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// starts_kernel (optional output): true initial state of every reporting
+// chunk, the prefix of Eq.SeqReduction.  One thread, P dependent steps.
+// ---------------------------------------------------------------------------
+__global__ void starts_kernel(DevTables T, Plan p, const uint16_t *row0, const uint16_t *rows, const uint16_t *dom,
+                              uint16_t *starts, DevStatus *status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    starts[0] = (uint16_t)T.q0;
+    if (p.P < 2) return;
+    uint32_t s = row0[0];
+    for (uint32_t k = 1; k < p.P; k++) {
+        starts[k] = (uint16_t)s;
+        if (test_bit(T.dead_bits, s)) continue;
+        const uint32_t r = T.rank[(uint64_t)dom[k] * T.nq + s];
+        if (r == kNone) { atomicMax(&status->err, 8u); return; }
+        s = rows[(uint64_t)(k - 1) * T.imax + r];
+    }
+}
+
+template <int MODE>
+void *lanes_ptr() { return (void *)lanes_kernel<MODE>; }
+template <int MODE>
+void *converge_ptr() { return (void *)converge_kernel<MODE>; }
+
+void *lanes_fn(int mode) {
+    switch (mode) {
+    case kIdentU8: return lanes_ptr<kIdentU8>();
+    case kIdentU16: return lanes_ptr<kIdentU16>();
+    case kWindowU8: return lanes_ptr<kWindowU8>();
+    case kWindowU16: return lanes_ptr<kWindowU16>();
+    case kPacked9: return lanes_ptr<kPacked9>();
+    default: return lanes_ptr<kGlobalU16>();
+    }
+}
+void *converge_fn(int mode) {
+    switch (mode) {
+    case kIdentU8: return converge_ptr<kIdentU8>();
+    case kIdentU16: return converge_ptr<kIdentU16>();
+    case kWindowU8: return converge_ptr<kWindowU8>();
+    case kWindowU16: return converge_ptr<kWindowU16>();
+    case kPacked9: return converge_ptr<kPacked9>();
+    default: return converge_ptr<kGlobalU16>();
+    }
+}
+
+int bits_words_host(uint32_t nq) { return (int)((((nq + 31) / 32) + 3) & ~3u); }
+
+} // namespace
+
+int lanes_smem_bytes(const DevTables &T) { return (int)(256 + T.image_words * 4 + bits_words_host(T.nq) * 4); }
+
+int converge_smem_bytes(const DevTables &T, int warps_per_cta) {
+    const uint32_t scr = (4 * T.imax + T.nq + 7) & ~7u;
+    return lanes_smem_bytes(T) + warps_per_cta * (int)scr * 2;
+}
+
+int compose_smem_bytes(const DevTables &T, uint32_t G) {
+    return (int)(((size_t)(G - 1) * T.nq + T.imax) * 2 + 16);
+}
+
+cudaError_t setup_kernel_attributes(const DevTables &T) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaError_t e = cudaFuncSetAttribute(lanes_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute((void *)compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+}
+
+int lanes_occupancy(const DevTables &T, int threads) {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lanes_fn(T.mode), threads, lanes_smem_bytes(T));
+    return blocks;
+}
+
+int converge_occupancy(const DevTables &T, int warps_per_cta) {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, converge_fn(T.mode), warps_per_cta * 32,
+                                                  converge_smem_bytes(T, warps_per_cta));
+    return blocks;
+}
+
+cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in, uint16_t *surv, uint8_t *surv_n,
+                            uint64_t *surv_pos, uint16_t *amap, int warps_per_cta, int grid, cudaStream_t s) {
+    void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
+                    (void *)&amap};
+    return cudaLaunchKernel(converge_fn(T.mode), dim3(grid), dim3(warps_per_cta * 32), args,
+                            converge_smem_bytes(T, warps_per_cta), s);
+}
+
+cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
+                         const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
+                         uint16_t *dom_of, int convergence, int threads, int grid, cudaStream_t s) {
+    void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
+                    (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence};
+    return cudaLaunchKernel(lanes_fn(T.mode), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
+}
+
+cudaError_t launch_compose(const DevTables &T, const LevelIn &in, const LevelOut &out, const Shape &sh,
+                           DevStatus *st, int grid, cudaStream_t s) {
+    compose_kernel<<<grid, 256, compose_smem_bytes(T, sh.G), s>>>(T, in, out, sh, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const DevTables &T, const uint16_t *final_row, DevStatus *st, uint16_t *dev_final,
+                            cudaStream_t s) {
+    finalize_kernel<<<1, 32, 0, s>>>(T, final_row, st, dev_final);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
+                          const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s) {
+    starts_kernel<<<1, 32, 0, s>>>(T, p, row0, rows, dom, starts, st);
+    return cudaGetLastError();
+}
+
+} // namespace dfa

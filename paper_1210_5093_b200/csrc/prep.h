@@ -1,0 +1,74 @@
+// prep.h -- host preprocessing of a DFA for the B200 matching path.
+//
+// Everything here runs once per DFA at dfa_create (the paper computes I_max
+// "online for every matching run" but notes it is a static property that can
+// be computed offline).  Product code: shares nothing with
+// oracle/.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dfa {
+
+constexpr uint16_t kNone = 0xFFFF;     // "no state" / map padding (reading R6)
+constexpr uint16_t kSurvBase = 0xFF00; // amap code: survivor index (internal)
+constexpr uint32_t kMaxStates = 65000; // leaves room for kSurvBase codes
+
+enum TableMode : int {
+    kIdentU8 = 1,   // smem, row = 256 byte columns, uint8 entries
+    kIdentU16 = 2,  // smem, row = 256 byte columns, uint16 entries
+    kWindowU8 = 3,  // smem, row = W window columns + 1 default column, uint8
+    kWindowU16 = 4, // same, uint16
+    kPacked9 = 5,   // smem, 256 columns of 9-bit states, 3 per 32-bit word
+    kGlobalU16 = 6  // global memory [nq][256] uint16 through the read-only path
+};
+
+struct Prep {
+    // user view
+    uint32_t nq_user = 0, ns = 0;
+    uint16_t q0 = 0;
+    // internal automaton: user states + (if ns < 256) one poison state that
+    // absorbs every byte >= ns (reading R12: bad symbols are detected without a
+    // per-byte check).  Internal table is byte-indexed over all 256 bytes.
+    uint32_t nq = 0;
+    uint16_t poison = kNone;
+    std::vector<uint16_t> full;      // [nq][256]
+    std::vector<uint8_t> accepting;  // [nq]
+    std::vector<uint8_t> dead;       // [nq] internal Z: absorbing over all 256 bytes, not accepting
+    std::vector<uint8_t> dead_user;  // [nq] user Z over Sigma (reading R1); == dead if no poison
+    std::vector<uint8_t> absorbing;  // [nq] delta(q,.) == q
+    // column classes over the 256 bytes (north_star "byte-class alphabet compression")
+    std::vector<uint8_t> byte_class; // [256]
+    std::vector<uint16_t> class_rep; // representative byte per class
+    uint32_t nclass = 0;
+    uint32_t start_dom = 0;          // domain id of the {q0} domain = nclass
+    // initial-state sets I_sigma = delta(Q, sigma) \ Z per class, ascending
+    // (Eq.istates P:946-951 with Alg.MatchingInitialStates line 5).
+    // dom_user uses the user's Z (what the API reports); dom uses the internal
+    // Z, a superset when a poison state exists (user error states must keep
+    // being tracked, since a later byte >= |Sigma| still leaves them).
+    std::vector<std::vector<uint16_t>> dom;      // [nclass + 1], last = {q0}
+    std::vector<std::vector<uint16_t>> dom_user; // [nclass]
+    std::vector<std::vector<uint16_t>> xlat;     // [nclass]: dom_user[c][j] == dom[c][xlat[c][j]]
+    uint32_t imax_user = 0;          // Eq.MaxIstates over valid symbols
+    uint32_t imax = 1;               // internal row stride (>= 1)
+    uint32_t imax_user_stride = 1;   // max(1, imax_user): API map row stride
+    uint32_t num_dead_user = 0, num_absorbing_user = 0;
+    uint16_t first_dead_user = kNone;
+    uint32_t nclass_user = 0;        // classes containing a valid symbol
+    // device table layout
+    int mode = 0;
+    uint32_t stride = 0;             // entries per row (u8/u16) or words per row (packed9)
+    uint32_t win_base = 0, win_w = 0;
+    std::vector<uint32_t> image;     // smem image (32-bit words), empty for global
+};
+
+// Validates and analyses; returns 0 or a dfa_status code.
+int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
+            const uint8_t *accept_bitmap, uint32_t smem_budget, Prep &out);
+
+// Exact c-form partition (header dfa.h), 128-bit integer arithmetic.
+uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uint32_t k);
+
+} // namespace dfa

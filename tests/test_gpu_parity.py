@@ -1,0 +1,320 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the CPU oracle,
+element by element, on the same seeded inputs.  Bit-exact: every value here is
+an integer (state ids, offsets, accept bits)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from workloads import automata, inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1210_5093_b200 as D  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def u16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+class Case:
+    def __init__(self, aut, x, name=""):
+        self.a = aut
+        self.x = np.ascontiguousarray(x, dtype=np.uint8)
+        self.od = oracle.Dfa(aut.table, aut.q0, aut.accepting)
+        self.name = name
+
+    def handle(self, **opts):
+        d = D.Dfa(self.a.table, self.a.q0, self.a.accept_bitmap)
+        for k, v in opts.items():
+            D.dfa_set_option(d.h, k, v)
+        return d
+
+
+def check_chunk_maps(c: Case, P: int, c_num=1, c_den=1, opts=None, dev=None, maps_rows=None):
+    """Full parity of bounds, e0, every map entry, true chunk starts, final, accept."""
+    d = c.handle(**(opts or {}))
+    try:
+        D.dfa_set_chunk_ratio(d.h, c_num, c_den)
+        x = c.x
+        dx = dev if dev is not None else torch.from_numpy(x).to(DEV)
+        bounds, e0, maps, starts, final = d.chunk_maps(dx, P, with_starts=True)
+        torch.cuda.synchronize()
+        assert D.dfa_get_last_device_error(d.h) == 0
+        ob = oracle.chunk_bounds_ratio(x.size, P, c_num, c_den)
+        assert np.array_equal(bounds.cpu().numpy().astype(np.uint64), ob), "bounds"
+        imax = d.info["i_max"]
+        ost, ofin = c.od.run_record(x, ob[:-1])
+        assert u16(final)[0] == ofin and u16(final)[1] == int(c.a.accepting[ofin]), "final/accept"
+        assert np.array_equal(u16(starts), ost), "chunk starts"
+        gm = u16(maps)
+        if maps_rows is None:
+            oe0, omaps = c.od.maps(x, ob, imax)
+            assert u16(e0)[0] == oe0, "e0"
+            if P > 1:
+                bad = np.argwhere(gm != omaps)
+                assert bad.size == 0, f"{len(bad)} map entries differ, first {bad[:3].tolist()}"
+        else:  # sampled rows at full size
+            for k in maps_rows:
+                row, _ = c.od.chunk_map(x, int(ob[k]), int(ob[k + 1]), imax)
+                assert np.array_equal(gm[k - 1], row), f"map row {k}"
+        return d.info
+    finally:
+        d.close()
+
+
+def check_match(c: Case, opts=None):
+    d = c.handle(**(opts or {}))
+    try:
+        fin, acc = d.match(torch.from_numpy(c.x).to(DEV))
+        ofin = c.od.run(c.x)
+        assert (fin, acc) == (ofin, bool(c.a.accepting[ofin]))
+    finally:
+        d.close()
+
+
+# ------------------------------------------------------------------ the five configs (small sizes)
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_config_small_full_parity(name):
+    w = W.get(name)
+    x = w.input(w.small_n)
+    c = Case(w.automaton, x, name)
+    P = min(w.chunks, max(1, x.size // 64))
+    check_chunk_maps(c, P)
+    check_match(c)
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_config_small_convergence_off(name):
+    w = W.get(name)
+    x = w.input(min(w.small_n, 1 << 20))
+    c = Case(w.automaton, x, name)
+    check_chunk_maps(c, 257, opts={D.DFA_OPT_CONVERGENCE: 0})
+
+
+def test_tiny_hard():
+    """P = 65,536 chunks of 16 symbols over the 1 MiB Tiny input (c = 1)."""
+    w = W.get("tiny")
+    c = Case(w.automaton, w.input(), "tiny-hard")
+    check_chunk_maps(c, 65536)
+
+
+@pytest.mark.parametrize("cn,cd", [(1, 1), (3, 1), (7, 2), (240, 1)])
+def test_chunk_ratio_c(cn, cd):
+    w = W.get("random")
+    c = Case(w.automaton, w.input(1 << 20), "random")
+    check_chunk_maps(c, 300, cn, cd)
+
+
+@pytest.mark.parametrize("target", [1, 7, 1000, 1 << 22])
+def test_subchunk_targets(target):
+    """The internal execution split must not change any result."""
+    w = W.get("keyword")
+    c = Case(w.automaton, w.input(1 << 20), "keyword")
+    check_chunk_maps(c, 129, opts={D.DFA_OPT_SUBCHUNK_TARGET: target})
+    w = W.get("worst")
+    c = Case(w.automaton, w.input(1 << 18), "worst")
+    check_chunk_maps(c, 33, opts={D.DFA_OPT_SUBCHUNK_TARGET: target})
+
+
+# ------------------------------------------------------------------ closed forms, special DFAs
+def test_counter_dfa_no_convergence():
+    a = automata.counter_dfa(37)
+    x = inputs.uniform_bytes(3 << 20, seed=4)
+    c = Case(a, x, "counter")
+    check_chunk_maps(c, 1000)
+    check_match(c)
+    d = c.handle()
+    fin, _ = d.match(torch.from_numpy(x).to(DEV))
+    assert fin == int(x.astype(np.int64).sum()) % 37
+    d.close()
+
+
+def test_reset_identity_permutation():
+    rng = np.random.default_rng(2)
+    f = rng.integers(0, 50, 256)
+    for a in (automata.reset_dfa(50, f), automata.identity_dfa(11),
+              automata.permutation_dfa(300, 256, 1), automata.permutation_dfa(20, 256, 2)):
+        x = inputs.uniform_bytes(1 << 19, seed=5)
+        c = Case(a, x, a.name)
+        check_chunk_maps(c, 77)
+        check_match(c)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_random_dfas(seed):
+    rng = np.random.default_rng(100 + seed)
+    nq = int(rng.choice([2, 5, 17, 64, 200, 255, 256, 257, 400, 511, 700, 1500]))
+    ns = int(rng.choice([1, 2, 4, 20, 100, 255, 256]))
+    kind = seed % 3
+    if kind == 0:
+        a = automata.random_dfa(nq, ns, seed)
+    elif kind == 1:
+        a = automata.random_dfa_with_sink(max(nq, 3), ns, seed, float(rng.uniform(0.05, 0.9)))
+    else:
+        a = automata.random_structured(max(nq, 8), ns, int(rng.integers(1, min(max(nq, 8), 300))),
+                                       max(1, nq // 4), seed)
+    n = int(rng.integers(1, 1 << 19))
+    x = rng.integers(0, ns, n).astype(np.uint8)
+    c = Case(a, x, f"fuzz{seed}")
+    P = int(rng.integers(1, max(2, min(n, 3000))))
+    check_chunk_maps(c, P)
+    check_match(c)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_arbitrary_partitions(seed):
+    """Fold invariant for any partition (dfa_chunk_maps_at), incl. very uneven ones."""
+    rng = np.random.default_rng(seed)
+    w = W.get(["random", "keyword", "protein", "worst", "tiny", "random"][seed])
+    n = 1 << 17
+    x = w.input(n)
+    c = Case(w.automaton, x, w.name)
+    P = int(rng.integers(2, 400))
+    cuts = np.sort(rng.choice(np.arange(1, n), P - 1, replace=False))
+    if seed % 2:
+        cuts = np.unique(np.concatenate([cuts[:P // 2], np.arange(1, min(P // 2, 50) + 1)]))
+        P = cuts.size + 1
+    ob = np.concatenate([[0], cuts, [n]]).astype(np.uint64)
+    d = c.handle()
+    try:
+        imax = d.info["i_max"]
+        dx = torch.from_numpy(x).to(DEV)
+        db = torch.from_numpy(ob.astype(np.int64)).to(DEV)
+        e0 = torch.empty(1, dtype=torch.int16, device=DEV)
+        maps = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=DEV)
+        starts = torch.empty(P, dtype=torch.int16, device=DEV)
+        final = torch.empty(2, dtype=torch.int16, device=DEV)
+        D.dfa_chunk_maps_at(d.h, dx, P, db, e0, maps, starts, final)
+        torch.cuda.synchronize()
+        oe0, omaps = c.od.maps(x, ob, imax)
+        ost, ofin = c.od.run_record(x, ob[:-1])
+        assert u16(e0)[0] == oe0
+        assert np.array_equal(u16(maps).reshape(-1, imax)[:P - 1], omaps)
+        assert np.array_equal(u16(starts), ost)
+        assert u16(final)[0] == ofin
+    finally:
+        d.close()
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_lengths_and_chunk_counts():
+    a = W.get("keyword").automaton
+    for n in (1, 2, 15, 16, 17, 31, 33, 255, 4097):
+        x = W.get("keyword").input(n)
+        c = Case(a, x)
+        check_match(c)
+        check_chunk_maps(c, 1)
+        check_chunk_maps(c, n)              # n == c + P - 1 with c = 1: every chunk one byte
+        if n >= 3:
+            check_chunk_maps(c, n - 2, 3, 1)
+
+
+def test_empty_input_and_errors():
+    a = W.get("tiny").automaton
+    d = D.Dfa(a.table, a.q0, a.accept_bitmap)
+    try:
+        empty = torch.empty(0, dtype=torch.uint8, device=DEV)
+        assert d.match(empty) == (a.q0, bool(a.accepting[a.q0]))
+        x = torch.from_numpy(np.array([0, 1, 2, 3] * 100, np.uint8)).to(DEV)
+        with pytest.raises(D.DfaError) as e:  # n < c + P - 1
+            d.chunk_maps(x, 401)
+        assert e.value.status == D.DFA_ERR_CHUNKS
+        bad = np.array([0, 1, 2] * 1000 + [7] + [1] * 5000, np.uint8)  # byte 7 >= |Sigma| = 4
+        with pytest.raises(D.DfaError) as e:
+            d.match(torch.from_numpy(bad).to(DEV))
+        assert e.value.status == D.DFA_ERR_SYMBOL
+        d.chunk_maps(torch.from_numpy(bad).to(DEV), 100)
+        torch.cuda.synchronize()
+        assert D.dfa_get_last_device_error(d.h) == D.DFA_ERR_SYMBOL
+        # handle still usable afterwards
+        good = np.array([0, 1, 2, 0] * 50, np.uint8)
+        assert d.match(torch.from_numpy(good).to(DEV))[0] == oracle.Dfa(a.table, a.q0, a.accepting).run(good)
+    finally:
+        d.close()
+
+
+def test_error_state_paper_example(golden_dir):
+    """Fig.ExampleDFA: the run enters q_E inside C_0; maps are all q_E (reading R1)."""
+    import json, os
+    g = json.load(open(os.path.join(golden_dir, "fig_example_dfa.json")))
+    table = np.full((5, 2), 4, np.uint16)
+    for s, lab, t in g["triples"]:
+        table[s, g["symbols"][lab]] = t
+    a = automata.Automaton(table, 0, np.arange(5) == 3)
+    x = np.array([g["symbols"][ch] for ch in g["input"]], np.uint8)
+    c = Case(a, x)
+    info = check_chunk_maps(c, 3, 2, 1)  # c = I_max = 2: Fig.InputString
+    assert info["i_max"] == 2
+    big = np.tile(x, 5000)
+    check_chunk_maps(Case(a, big), 999)
+
+
+def test_match_host_equals_match():
+    w = W.get("random")
+    x = w.input(1 << 22)
+    d = D.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accept_bitmap)
+    try:
+        pinned = torch.from_numpy(x).pin_memory()
+        assert D.dfa_match_host(d.h, pinned) == d.match(pinned.to(DEV))
+        assert D.dfa_match_host(d.h, x) == d.match(pinned.to(DEV))
+    finally:
+        d.close()
+
+
+def test_streams_and_repeat_determinism():
+    w = W.get("protein")
+    x = w.input(1 << 21)
+    c = Case(w.automaton, x)
+    d = c.handle()
+    try:
+        s = torch.cuda.Stream()
+        dx = torch.from_numpy(x).to(DEV)
+        with torch.cuda.stream(s):
+            r1 = d.match(dx, stream=s)
+        r2 = d.match(dx)
+        assert r1 == r2 == (c.od.run(x), bool(c.a.accepting[c.od.run(x)]))
+    finally:
+        d.close()
+
+
+# ------------------------------------------------------------------ full sizes (sampled)
+def full_size(name, rows=4, seed=0):
+    w = W.get(name, seed)
+    x = w.input()
+    c = Case(w.automaton, x, name)
+    dx = torch.from_numpy(x).to(DEV)
+    rng = np.random.default_rng(1)
+    P = w.chunks
+    rows_ = sorted(set([1, P - 1] + rng.integers(1, P, rows).tolist()))
+    check_chunk_maps(c, P, dev=dx, maps_rows=rows_)
+    d = c.handle()
+    try:
+        fin, acc = d.match(dx)
+        assert fin == c.od.run(x)
+    finally:
+        d.close()
+
+
+def test_full_random():
+    full_size("random")
+
+
+def test_full_keyword():
+    full_size("keyword")
+
+
+@pytest.mark.slow
+def test_full_protein():
+    full_size("protein", rows=2)
+
+
+@pytest.mark.slow
+def test_full_worst():
+    full_size("worst", rows=2)
