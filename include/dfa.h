@@ -200,6 +200,10 @@ dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out);
 
 const char *dfa_status_string(dfa_status s);
 
+/* Human-readable detail (CUDA error name, call site) of the last DFA_ERR_CUDA /
+ * DFA_ERR_OOM returned on the calling thread; "" if none. */
+const char *dfa_error_detail(void);
+
 #ifdef __cplusplus
 }
 #endif

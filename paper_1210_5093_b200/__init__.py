@@ -21,7 +21,7 @@ __all__ = [
     "DfaError", "dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
     "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
     "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
-    "dfa_status_string", "Dfa", "lib", "EXPORTED",
+    "dfa_status_string", "dfa_error_detail", "Dfa", "lib", "EXPORTED",
 ]
 
 DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
@@ -47,14 +47,15 @@ class DfaStats(ctypes.Structure):
 class DfaError(RuntimeError):
     def __init__(self, status: int, what: str = ""):
         self.status = status
-        super().__init__(f"{what}: {dfa_status_string(status)} ({status})")
+        detail = dfa_error_detail() if status in (DFA_ERR_CUDA, DFA_ERR_OOM) else ""
+        super().__init__(f"{what}: {dfa_status_string(status)} ({status}) {detail}".rstrip())
 
 
 # every function declared in include/dfa.h
 EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
             "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
             "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
-            "dfa_status_string"]
+            "dfa_status_string", "dfa_error_detail"]
 
 _lib = None
 
@@ -90,8 +91,14 @@ def lib():
             f.restype = i32
         L.dfa_status_string.argtypes = [i32]
         L.dfa_status_string.restype = ctypes.c_char_p
+        L.dfa_error_detail.argtypes = []
+        L.dfa_error_detail.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def dfa_error_detail() -> str:
+    return lib().dfa_error_detail().decode()
 
 
 def dfa_status_string(status: int) -> str:

@@ -82,10 +82,18 @@ dfa_status cuda_status(cudaError_t e) {
     return DFA_ERR_CUDA;
 }
 
-#define CK(expr)                                        \
-    do {                                                \
-        cudaError_t _e = (expr);                        \
-        if (_e != cudaSuccess) return cuda_status(_e);  \
+thread_local char g_detail[256] = "";
+
+dfa_status cuda_fail(cudaError_t e, const char *expr, int line) {
+    std::snprintf(g_detail, sizeof g_detail, "%s (%s) at api.cpp:%d: %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e), line, expr);
+    return cuda_status(e);
+}
+
+#define CK(expr)                                                         \
+    do {                                                                 \
+        cudaError_t _e = (expr);                                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr, __LINE__);    \
     } while (0)
 
 uint32_t gcd32(uint32_t a, uint32_t b) {
@@ -177,6 +185,17 @@ dfa_status upload(dfa_handle *h) {
     CK(cudaEventCreateWithFlags(&h->staging_done, cudaEventDisableTiming));
     for (int i = 0; i < 2 * kMaxProf; i++) CK(cudaEventCreate(&h->ev[i]));
     h->device_ready = true;
+    return DFA_OK;
+}
+
+// IdentU8 needs (encoded state) << 8 | byte to be the entry's shared address,
+// so |Q| + (table address >> 8) <= 256: measure where dynamic smem starts.
+dfa_status probe(dfa_handle *h, uint32_t &u8_limit) {
+    CK(h->status.ensure(sizeof(DevStatus)));
+    int base = probe_dynamic_smem_base(h->status.as<uint32_t>());
+    if (base < 0) return cuda_fail(cudaGetLastError(), "probe_dynamic_smem_base", __LINE__);
+    const uint32_t bias = (((uint32_t)base + 255u) & ~255u) >> 8;
+    u8_limit = bias >= 256 ? 0 : 256 - bias;
     return DFA_OK;
 }
 
@@ -367,6 +386,8 @@ dfa_status fetch_status(dfa_handle *h, cudaStream_t s, DevStatus &out) {
 
 extern "C" {
 
+const char *dfa_error_detail(void) { return g_detail; }
+
 const char *dfa_status_string(dfa_status s) {
     switch (s) {
     case DFA_OK: return "ok";
@@ -388,13 +409,16 @@ dfa_status dfa_create_ex(const uint16_t *table, uint32_t num_states, uint32_t al
     std::unique_ptr<dfa_handle> h(new (std::nothrow) dfa_handle());
     if (!h) return DFA_ERR_OOM;
     uint32_t budget = 200 * 1024;
+    uint32_t u8_limit = 256 - 4;  // dynamic smem starts at shared address 0x400 on sm_100
     if (!(flags & DFA_CREATE_HOST_ONLY)) {
         int dev = 0, optin = 0;
         if (cudaGetDevice(&dev) != cudaSuccess) return DFA_ERR_CUDA;
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0)
             budget = (uint32_t)optin - 24 * 1024;
+        dfa_status ps = probe(h.get(), u8_limit);
+        if (ps != DFA_OK) return ps;
     }
-    int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, h->prep);
+    int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, u8_limit, h->prep);
     if (st != 0) return (dfa_status)st;
     if (!(flags & DFA_CREATE_HOST_ONLY)) {
         dfa_status ds = upload(h.get());
@@ -501,7 +525,7 @@ dfa_status dfa_match(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, voi
     Outputs o;
     st = run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), m0, m, s, o);
     if (st != DFA_OK) return st;
-    DevStatus ds;
+    DevStatus ds{};
     st = fetch_status(h, s, ds);
     if (st != DFA_OK) return st;
     if (ds.err) return (dfa_status)ds.err;
@@ -567,7 +591,7 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
 dfa_status dfa_get_last_device_error(dfa_handle_t h) {
     dfa_status st = check_ready(h);
     if (st != DFA_OK) return st;
-    DevStatus ds;
+    DevStatus ds{};
     st = fetch_status(h, h->last_stream, ds);
     if (st != DFA_OK) return st;
     return (dfa_status)ds.err;

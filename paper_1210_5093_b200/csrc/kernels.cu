@@ -227,13 +227,14 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, uint32_t bias
     uint32_t ns[kLanes];
 #pragma unroll
     for (int t = 0; t < kLanes; t++) {
-        uint32_t v = 0;
+        uint32_t v = 0, any = 0;
 #pragma unroll
         for (int s = t; s < kLanes; s++) {
             const uint32_t hit = 0u - (uint32_t)((((lm >> s) & 1u) != 0) & (pc[s] == (uint32_t)t));
             v |= st[s] & hit;
+            any |= hit;
         }
-        ns[t] = v;
+        ns[t] = v | (bias & ~any);  // unused slots keep a valid (encoded) state id
     }
 #pragma unroll
     for (int t = 0; t < kLanes; t++) st[t] = ns[t];
@@ -617,6 +618,20 @@ void *converge_fn(int mode) {
 int bits_words_host(uint32_t nq) { return (int)((((nq + 31) / 32) + 3) & ~3u); }
 
 } // namespace
+
+__global__ void probe_smem_kernel(uint32_t *out) {
+    extern __shared__ uint4 smem4[];
+    if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(smem4);
+}
+
+// Shared-space address at which dynamic shared memory starts (the IdentU8
+// table bias of Tab<kIdentU8> is that address rounded up to 256, >> 8).
+int probe_dynamic_smem_base(uint32_t *dev_scratch) {
+    probe_smem_kernel<<<1, 32, 256>>>(dev_scratch);
+    uint32_t v = 0;
+    if (cudaMemcpy(&v, dev_scratch, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return (int)v;
+}
 
 int lanes_smem_bytes(const DevTables &T) { return (int)(256 + T.image_words * 4 + bits_words_host(T.nq) * 4); }
 

@@ -106,5 +106,6 @@ cudaError_t launch_finalize(const DevTables &T, const uint16_t *final_row, DevSt
 cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s);
 cudaError_t setup_kernel_attributes(const DevTables &T);
+int probe_dynamic_smem_base(uint32_t *dev_scratch);
 
 } // namespace dfa

@@ -40,7 +40,7 @@ uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uin
 }
 
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
-            const uint8_t *accept_bitmap, uint32_t smem_budget, Prep &p) {
+            const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &p) {
     if (!table || !accept_bitmap) return ST_ARG;
     if (ns == 0 || ns > 256) return ST_ALPHABET;
     if (nq == 0 || nq > kMaxStates || q0 >= nq) return ST_STATES;
@@ -155,7 +155,7 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
         if (!(w & 1)) w++;
         return w;
     };
-    if (p.nq <= 256) {
+    if (p.nq <= u8_state_limit) {
         p.mode = kIdentU8;
         p.stride = 256;
     } else if (W && (size_t)p.nq * window_words_u16(W + 1) * 4 <= smem_budget) {

@@ -30,16 +30,16 @@ class Case:
         self.od = oracle.Dfa(aut.table, aut.q0, aut.accepting)
         self.name = name
 
-    def handle(self, **opts):
+    def handle(self, opts=None):
         d = D.Dfa(self.a.table, self.a.q0, self.a.accept_bitmap)
-        for k, v in opts.items():
+        for k, v in (opts or {}).items():
             D.dfa_set_option(d.h, k, v)
         return d
 
 
 def check_chunk_maps(c: Case, P: int, c_num=1, c_den=1, opts=None, dev=None, maps_rows=None):
     """Full parity of bounds, e0, every map entry, true chunk starts, final, accept."""
-    d = c.handle(**(opts or {}))
+    d = c.handle(opts)
     try:
         D.dfa_set_chunk_ratio(d.h, c_num, c_den)
         x = c.x
@@ -70,7 +70,7 @@ def check_chunk_maps(c: Case, P: int, c_num=1, c_den=1, opts=None, dev=None, map
 
 
 def check_match(c: Case, opts=None):
-    d = c.handle(**(opts or {}))
+    d = c.handle(opts)
     try:
         fin, acc = d.match(torch.from_numpy(c.x).to(DEV))
         ofin = c.od.run(c.x)
