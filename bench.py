@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""bench.py -- matched input GB/s of the speculative chunked DFA membership
+test (arXiv:1210.5093) on B200, and its roofline fraction.
+
+One step = one full pass of the hot path
+over the workload's input: dfa_chunk_maps with P reporting chunks, i.e. the
+partition, per-chunk initial-state sets, the match kernels, every chunk map,
+their composition into the final state and its accept bit.  The input is
+resident in HBM before timing starts and is larger than L2 (no flush needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config random]
+  python bench.py --impl reference ...     # the CPU oracle (Alg. 1) on host cores
+
+N > 1 (torchrun, one rank per GPU): weak scaling -- rank r holds segment r of
+an N-segment input, computes its segment map over the initial-state set of the
+previous segment's last byte (one halo byte), and the G segment maps are
+all-gathered over NCCL and folded into the replicated final state
+(the on-NVLink form of the paper's two-tier merge, Fig.Merge).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "matched input GB/s on 1 B200; achieved fraction of HBM/smem-lookup roofline"
+UNIT = "GB/s"
+BASELINE_WORKLOAD = {"random": "configs[1] Random structured DFA |Q|=64, |Sigma|=256, images of size 7, "
+                               "256 MiB uniform bytes, 4096 chunks"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", default="random", choices=list(W.CONFIGS))
+    ap.add_argument("--chunks", type=int, default=0, help="reporting chunks P (0 = config default)")
+    ap.add_argument("--n", type=int, default=0, help="input bytes per GPU (0 = config full size)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--convergence", type=int, default=1)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "MEASURED_PEAKS.json hbm_gbs (copy)"
+    return 6650.0, 1965.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.1)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_lookups(x: np.ndarray, bounds: np.ndarray, dom_size: np.ndarray) -> int:
+    """L_alg = len_0 + sum_{k>=1} len_k * |I_sigma_k|."""
+    b = bounds.astype(np.int64)
+    lens = np.diff(b)
+    sig = x[b[1:-1] - 1]
+    return int(lens[0] + (lens[1:] * dom_size[sig].astype(np.int64)).sum())
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle's Alg. 1 (oracle_run) on one host core, as it stands."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = W.get(args.config, args.seed)
+    n = args.n or w.full_n
+    sample = min(n, 64 << 20)  # bounded sample per step: the first 64 MiB of the workload input
+    x = w.input(sample)
+    a = w.automaton
+    od = oracle.Dfa(a.table, a.q0, a.accepting)
+    for _ in range(args.warmup):
+        od.run(x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        od.run(x)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = sample / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": BASELINE_WORKLOAD.get(args.config, args.config), "bytes_per_step": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"oracle_run (Alg.1, one core) over the first {sample >> 20} MiB "
+                                       f"of the {args.config} input per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import paper_1210_5093_b200 as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    w = W.get(args.config, args.seed)
+    a = w.automaton
+    n = args.n or w.full_n
+    P = args.chunks or w.chunks
+    x = w.input(n) if rank == 0 else W.CONFIGS[args.config](args.seed + rank).input(n)
+    dx = torch.from_numpy(x).to(dev)
+
+    d = D.Dfa(a.table, a.q0, a.accept_bitmap)
+    D.dfa_set_option(d.h, D.DFA_OPT_CONVERGENCE, args.convergence)
+    imax = d.info["i_max"]
+    bounds = torch.empty(P + 1, dtype=torch.int64, device=dev)
+    e0 = torch.empty(1, dtype=torch.int16, device=dev)
+    maps = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=dev)
+    final = torch.empty(2, dtype=torch.int16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    seg = None
+    if world > 1:
+        from paper_1210_5093_b200 import multi_gpu
+        seg = multi_gpu.SegmentMatcher(d, dx, rank, world, dist)
+
+    def step():
+        D.dfa_chunk_maps(d.h, dx, P, bounds, e0, maps, None, final, stream=stream)
+        if seg is not None:
+            seg.step(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    D.dfa_set_option(d.h, D.DFA_OPT_PROFILE, 1)
+    D.dfa_get_stats(d.h)  # reset accumulators
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    stats = D.dfa_get_stats(d.h)
+    D.dfa_set_option(d.h, D.DFA_OPT_PROFILE, 0)
+    ms = t0.elapsed_time(t1) / args.steps
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n / (ms * 1e-3) / 1e9
+    if D.dfa_get_last_device_error(d.h) != 0:
+        raise SystemExit("device error during bench")
+
+    # end to end through the public API from pinned host memory (H2D + match + D2H of the result)
+    xp = torch.from_numpy(x).pin_memory()
+    for _ in range(2):
+        D.dfa_match_host(d.h, xp, stream=stream)
+    torch.cuda.synchronize(dev)
+    e_0 = torch.cuda.Event(enable_timing=True)
+    e_1 = torch.cuda.Event(enable_timing=True)
+    e_0.record(stream)
+    for _ in range(args.e2e_steps):
+        fin_state, acc = D.dfa_match_host(d.h, xp, stream=stream)
+    e_1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e_0.elapsed_time(e_1) / args.e2e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = world * n / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        dist.barrier() if dist else None
+        return 0
+
+    # roofline of the dominant kernel (the lanes kernel) and of the whole step
+    hbm_peak, sm_max, peak_src = peaks()
+    km = stats.get("kernel_ms", {})
+    calls = max(1, stats.get("profiled_calls", 1))
+    lanes_ms = km.get("lanes", 0.0) / calls
+    conv_ms = km.get("converge", 0.0) / calls
+    comp_ms = km.get("compose", 0.0) / calls
+    clocks = clk.summary()
+    hb = D.dfa_plan_bounds(n, P, d.info["c_num"], d.info["c_den"])
+    dom_size = np.array([D.dfa_domain(d.h, s).size for s in range(256)] if a.ns == 256 else
+                        [D.dfa_domain(d.h, s).size if s < a.ns else 0 for s in range(256)], np.int64)
+    L_alg = algorithmic_lookups(x, hb, dom_size)
+    f_clk = (clocks["sm_mhz"] or sm_max) * 1e6
+    lds_peak = 148 * 32 * f_clk
+    achieved = n / (lanes_ms * 1e-3) / 1e9 if lanes_ms else None
+    t_star = max(n / (hbm_peak * 1e9), L_alg / (148 * 32 * 1965e6))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": BASELINE_WORKLOAD.get(args.config, args.config), "name": args.config,
+                   "input_bytes_per_gpu": n, "chunks": P, "states": a.nq, "alphabet": a.ns,
+                   "i_max": imax, "gamma": f"{d.info['gamma_num']}/{d.info['gamma_den']}",
+                   "table_mode": d.info["table_mode_name"], "chunk_ratio_c": f"{d.info['c_num']}/{d.info['c_den']}",
+                   "convergence": bool(args.convergence), "l2": "input 256 MiB+ > 126 MB L2, no flush",
+                   "seed": args.seed, "input_sha256": W.sha256(x)[:16]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "kernel": "lanes_kernel", "algorithmic_bytes_per_launch": n, "kernel_ms": lanes_ms,
+                     "peak_source": peak_src,
+                     "step_frac_of_hbm": (n / (ms * 1e-3) / 1e9) / hbm_peak,
+                     "lookup": {"L_alg": L_alg, "lookups_per_s": L_alg / (ms * 1e-3),
+                                "lds_peak_per_s_at_sampled_clock": lds_peak,
+                                "frac_ns": t_star / (ms * 1e-3),
+                                "note": "north_star t* = max(n/8TB/s... here measured HBM, L_alg/(148*32*1.965GHz)); "
+                                        "convergence lets frac_ns exceed 1"}},
+        "kernels_ms_per_step": {"converge": conv_ms, "lanes": lanes_ms, "compose+finalize": comp_ms},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": n, "d2h_bytes_per_step": 16,
+                "api": "dfa_match_host (pinned host input)", "ms_per_step": e2e_ms},
+        "gpu_launches": int(stats["num_kernels"]) * args.steps,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        import oracle
+        od = oracle.Dfa(a.table, a.q0, a.accepting)
+        reps, t_tot = 0, 0.0
+        fin_cpu = None
+        while t_tot < 10.0 and reps < 64:
+            t_a = time.perf_counter()
+            fin_cpu = od.run(x)
+            t_tot += time.perf_counter() - t_a
+            reps += 1
+        line["cpu_baseline"] = {"value": reps * n / t_tot / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"oracle_run (Alg.1, one core) over the full {n >> 20} MiB input "
+                                          f"x {reps} (~{t_tot:.1f} s)"}
+        line["parity"] = {"final_state_gpu": int(fin_state), "final_state_oracle": int(fin_cpu),
+                          "match": int(fin_state) == int(fin_cpu)}
+    print(json.dumps(line))
+    if dist:
+        dist.barrier()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

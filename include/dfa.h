@@ -186,14 +186,18 @@ enum {
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 
-/* Per-call statistics of the last completed call (valid after a stream sync). */
+/* Statistics.  input_bytes .. num_kernels describe the last call.  With
+ * DFA_OPT_PROFILE on, every call records CUDA events (on its stream) around
+ * its kernel sections; dfa_get_stats synchronises them, returns the summed
+ * durations per section over all calls since the previous dfa_get_stats
+ * (kernel_name[i] / kernel_ms[i]; profiled = number of calls summed) and
+ * resets the accumulators. */
 typedef struct {
     uint64_t input_bytes;      /* n */
     uint64_t num_subchunks;    /* execution sub-chunks of the last call */
-    uint64_t lanes_initial;    /* sum over sub-chunks of |I_sigma| (1 for the first) */
     uint32_t num_kernels;      /* kernels launched by the last call */
-    uint32_t profiled;         /* 1 if kernel_ms below are valid */
-    float kernel_ms[8];        /* per-kernel durations (DFA_OPT_PROFILE) */
+    uint32_t profiled;         /* calls accumulated in kernel_ms */
+    float kernel_ms[8];        /* summed section durations (DFA_OPT_PROFILE) */
     char kernel_name[8][32];
 } dfa_stats;
 dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out);

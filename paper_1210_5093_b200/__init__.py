@@ -39,7 +39,7 @@ class DfaInfo(ctypes.Structure):
 
 class DfaStats(ctypes.Structure):
     _fields_ = [("input_bytes", ctypes.c_uint64), ("num_subchunks", ctypes.c_uint64),
-                ("lanes_initial", ctypes.c_uint64), ("num_kernels", ctypes.c_uint32),
+                ("num_kernels", ctypes.c_uint32),
                 ("profiled", ctypes.c_uint32), ("kernel_ms", ctypes.c_float * 8),
                 ("kernel_name", (ctypes.c_char * 32) * 8)]
 
@@ -228,10 +228,12 @@ def dfa_set_option(h, key: int, value: int):
 
 
 def dfa_get_stats(h) -> dict:
+    """Last-call counters, plus per-section kernel milliseconds summed over the
+    calls since the previous dfa_get_stats (DFA_OPT_PROFILE)."""
     s = DfaStats()
     _ck(lib().dfa_get_stats(h, ctypes.byref(s)), "dfa_get_stats")
-    d = {"input_bytes": s.input_bytes, "num_subchunks": s.num_subchunks, "lanes_initial": s.lanes_initial,
-         "num_kernels": s.num_kernels, "profiled": bool(s.profiled)}
+    d = {"input_bytes": s.input_bytes, "num_subchunks": s.num_subchunks,
+         "num_kernels": s.num_kernels, "profiled_calls": s.profiled}
     if s.profiled:
         d["kernel_ms"] = {bytes(s.kernel_name[i]).split(b"\0")[0].decode(): s.kernel_ms[i]
                           for i in range(8) if s.kernel_name[i][0]}

@@ -47,7 +47,6 @@ struct HostPinned {
     template <class T> T *as() const { return reinterpret_cast<T *>(p); }
 };
 
-constexpr int kMaxProf = 8;
 
 } // namespace
 
@@ -68,10 +67,15 @@ struct dfa_handle {
     cudaEvent_t staging_done = nullptr;
     bool staging_pending = false;
     cudaStream_t last_stream = nullptr;
-    // stats / profiling
+    // stats / profiling: event pairs around each kernel section, accumulated
+    // over calls until dfa_get_stats reads (and resets) them
     dfa_stats stats{};
-    cudaEvent_t ev[2 * kMaxProf] = {};
-    int nprof = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Rec { int section; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    int open_section = -1;
+    cudaEvent_t open_event = nullptr;
 };
 
 namespace {
@@ -183,7 +187,6 @@ dfa_status upload(dfa_handle *h) {
     CK(h->status.ensure(sizeof(DevStatus)));
     CK(h->h_status.ensure(sizeof(DevStatus)));
     CK(cudaEventCreateWithFlags(&h->staging_done, cudaEventDisableTiming));
-    for (int i = 0; i < 2 * kMaxProf; i++) CK(cudaEventCreate(&h->ev[i]));
     h->device_ready = true;
     return DFA_OK;
 }
@@ -199,15 +202,31 @@ dfa_status probe(dfa_handle *h, uint32_t &u8_limit) {
     return DFA_OK;
 }
 
-void prof_begin(dfa_handle *h, cudaStream_t s) {
-    if (h->profile && h->nprof < kMaxProf) cudaEventRecord(h->ev[2 * h->nprof], s);
-}
-void prof_end(dfa_handle *h, cudaStream_t s, const char *name) {
-    if (h->profile && h->nprof < kMaxProf) {
-        cudaEventRecord(h->ev[2 * h->nprof + 1], s);
-        std::snprintf(h->stats.kernel_name[h->nprof], 32, "%s", name);
-        h->nprof++;
+const char *const kSections[] = {"converge", "lanes", "compose"};
+constexpr int kNumSections = 3;
+
+cudaEvent_t prof_event(dfa_handle *h) {
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        h->ev_pool.push_back(e);
     }
+    return h->ev_pool[h->ev_used++];
+}
+void prof_begin(dfa_handle *h, cudaStream_t s, int section) {
+    if (!h->profile || h->ev_used + 2 > (1u << 16)) return;
+    h->open_event = prof_event(h);
+    h->open_section = section;
+    if (h->open_event) cudaEventRecord(h->open_event, s);
+}
+void prof_end(dfa_handle *h, cudaStream_t s) {
+    if (!h->profile || h->open_section < 0 || !h->open_event) return;
+    cudaEvent_t b = prof_event(h);
+    if (b) {
+        cudaEventRecord(b, s);
+        h->recs.push_back({h->open_section, h->open_event, b});
+    }
+    h->open_section = -1;
 }
 
 uint32_t compose_group(const dfa_handle *h) {
@@ -247,8 +266,7 @@ void plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb,
 dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const uint64_t *dev_bounds,
                uint32_t m0, uint32_t m, cudaStream_t s, const Outputs &o) {
     DevTables &T = h->T;
-    h->nprof = 0;
-    h->stats = dfa_stats{};
+    h->stats.input_bytes = 0;
     h->last_stream = s;
     CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds};
@@ -277,10 +295,10 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         CK(h->amap.ensure(NS * T.imax * 2));
         const int occ = std::max(1, converge_occupancy(T, wpc));
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + wpc - 1) / wpc);
-        prof_begin(h, s);
+        prof_begin(h, s, 0);
         CK(launch_converge(T, plan, in, h->surv.as<uint16_t>(), h->surv_n.as<uint8_t>(), h->surv_pos.as<uint64_t>(),
                            h->amap.as<uint16_t>(), wpc, (int)grid, s));
-        prof_end(h, s, "converge");
+        prof_end(h, s);
         kernels++;
         amap = h->amap.as<uint16_t>();
         surv = h->surv.as<uint16_t>();
@@ -291,10 +309,10 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         const int threads = h->threads;
         const int occ = std::max(1, lanes_occupancy(T, threads));
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
-        prof_begin(h, s);
+        prof_begin(h, s, 1);
         CK(launch_lanes(T, plan, in, surv, surv_n, surv_pos, h->sfin.as<uint16_t>(), sk, h->dom_of.as<uint16_t>(),
                         h->convergence, threads, (int)grid, s));
-        prof_end(h, s, "lanes");
+        prof_end(h, s);
         kernels++;
     }
     // composition: sub-chunk maps -> reporting maps -> final state
@@ -311,7 +329,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     LevelIn lin{0, amap, h->sfin.as<uint16_t>(), sk, nullptr, nullptr, h->dom_of.as<uint16_t>()};
     bool useA = true;
     const int cgrid_cap = h->sms * 8;
-    prof_begin(h, s);
+    prof_begin(h, s, 2);
     for (;;) {
         const uint64_t gf = (sh.f + G - 1) / G, gm = sh.S > 1 ? (sh.m + G - 1) / G : 0;
         const bool last = gf == 1 && (sh.S == 1 || gm == 1);
@@ -352,7 +370,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     }
     CK(launch_finalize(T, lin.row0, h->status.as<DevStatus>(), o.final2, s));
     kernels++;
-    prof_end(h, s, "compose+finalize");
+    prof_end(h, s);
     if (o.starts) {
         CK(launch_starts(T, plan, rep.row0, rep.rows, rep.dom, o.starts, h->status.as<DevStatus>(), s));
         kernels++;
@@ -444,7 +462,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         h->h_status.release();
         h->h_bounds.release();
         if (h->staging_done) cudaEventDestroy(h->staging_done);
-        for (auto &e : h->ev) if (e) cudaEventDestroy(e);
+        for (auto &e : h->ev_pool) if (e) cudaEventDestroy(e);
     }
     delete h;
     return DFA_OK;
@@ -615,15 +633,21 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
 dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out) {
     if (!h || !out) return DFA_ERR_ARG;
     dfa_stats s = h->stats;
-    if (h->device_ready && h->profile && h->nprof > 0) {
-        CK(cudaEventSynchronize(h->ev[2 * h->nprof - 1]));
-        for (int i = 0; i < h->nprof; i++) {
+    for (int i = 0; i < 8; i++) { s.kernel_ms[i] = 0; s.kernel_name[i][0] = 0; }
+    s.profiled = 0;
+    if (h->device_ready && !h->recs.empty()) {
+        CK(cudaEventSynchronize(h->recs.back().b));
+        uint32_t calls = 0;
+        for (const auto &r : h->recs) {
             float ms = 0;
-            CK(cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]));
-            s.kernel_ms[i] = ms;
-            std::snprintf(s.kernel_name[i], 32, "%s", h->stats.kernel_name[i]);
+            CK(cudaEventElapsedTime(&ms, r.a, r.b));
+            s.kernel_ms[r.section] += ms;
+            if (r.section == 1) calls++;
         }
-        s.profiled = 1;
+        for (int i = 0; i < kNumSections; i++) std::snprintf(s.kernel_name[i], 32, "%s", kSections[i]);
+        s.profiled = calls;
+        h->recs.clear();
+        h->ev_used = 0;
     }
     *out = s;
     return DFA_OK;
