@@ -53,7 +53,13 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--convergence", type=int, default=1)
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library option NAME=VALUE (subchunk_target, tree_fanin, threads_per_cta)")
+    ap.add_argument("--quiet-json", action="store_true", help="print a one-line summary instead of JSON")
     return ap.parse_args()
+
+
+OPTS = {"subchunk_target": 1, "convergence": 2, "threads_per_cta": 4, "tree_fanin": 5}
 
 
 def peaks():
@@ -174,6 +180,9 @@ def main():
 
     d = D.Dfa(a.table, a.q0, a.accept_bitmap)
     D.dfa_set_option(d.h, D.DFA_OPT_CONVERGENCE, args.convergence)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        D.dfa_set_option(d.h, OPTS[k], int(v))
     imax = d.info["i_max"]
     bounds = torch.empty(P + 1, dtype=torch.int64, device=dev)
     e0 = torch.empty(1, dtype=torch.int16, device=dev)
@@ -299,7 +308,11 @@ def main():
                                           f"x {reps} (~{t_tot:.1f} s)"}
         line["parity"] = {"final_state_gpu": int(fin_state), "final_state_oracle": int(fin_cpu),
                           "match": int(fin_state) == int(fin_cpu)}
-    print(json.dumps(line))
+    if args.quiet_json:
+        print(f"{args.config} {' '.join(args.opt)} value={value:.1f} GB/s ms={ms:.4f} "
+              f"kernels={ {k: round(v, 4) for k, v in line['kernels_ms_per_step'].items()} }")
+    else:
+        print(json.dumps(line))
     if dist:
         dist.barrier()
     return 0

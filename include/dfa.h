@@ -182,7 +182,8 @@ enum {
     DFA_OPT_SUBCHUNK_TARGET = 1, /* number of execution sub-chunks per call (0 = auto) */
     DFA_OPT_CONVERGENCE = 2,     /* 1 = merge converged lanes (default), 0 = off */
     DFA_OPT_PROFILE = 3,         /* 1 = record per-kernel CUDA-event times */
-    DFA_OPT_THREADS_PER_CTA = 4  /* match kernel CTA size (0 = auto) */
+    DFA_OPT_THREADS_PER_CTA = 4, /* match kernel CTA size (0 = auto) */
+    DFA_OPT_TREE_FANIN = 5       /* max children per composition-tree node, 2..64 (default 32) */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 

@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libdfa.so")
+LIB = os.environ.get("DFA_LIB") or os.path.join(HERE, "libdfa.so")
 SOURCES = ["api.cpp", "prep.cpp", "kernels.cu"]
 HEADERS = ["kernels.cuh", "prep.h", os.path.join("..", "..", "include", "dfa.h")]
 

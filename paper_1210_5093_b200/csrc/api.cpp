@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -59,10 +60,12 @@ struct dfa_handle {
     uint32_t c_num = 1, c_den = 1;
     // options
     int convergence = 1, profile = 0, threads = 512;
+    uint32_t tree_fanin_cap = 32;
     int64_t subchunk_target = 0;
     // scratch
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
-    DevBuf lvlA, lvlB, domA, domB, rep_rows, rep_dom, bounds, input;
+    DevBuf lvlA, domA, counters, bounds, input;
+    std::vector<uint64_t> tree_sig;
     HostPinned h_status, h_bounds;
     cudaEvent_t staging_done = nullptr;
     bool staging_pending = false;
@@ -117,11 +120,13 @@ dfa_status upload(dfa_handle *h) {
     while (image.size() % 4) image.push_back(0);
     std::vector<uint16_t> dom_list((size_t)(nc + 1) * imax, kNone), dom_size(nc + 1, 0);
     std::vector<uint16_t> rank((size_t)(nc + 1) * nq, kNone);
+    std::vector<uint8_t> rank8(imax < 255 ? (size_t)(nc + 1) * nq : 0, 0xFF);
     for (uint32_t c = 0; c <= nc; c++) {
         dom_size[c] = (uint16_t)p.dom[c].size();
         for (uint32_t j = 0; j < p.dom[c].size(); j++) {
             dom_list[(size_t)c * imax + j] = p.dom[c][j];
             rank[(size_t)c * nq + p.dom[c][j]] = (uint16_t)j;
+            if (!rank8.empty()) rank8[(size_t)c * nq + p.dom[c][j]] = (uint8_t)j;
         }
     }
     std::vector<uint16_t> xlat((size_t)nc * imu, 0), dom_user_size(nc, 0);
@@ -150,6 +155,7 @@ dfa_status upload(dfa_handle *h) {
         {accept.data(), accept.size() * 4, 0},
         {xlat.data(), xlat.size() * 2, 0},
         {dom_user_size.data(), dom_user_size.size() * 2, 0},
+        {rank8.data(), rank8.size(), 0},
     };
     size_t total = 0;
     for (auto &s : secs) { s.off = total; total += (s.bytes + 255) & ~size_t(255); }
@@ -171,11 +177,15 @@ dfa_status upload(dfa_handle *h) {
     T.accept_bits = reinterpret_cast<const uint32_t *>(at(8));
     T.xlat = reinterpret_cast<const uint16_t *>(at(9));
     T.dom_user_size = reinterpret_cast<const uint16_t *>(at(10));
+    T.rank8 = rank8.empty() ? nullptr : at(11);
     T.nq = nq;
     T.nclass = nc;
     T.start_dom = p.start_dom;
     T.imax = imax;
     T.imax_user = imu;
+    T.rs = (imax + 7) & ~7u;
+    T.has_dead = 0;
+    for (uint32_t q = 0; q < nq; q++) T.has_dead |= p.dead[q];
     T.stride = p.stride;
     T.win_base = p.win_base;
     T.win_w = p.win_w;
@@ -229,10 +239,21 @@ void prof_end(dfa_handle *h, cudaStream_t s) {
     h->open_section = -1;
 }
 
-uint32_t compose_group(const dfa_handle *h) {
-    const uint64_t room = (uint64_t)h->optin_smem - (uint64_t)h->T.imax * 2 - 64;
-    uint64_t G = 1 + room / ((uint64_t)h->T.nq * 2);
-    return (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(2, G));
+// Children per composition-tree node: as many as fit a warp's shared-memory
+// slice (8 warps per CTA), at most 64.  The rank table is staged as uint8 when
+// I_max < 255 and it is small.
+uint32_t tree_fanin(const dfa_handle *h, int &rank_smem, int &smem_bytes) {
+    const DevTables &T = h->T;
+    const uint64_t cap = (uint64_t)h->optin_smem;
+    // stage the uint8 rank table in shared memory when it leaves room for F >= 8
+    rank_smem = 0;
+    if (T.rank8 && (uint64_t)tree_fixed_bytes(T, 1) + (uint64_t)tree_slice_bytes(T, 8) * 8 <= cap) rank_smem = 1;
+    const uint64_t fixed = (uint64_t)tree_fixed_bytes(T, rank_smem);
+    const uint64_t budget = cap - fixed;
+    uint32_t F = h->tree_fanin_cap;
+    while (F > 2 && (uint64_t)tree_slice_bytes(T, F) * 8 > budget) F--;
+    smem_bytes = (int)(fixed + (uint64_t)tree_slice_bytes(T, F) * 8);
+    return F;
 }
 
 struct Outputs {
@@ -281,7 +302,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         for (int w = 16; w >= 1; w /= 2)
             if (converge_smem_bytes(T, w) <= h->optin_smem) { wpc = w; break; }
     }
-    const uint32_t sk = stageA && wpc ? (uint32_t)kLanes : std::max<uint32_t>(kLanes, (T.imax + 7) & ~7u);
+    const uint32_t sk = stageA && wpc ? (uint32_t)kLanes : std::max<uint32_t>(kLanes, T.rs);
     CK(h->sfin.ensure(NS * sk * 2));
     CK(h->dom_of.ensure(NS * 2));
     const uint16_t *amap = nullptr, *surv = nullptr;
@@ -292,7 +313,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         CK(h->surv.ensure(NS * kLanes * 2));
         CK(h->surv_n.ensure(NS));
         CK(h->surv_pos.ensure(NS * 8));
-        CK(h->amap.ensure(NS * T.imax * 2));
+        CK(h->amap.ensure(NS * T.rs * 2));
         const int occ = std::max(1, converge_occupancy(T, wpc));
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + wpc - 1) / wpc);
         prof_begin(h, s, 0);
@@ -315,64 +336,78 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         prof_end(h, s);
         kernels++;
     }
-    // composition: sub-chunk maps -> reporting maps -> final state
-    const uint32_t G = compose_group(h);
-    Shape sh{m0, P > 1 ? m : 0, P, G};
-    const uint64_t first_groups = sh.groups();
-    const uint64_t ping = std::max<uint64_t>(first_groups, (P + G - 1) / G) + 1;
-    CK(h->lvlA.ensure(ping * T.imax * 2));
-    CK(h->lvlB.ensure(ping * T.imax * 2));
-    CK(h->domA.ensure(ping * 2));
-    CK(h->domB.ensure(ping * 2));
-    CK(h->rep_rows.ensure((uint64_t)(P + 1) * T.imax * 2));
-    CK(h->rep_dom.ensure((uint64_t)(P + 1) * 2));
-    LevelIn lin{0, amap, h->sfin.as<uint16_t>(), sk, nullptr, nullptr, h->dom_of.as<uint16_t>()};
-    bool useA = true;
-    const int cgrid_cap = h->sms * 8;
-    prof_begin(h, s, 2);
-    for (;;) {
-        const uint64_t gf = (sh.f + G - 1) / G, gm = sh.S > 1 ? (sh.m + G - 1) / G : 0;
-        const bool last = gf == 1 && (sh.S == 1 || gm == 1);
-        LevelOut out{};
-        if (last) {
-            out.row0 = h->rep_rows.as<uint16_t>();
-            out.rows = h->rep_rows.as<uint16_t>() + T.imax;
-            out.dom = h->rep_dom.as<uint16_t>();
-            out.user_rows = o.user_maps;
-            out.e0 = o.chunk0_end;
-        } else {
-            DevBuf &b = useA ? h->lvlA : h->lvlB;
-            DevBuf &d = useA ? h->domA : h->domB;
-            out.row0 = b.as<uint16_t>();
-            out.rows = b.as<uint16_t>() + T.imax;
-            out.dom = d.as<uint16_t>();
-            useA = !useA;
+    // composition: sub-chunk maps -> reporting maps -> final state, one launch
+    Tree tr{};
+    int tree_smem = 0;
+    const uint32_t F = tree_fanin(h, tr.rank_smem, tree_smem);
+    tr.F = F;
+    tr.dbg = getenv("DFA_TREE_DBG") ? atoi(getenv("DFA_TREE_DBG")) : 0;
+    {
+        uint32_t L = 0;
+        uint64_t total = 0;
+        struct Sh { uint64_t f, m, S; };
+        Sh cur{m0, P > 1 ? m : 0, P};
+        bool overflow = false;
+        auto add = [&](Sh prev, uint32_t G) {
+            L++;
+            if (L > (uint32_t)kMaxLevels) { overflow = true; return Sh{1, 1, 1}; }
+            const uint64_t gf = (prev.f + G - 1) / G, gm = prev.S > 1 ? (prev.m + G - 1) / G : 0;
+            TreeLevel &lv = tr.lv[L];
+            lv.f = (uint32_t)prev.f;
+            lv.m = (uint32_t)std::max<uint64_t>(prev.m, 1);
+            lv.S = (uint32_t)prev.S;
+            lv.G = G;
+            lv.gf = (uint32_t)gf;
+            lv.gm = (uint32_t)std::max<uint64_t>(gm, 1);
+            lv.nodes = (uint32_t)(gf + (prev.S - 1) * gm);
+            lv.off = (uint32_t)total;
+            total += lv.nodes;
+            return Sh{gf, gm, prev.S};
+        };
+        if (cur.f == 1 && (cur.S == 1 || cur.m == 1)) cur = add(cur, 1);  // leaves are the chunks
+        while (!overflow && !(cur.f == 1 && (cur.S == 1 || cur.m == 1))) cur = add(cur, F);
+        tr.rep_level = L;
+        Sh fold{P, 0, 1};
+        while (!overflow && fold.f > 1) fold = add(fold, F);
+        if (overflow || total >= (1ull << 31) || NS >= (1ull << 31)) return DFA_ERR_INTERNAL;
+        tr.nlevels = L;
+        tr.lrs = tree_lrs(T);
+        CK(h->lvlA.ensure(total * T.rs * 2));
+        CK(h->domA.ensure(total * 2));
+        // arrival counters: valid across calls with the same tree (multiples of
+        // the child counts), zeroed when the tree changes
+        std::vector<uint64_t> sig = {total, F, L, (uint64_t)m0, (uint64_t)m, (uint64_t)P};
+        if (sig != h->tree_sig || h->counters.cap < total * 4) {
+            CK(h->counters.ensure(total * 4));
+            CK(cudaMemsetAsync(h->counters.p, 0, total * 4, s));
+            h->tree_sig = sig;
         }
-        const uint64_t ng = sh.groups();
-        CK(launch_compose(T, lin, out, sh, h->status.as<DevStatus>(), (int)std::min<uint64_t>(ng, cgrid_cap), s));
-        kernels++;
-        lin = LevelIn{1, nullptr, nullptr, 0, out.row0, out.rows, out.dom};
-        sh = Shape{gf, gm, sh.S, G};
-        if (last) break;
     }
-    const LevelIn rep = lin;
-    Shape fs{P, 0, 1, G};
-    while (fs.f > 1) {
-        DevBuf &b = useA ? h->lvlA : h->lvlB;
-        DevBuf &d = useA ? h->domA : h->domB;
-        useA = !useA;
-        LevelOut out{b.as<uint16_t>(), b.as<uint16_t>() + T.imax, d.as<uint16_t>(), nullptr, nullptr};
-        const uint64_t ng = fs.groups();
-        CK(launch_compose(T, lin, out, fs, h->status.as<DevStatus>(), (int)std::min<uint64_t>(ng, cgrid_cap), s));
+    tr.amap = amap;
+    tr.sfin = h->sfin.as<uint16_t>();
+    tr.sk = sk;
+    tr.dom_of = h->dom_of.as<uint16_t>();
+    tr.rows = h->lvlA.as<uint16_t>();
+    tr.doms = h->domA.as<uint16_t>();
+    tr.counters = h->counters.as<uint32_t>();
+    tr.user_rows = o.user_maps;
+    tr.e0 = o.chunk0_end;
+    tr.dev_final = o.final2;
+    tr.status = h->status.as<DevStatus>();
+    {
+        const uint64_t warps = (tr.lv[1].nodes + 0);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_fn(), 256, tree_smem);
+        const uint64_t grid = std::min<uint64_t>((warps + 7) / 8, (uint64_t)h->sms * std::max(1, occ));
+        prof_begin(h, s, 2);
+        CK(launch_tree(T, tr, (int)std::max<uint64_t>(1, grid), tree_smem, s));
+        prof_end(h, s);
         kernels++;
-        lin = LevelIn{1, nullptr, nullptr, 0, out.row0, out.rows, out.dom};
-        fs = Shape{(fs.f + G - 1) / G, 0, 1, G};
     }
-    CK(launch_finalize(T, lin.row0, h->status.as<DevStatus>(), o.final2, s));
-    kernels++;
-    prof_end(h, s);
     if (o.starts) {
-        CK(launch_starts(T, plan, rep.row0, rep.rows, rep.dom, o.starts, h->status.as<DevStatus>(), s));
+        const uint16_t *rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
+        CK(launch_starts(T, plan, rep_rows, rep_rows + T.rs, tr.doms + tr.lv[tr.rep_level].off, o.starts,
+                         h->status.as<DevStatus>(), s));
         kernels++;
     }
     h->stats.num_kernels = kernels;
@@ -456,8 +491,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
     if (h->device_ready) {
         if (h->last_stream) cudaStreamSynchronize(h->last_stream);
         for (DevBuf *b : {&h->tables, &h->status, &h->sfin, &h->dom_of, &h->surv, &h->surv_n, &h->surv_pos,
-                          &h->amap, &h->lvlA, &h->lvlB, &h->domA, &h->domB, &h->rep_rows, &h->rep_dom,
-                          &h->bounds, &h->input})
+                          &h->amap, &h->lvlA, &h->domA, &h->counters, &h->bounds, &h->input})
             b->release();
         h->h_status.release();
         h->h_bounds.release();
@@ -621,6 +655,10 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
     case DFA_OPT_SUBCHUNK_TARGET: if (value < 0) return DFA_ERR_ARG; h->subchunk_target = value; return DFA_OK;
     case DFA_OPT_CONVERGENCE: h->convergence = value ? 1 : 0; return DFA_OK;
     case DFA_OPT_PROFILE: h->profile = value ? 1 : 0; return DFA_OK;
+    case DFA_OPT_TREE_FANIN:
+        if (value < 2 || value > 64) return DFA_ERR_ARG;
+        h->tree_fanin_cap = (uint32_t)value;
+        return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         if (value == 0) value = 512;
         if (value < 32 || value > 512 || value % 32) return DFA_ERR_ARG;

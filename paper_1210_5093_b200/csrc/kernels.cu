@@ -464,109 +464,188 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
         for (uint32_t j = lane; j < u; j += 32) {
             uint32_t r = j;
             while (parent[r] != r) r = parent[r];
-            amap[i * T.imax + j] = res[r];
+            amap[i * T.rs + j] = res[r];
         }
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------
-// compose_kernel: one CTA per group of <= G consecutive maps.  Maps 2..cnt of
-// the group are expanded to dense maps over Q in shared memory
-// (dense[q] = L[rank(q)], error states map to themselves), then every entry
-// of the first map is pushed through them: Eq.MapReduction
-// L_{i,j}[q] = L_j[L_i[q]] applied cnt-1 times.
+// tree_kernel: the composition tree of Tree (kernels.cuh) in one launch.  Warps
+// take level-1 nodes; a warp that finishes a node bumps its parent's arrival
+// counter and, if it was the last child, processes the parent too (no warp
+// ever waits for another).  A node stages its <= F children's maps in the
+// warp's shared-memory slice, then pushes every entry of the first child's
+// map through the others: L_{i,j}[q] = L_j[rank_j(L_i[q])] (Eq.MapReduction,
+// P:819-830); error states map to themselves (reading R1).
+// Counters are never reset: a node is complete when its count reaches a
+// multiple of its child count (calls on a stream do not overlap).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t level_entry(const LevelIn &in, const DevTables &T, uint64_t i, uint32_t r) {
-    if (in.kind == 0) {
-        if (in.amap) {
-            const uint32_t a = in.amap[i * T.imax + r];
-            return a < kSurvBase ? a : in.sfin[i * in.sk + (a - kSurvBase)];
-        }
-        return in.sfin[i * in.sk + r];
-    }
-    const uint16_t *row = i == 0 ? in.row0 : in.rows + (i - 1) * T.imax;
-    return row[r];
+#ifdef DFA_TREE_TIMING
+__device__ unsigned long long g_tree_t[32];  // [0] kernel start (min), [L] level L done (max)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+__device__ __forceinline__ void group_range(const TreeLevel &lv, uint32_t g, uint32_t &st, uint32_t &en) {
+    if (g < lv.gf) { st = g * lv.G; en = min(lv.f, st + lv.G); return; }
+    const uint32_t t = g - lv.gf, seg = t / lv.gm, r = t - seg * lv.gm;
+    const uint32_t base = lv.f + seg * lv.m;
+    st = base + r * lv.G;
+    en = min(base + lv.m, st + lv.G);
 }
 
-__device__ __forceinline__ void group_range(const Shape &sh, uint64_t g, uint64_t &st, uint64_t &en) {
-    const uint64_t gf = (sh.f + sh.G - 1) / sh.G;
-    if (g < gf) { st = g * sh.G; en = min(sh.f, st + sh.G); return; }
-    const uint64_t gm = (sh.m + sh.G - 1) / sh.G;
-    const uint64_t t = g - gf, seg = t / gm, r = t % gm;
-    const uint64_t base = sh.f + seg * sh.m;
-    st = base + r * sh.G;
-    en = min(base + sh.m, st + sh.G);
+__device__ __forceinline__ uint32_t parent_of(const TreeLevel &lv, uint32_t c) {
+    if (c < lv.f) return c / lv.G;
+    const uint32_t t = c - lv.f, seg = t / lv.m;
+    return lv.gf + seg * lv.gm + (t - seg * lv.m) / lv.G;
 }
 
-__global__ void __launch_bounds__(256) compose_kernel(DevTables T, LevelIn in, LevelOut out, Shape sh,
-                                                      DevStatus *status) {
+__device__ __forceinline__ const uint4 *tree_child_row(const Tree &tr, const DevTables &T, uint32_t Lc, uint32_t c) {
+    const uint16_t *p = Lc == 0 ? (tr.amap ? tr.amap + (uint64_t)c * T.rs : tr.sfin + (uint64_t)c * tr.sk)
+                                : tr.rows + (uint64_t)(tr.lv[Lc].off + c) * T.rs;
+    return reinterpret_cast<const uint4 *>(p);
+}
+
+__device__ __forceinline__ uint32_t tree_child_dom(const Tree &tr, uint32_t Lc, uint32_t c) {
+    return Lc == 0 ? tr.dom_of[c] : __ldcg(tr.doms + tr.lv[Lc].off + c);
+}
+
+__global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
     extern __shared__ uint4 smem4[];
-    uint16_t *dense = reinterpret_cast<uint16_t *>(smem4);
-    const uint64_t ngroups = sh.groups();
-    for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-        uint64_t st, en;
-        group_range(sh, g, st, en);
-        const uint32_t cnt = (uint32_t)(en - st);
-        uint16_t *rowbuf = dense + (size_t)(sh.G - 1) * T.nq;
-        const uint32_t total = (cnt - 1) * T.nq;
-        for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-            const uint32_t c = t / T.nq, q = t - c * T.nq;
-            const uint64_t i = st + 1 + c;
-            uint32_t v;
-            if (test_bit(T.dead_bits, q)) v = q;
-            else {
-                const uint32_t d = in.dom[i];
-                const uint32_t r = T.rank[(uint64_t)d * T.nq + q];
-                v = r == kNone ? kNone : level_entry(in, T, i, r);
-            }
-            dense[t] = (uint16_t)v;
-        }
-        __syncthreads();
-        const uint32_t d0 = in.dom[st];
-        const uint32_t u = T.dom_size[d0];
-        for (uint32_t j = threadIdx.x; j < T.imax; j += blockDim.x) {
-            uint32_t s = kNone;
-            if (j < u) {
-                s = level_entry(in, T, st, j);
-                for (uint32_t c = 0; c + 1 < cnt; c++) {
-                    const uint32_t s2 = dense[(size_t)c * T.nq + s];
-                    if (s2 == kNone) { atomicMax(&status->err, 8u); s = 0; break; }
-                    s = s2;
-                }
-            }
-            rowbuf[j] = (uint16_t)s;
-            uint16_t *orow = g == 0 ? out.row0 : out.rows + (g - 1) * T.imax;
-            orow[j] = (uint16_t)s;
-        }
-        if (threadIdx.x == 0) out.dom[g] = (uint16_t)d0;
-        __syncthreads();
-        if (out.user_rows && g > 0) {
-            // API row in the user's I_sigma order (reading R1): drop internal-only states
-            const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : 0;
-            uint16_t *urow = out.user_rows + (g - 1) * T.imax_user;
-            for (uint32_t j = threadIdx.x; j < T.imax_user; j += blockDim.x)
-                urow[j] = j < du ? rowbuf[T.xlat[(uint64_t)d0 * T.imax_user + j]] : kNone;
-        }
-        if (out.e0 && g == 0 && threadIdx.x == 0) out.e0[0] = rowbuf[0];
-        __syncthreads();
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMin(&g_tree_t[0], gtimer());
+#endif
+    // shared: [rank table u8 (optional)][dom sizes u16][error-state bits][warp slices].
+    // The walk must not depend on L1: every acquire invalidates it.
+    uint8_t *sb = reinterpret_cast<uint8_t *>(smem4);
+    const uint32_t rank_bytes = tr.rank_smem ? (((T.nclass + 1) * T.nq + 15) & ~15u) : 0u;
+    const uint8_t *rank8 = tr.rank_smem ? sb : T.rank8;
+    if (tr.rank_smem) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(T.rank8);
+        for (uint32_t i = threadIdx.x; i < rank_bytes / 16; i += blockDim.x)
+            reinterpret_cast<uint4 *>(sb)[i] = __ldg(src + i);
     }
-}
+    uint16_t *dsz = reinterpret_cast<uint16_t *>(sb + rank_bytes);
+    const uint32_t dsz_bytes = ((T.nclass + 1) * 2 + 15) & ~15u;
+    uint32_t *dead = reinterpret_cast<uint32_t *>(sb + rank_bytes + dsz_bytes);
+    const uint32_t dead_words = ((T.nq + 31) / 32 + 3) & ~3u;
+    for (uint32_t i = threadIdx.x; i <= T.nclass; i += blockDim.x) dsz[i] = T.dom_size[i];
+    for (uint32_t i = threadIdx.x; i < dead_words; i += blockDim.x) dead[i] = __ldg(T.dead_bits + i);
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t lrs = tr.lrs, rsp = 1u << lrs;     // shared row stride (power of two)
+    const uint32_t q4 = T.rs >> 3;                     // 16-byte pieces of a global row
+    uint32_t lq = 0;
+    while ((1u << lq) < q4) lq++;                      // pieces per row rounded to a power of two
+    uint16_t *slice = reinterpret_cast<uint16_t *>(sb + rank_bytes + dsz_bytes + dead_words * 4) +
+                      (size_t)warp * ((tr.F << lrs) + ((tr.F + 7) & ~7u) + rsp);
+    uint16_t *st = slice, *dch = slice + (tr.F << lrs), *row = dch + ((tr.F + 7) & ~7u);
 
-// ---------------------------------------------------------------------------
-// finalize_kernel: Alg.seqmatch lines 4-6 on the composed state.
-// ---------------------------------------------------------------------------
-__global__ void finalize_kernel(DevTables T, const uint16_t *final_row, DevStatus *status, uint16_t *dev_final) {
-    if (threadIdx.x != 0) return;
-    const uint32_t s = final_row[0];
-    uint32_t err = status->err;
-    if (s == T.poison) err = max(err, 5u);
-    status->final_state = s;
-    status->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
-    status->err = err;
-    if (dev_final) {
-        dev_final[0] = (uint16_t)s;
-        dev_final[1] = (uint16_t)status->accept;
+    for (uint32_t g1 = blockIdx.x * nwarps + warp; g1 < tr.lv[1].nodes; g1 += gridDim.x * nwarps) {
+        uint32_t L = 1;
+        uint32_t node = g1;
+        for (;;) {
+            // ---- process node (L, node): stage children (doms, 16-byte row pieces)
+            const TreeLevel lv = tr.lv[L];
+            uint32_t c0, c1;
+            group_range(lv, node, c0, c1);
+            const uint32_t nc = c1 - c0;
+            for (uint32_t t = lane; t < nc; t += 32) dch[t] = (uint16_t)tree_child_dom(tr, L - 1, c0 + t);
+            for (uint32_t t = lane; t < (nc << lq); t += 32) {
+                const uint32_t c = t >> lq, k = t & ((1u << lq) - 1);
+                if (k < q4)
+                    reinterpret_cast<uint4 *>(st + (c << lrs))[k] = __ldcg(tree_child_row(tr, T, L - 1, c0 + c) + k);
+            }
+            __syncwarp();
+            if (L == 1 && tr.amap) {  // leaves after converge_kernel: resolve survivor codes
+                for (uint32_t t = lane; t < (nc << lrs); t += 32) {
+                    const uint32_t c = t >> lrs, r = t & (rsp - 1);
+                    const uint32_t a = st[t];
+                    if (r < dsz[dch[c]] && a >= kSurvBase && a != kNone)
+                        st[t] = tr.sfin[(uint64_t)(c0 + c) * tr.sk + (a - kSurvBase)];
+                }
+                __syncwarp();
+            }
+            // pairwise tree over the children in the warp: in round `step`, map a
+            // (a = 0, 2step, ...) absorbs map a+step: L_a <- L_{a+step} o L_a
+            for (uint32_t step = 1; step < nc && !(tr.dbg & 1); step *= 2) {
+                const uint32_t npairs = (nc - step + 2 * step - 1) / (2 * step);
+                for (uint32_t t = lane; t < (npairs << lrs); t += 32) {
+                    const uint32_t p = t >> lrs, j = t & (rsp - 1);
+                    const uint32_t a = p * 2 * step, b = a + step;
+                    uint32_t s = st[(a << lrs) + j];
+                    if (j >= dsz[dch[a]] || (T.has_dead && test_bit(dead, s))) continue;
+                    const uint32_t d = dch[b];
+                    uint32_t r;
+                    if (rank8) { r = rank8[d * T.nq + s]; r = r == 0xFFu ? kNone : r; }
+                    else r = __ldg(T.rank + (uint64_t)d * T.nq + s);
+                    if (r == kNone) { atomicMax(&tr.status->err, 8u); r = 0; }
+                    st[(a << lrs) + j] = st[(b << lrs) + r];
+                }
+                __syncwarp();
+            }
+            const uint32_t d0 = dch[0];
+            const uint32_t u = dsz[d0];
+            for (uint32_t j = lane; j < T.rs; j += 32) row[j] = j < u ? st[j] : kNone;
+            __syncwarp();
+            uint16_t *orow = tr.rows + (uint64_t)(lv.off + node) * T.rs;
+            for (uint32_t t = lane; t < q4; t += 32)
+                reinterpret_cast<uint4 *>(orow)[t] = reinterpret_cast<const uint4 *>(row)[t];
+            if (lane == 0) tr.doms[lv.off + node] = (uint16_t)d0;
+            if (L == tr.rep_level) {
+                // reporting chunk k = node: API row in the user's I_sigma order
+                if (tr.user_rows && node > 0) {
+                    const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : 0;
+                    uint16_t *urow = tr.user_rows + (uint64_t)(node - 1) * T.imax_user;
+                    for (uint32_t j = lane; j < T.imax_user; j += 32)
+                        urow[j] = j < du ? row[T.xlat[(uint64_t)d0 * T.imax_user + j]] : kNone;
+                }
+                if (tr.e0 && node == 0 && lane == 0) tr.e0[0] = row[0];
+            }
+#ifdef DFA_TREE_TIMING
+            if (lane == 0) atomicMax(&g_tree_t[L], gtimer());
+#endif
+            if (L == tr.nlevels) {
+                // root: Alg.seqmatch lines 4-6 on delta-hat(q0, x)
+                if (lane == 0) {
+                    const uint32_t fs = row[0];
+                    DevStatus *S = tr.status;
+                    if (fs == T.poison) atomicMax(&S->err, 5u);
+                    S->final_state = fs;
+                    S->accept = fs < T.nq ? (uint32_t)test_bit(T.accept_bits, fs) : 0u;
+                    if (tr.dev_final) {
+                        tr.dev_final[0] = (uint16_t)fs;
+                        tr.dev_final[1] = (uint16_t)S->accept;
+                    }
+                }
+                __syncwarp();
+                break;
+            }
+            // ---- hand the result to the parent; continue with it if last to arrive
+            const TreeLevel &up = tr.lv[L + 1];
+            const uint32_t parent = parent_of(up, node);
+            uint32_t p0, p1;
+            group_range(up, parent, p0, p1);
+            const uint32_t nchild = p1 - p0;
+            __syncwarp();
+            uint32_t prev = 0;
+            if (lane == 0 && (tr.dbg & 2)) prev = atomicAdd(tr.counters + up.off + parent, 1u);
+            else if (lane == 0) {
+                // release: this node's row (written by all lanes, ordered by the
+                // syncwarp) before the count; acquire: the siblings' rows after it.
+                // A release/acquire RMW, not fence.sc: thousands of warps do this.
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                             : "=r"(prev) : "l"(tr.counters + up.off + parent) : "memory");
+            }
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if ((prev + 1) % nchild != 0) break;
+            L++;
+            node = parent;
+        }
     }
 }
 
@@ -585,7 +664,7 @@ __global__ void starts_kernel(DevTables T, Plan p, const uint16_t *row0, const u
         if (test_bit(T.dead_bits, s)) continue;
         const uint32_t r = T.rank[(uint64_t)dom[k] * T.nq + s];
         if (r == kNone) { atomicMax(&status->err, 8u); return; }
-        s = rows[(uint64_t)(k - 1) * T.imax + r];
+        s = rows[(uint64_t)(k - 1) * T.rs + r];
     }
 }
 
@@ -640,8 +719,20 @@ int converge_smem_bytes(const DevTables &T, int warps_per_cta) {
     return lanes_smem_bytes(T) + warps_per_cta * (int)scr * 2;
 }
 
-int compose_smem_bytes(const DevTables &T, uint32_t G) {
-    return (int)(((size_t)(G - 1) * T.nq + T.imax) * 2 + 16);
+uint32_t tree_lrs(const DevTables &T) {
+    uint32_t l = 3;
+    while ((1u << l) < T.rs) l++;
+    return l;
+}
+int tree_slice_bytes(const DevTables &T, uint32_t F) {
+    const uint32_t rsp = 1u << tree_lrs(T);
+    return (int)((F * rsp + ((F + 7) & ~7u) + rsp) * 2);
+}
+int tree_fixed_bytes(const DevTables &T, int rank_smem) {
+    const uint32_t rank_bytes = rank_smem ? (((T.nclass + 1) * T.nq + 15) & ~15u) : 0u;
+    const uint32_t dsz_bytes = ((T.nclass + 1) * 2 + 15) & ~15u;
+    const uint32_t dead_words = ((T.nq + 31) / 32 + 3) & ~3u;
+    return (int)(rank_bytes + dsz_bytes + dead_words * 4);
 }
 
 cudaError_t setup_kernel_attributes(const DevTables &T) {
@@ -652,7 +743,7 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute((void *)compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    return cudaFuncSetAttribute((void *)tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 int lanes_occupancy(const DevTables &T, int threads) {
@@ -684,15 +775,23 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
     return cudaLaunchKernel(lanes_fn(T.mode), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
 }
 
-cudaError_t launch_compose(const DevTables &T, const LevelIn &in, const LevelOut &out, const Shape &sh,
-                           DevStatus *st, int grid, cudaStream_t s) {
-    compose_kernel<<<grid, 256, compose_smem_bytes(T, sh.G), s>>>(T, in, out, sh, st);
-    return cudaGetLastError();
-}
+const void *tree_fn() { return (const void *)tree_kernel; }
 
-cudaError_t launch_finalize(const DevTables &T, const uint16_t *final_row, DevStatus *st, uint16_t *dev_final,
-                            cudaStream_t s) {
-    finalize_kernel<<<1, 32, 0, s>>>(T, final_row, st, dev_final);
+#ifdef DFA_TREE_TIMING
+extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, g_tree_t, sizeof(unsigned long long) * 32) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long init[32];
+        init[0] = ~0ull;
+        for (int i = 1; i < 32; i++) init[i] = 0;
+        cudaMemcpyToSymbol(g_tree_t, init, sizeof(init));
+    }
+    return 0;
+}
+#endif
+
+cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s) {
+    tree_kernel<<<grid, 256, smem_bytes, s>>>(T, tr);
     return cudaGetLastError();
 }
 

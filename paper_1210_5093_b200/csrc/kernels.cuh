@@ -8,10 +8,11 @@
 //      lanes in registers through the rest of the sub-chunk (Alg.MatchingInitialStates
 //      lines 17-19), merging converged lanes and dropping lanes in
 //      absorbing states.
-//   3. compose_kernel: tree composition of sub-chunk maps into the reporting
-//      chunk maps, then of those into the final state (Eq.MapReduction,
-//      P:819-830, applied hierarchically: the on-GPU analog of Fig.Merge).
-//   4. finalize_kernel: final state, accept bit (Alg.seqmatch l.4-6), errors.
+//   3. tree_kernel: one launch composing the sub-chunk maps into the
+//      reporting chunk maps and those into the final state and its accept bit
+//      (Eq.MapReduction P:819-830 hierarchically -- the on-GPU analog of the
+//      two-tier merge of Fig.Merge -- with a last-arriver-continues rule per
+//      tree node instead of barriers; Alg.seqmatch l.4-6 at the root).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -30,12 +31,15 @@ struct DevTables {
     const uint16_t *dom_list;   // [(nclass+1) * imax] internal I_sigma, ascending
     const uint16_t *dom_size;   // [nclass+1]
     const uint16_t *rank;       // [(nclass+1) * nq] index in dom_list or 0xFFFF
+    const uint8_t *rank8;       // same as uint8 (0xFF = none) when imax < 255, else null
     const uint32_t *dead_bits;  // internal Z
     const uint32_t *absorb_bits;
     const uint32_t *accept_bits;
     const uint16_t *xlat;       // [nclass * imax_user]
     const uint16_t *dom_user_size; // [nclass]
     uint32_t nq, nclass, start_dom, imax, imax_user;
+    uint32_t rs;                // map row stride: imax rounded up to 8 (16-byte rows)
+    uint32_t has_dead;          // internal Z non-empty
     uint32_t stride, win_base, win_w;
     int mode;
     uint32_t q0, poison;
@@ -56,22 +60,6 @@ struct DevStatus {
     uint32_t pad;
 };
 
-struct LevelIn {
-    int kind;                // 0: sub-chunk maps (amap/sfin), 1: rows
-    const uint16_t *amap;    // kind 0, may be null
-    const uint16_t *sfin;
-    uint32_t sk;             // sfin row stride
-    const uint16_t *row0, *rows;
-    const uint16_t *dom;
-};
-
-struct LevelOut {
-    uint16_t *row0, *rows;   // internal rows; row(g) = g ? rows + (g-1)*imax : row0
-    uint16_t *dom;
-    uint16_t *user_rows;     // optional API rows (k >= 1) in the user's domain order
-    uint16_t *e0;            // optional chunk-0 end state
-};
-
 struct Shape {
     uint64_t f, m, S;        // segment 0 holds f maps, segments 1..S-1 hold m maps
     uint32_t G;              // max maps per group
@@ -80,6 +68,38 @@ struct Shape {
         uint64_t gm = S > 1 ? (m + G - 1) / G : 0;
         return gf + (S - 1) * gm;
     }
+};
+
+// Composition tree (Eq.MapReduction applied hierarchically, the on-GPU analog
+// of the paper's two-tier merge, Fig.Merge): level 0 = the sub-chunk maps
+// (leaves), level L >= 1 groups <= G consecutive level L-1 nodes that lie in
+// the same reporting chunk, up to one node per reporting chunk (rep_level),
+// then groups reporting chunk nodes up to the single root (final state).
+constexpr int kMaxLevels = 24;
+struct TreeLevel {            // all 32-bit: node counts stay far below 2^32
+    uint32_t f, m, S, G;     // shape of level L-1 (segment 0: f nodes, others m) and group size
+    uint32_t gf, gm;         // groups of segment 0 / of every other segment
+    uint32_t nodes;          // node count of this level
+    uint32_t off;            // offset of this level's nodes in rows/doms/counters
+};
+struct Tree {
+    uint32_t nlevels;        // levels 1..nlevels
+    uint32_t rep_level;      // its nodes are the reporting chunks 0..P-1
+    uint32_t F;              // staging capacity (children per node) of a warp
+    uint32_t lrs;            // log2 of the shared-memory row stride (>= T.rs)
+    int rank_smem;           // uint8 rank table staged in shared memory
+    int dbg;                 // debug experiment bits (0 in production)
+    TreeLevel lv[kMaxLevels + 1];
+    // leaves (lanes kernel output)
+    const uint16_t *amap, *sfin;
+    uint32_t sk;
+    const uint16_t *dom_of;
+    // nodes
+    uint16_t *rows, *doms;
+    uint32_t *counters;
+    // outputs
+    uint16_t *user_rows, *e0, *dev_final;
+    DevStatus *status;
 };
 
 struct LaunchCfg {
@@ -98,11 +118,11 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
 int lanes_smem_bytes(const DevTables &T);
 int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);
-cudaError_t launch_compose(const DevTables &T, const LevelIn &in, const LevelOut &out, const Shape &sh,
-                           DevStatus *st, int grid, cudaStream_t s);
-int compose_smem_bytes(const DevTables &T, uint32_t G);
-cudaError_t launch_finalize(const DevTables &T, const uint16_t *final_row, DevStatus *st,
-                            uint16_t *dev_final, cudaStream_t s);
+cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s);
+int tree_slice_bytes(const DevTables &T, uint32_t F);
+uint32_t tree_lrs(const DevTables &T);
+int tree_fixed_bytes(const DevTables &T, int rank_smem);
+const void *tree_fn();
 cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s);
 cudaError_t setup_kernel_attributes(const DevTables &T);

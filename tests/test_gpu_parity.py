@@ -318,3 +318,12 @@ def test_full_protein():
 @pytest.mark.slow
 def test_full_worst():
     full_size("worst", rows=2)
+
+
+@pytest.mark.parametrize("fanin", [2, 3, 17, 64])
+def test_tree_fanin(fanin):
+    """The composition tree's shape must not change any result."""
+    for name, n, P in (("random", 1 << 20, 1000), ("protein", 1 << 19, 300), ("tiny", 1 << 18, 64)):
+        w = W.get(name)
+        c = Case(w.automaton, w.input(n), name)
+        check_chunk_maps(c, P, opts={D.DFA_OPT_TREE_FANIN: fanin, D.DFA_OPT_SUBCHUNK_TARGET: 5000})
