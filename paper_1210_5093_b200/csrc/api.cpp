@@ -61,6 +61,7 @@ struct dfa_handle {
     // options
     int convergence = 1, profile = 0, threads = 512;
     uint32_t tree_fanin_cap = 32;
+    uint32_t walk_fanin = 8;
     int64_t subchunk_target = 0;
     // scratch
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
@@ -129,10 +130,14 @@ dfa_status upload(dfa_handle *h) {
             if (!rank8.empty()) rank8[(size_t)c * nq + p.dom[c][j]] = (uint8_t)j;
         }
     }
-    std::vector<uint16_t> xlat((size_t)nc * imu, 0), dom_user_size(nc, 0);
+    const uint32_t rs = (imax + 7) & ~7u;
+    std::vector<uint16_t> xlat((size_t)nc * imu, 0), dom_user_size(nc, 0), ixlat((size_t)nc * rs, kNone);
     for (uint32_t c = 0; c < nc; c++) {
         dom_user_size[c] = (uint16_t)p.dom_user[c].size();
-        for (uint32_t j = 0; j < p.xlat[c].size(); j++) xlat[(size_t)c * imu + j] = p.xlat[c][j];
+        for (uint32_t j = 0; j < p.xlat[c].size(); j++) {
+            xlat[(size_t)c * imu + j] = p.xlat[c][j];
+            ixlat[(size_t)c * rs + p.xlat[c][j]] = (uint16_t)j;
+        }
     }
     const uint32_t bw = ((nq + 31) / 32 + 3) & ~3u;
     std::vector<uint32_t> dead(bw, 0), absorb(bw, 0), accept(bw, 0);
@@ -156,6 +161,7 @@ dfa_status upload(dfa_handle *h) {
         {xlat.data(), xlat.size() * 2, 0},
         {dom_user_size.data(), dom_user_size.size() * 2, 0},
         {rank8.data(), rank8.size(), 0},
+        {ixlat.data(), ixlat.size() * 2, 0},
     };
     size_t total = 0;
     for (auto &s : secs) { s.off = total; total += (s.bytes + 255) & ~size_t(255); }
@@ -178,6 +184,7 @@ dfa_status upload(dfa_handle *h) {
     T.xlat = reinterpret_cast<const uint16_t *>(at(9));
     T.dom_user_size = reinterpret_cast<const uint16_t *>(at(10));
     T.rank8 = rank8.empty() ? nullptr : at(11);
+    T.ixlat = reinterpret_cast<const uint16_t *>(at(12));
     T.nq = nq;
     T.nclass = nc;
     T.start_dom = p.start_dom;
@@ -185,7 +192,9 @@ dfa_status upload(dfa_handle *h) {
     T.imax_user = imu;
     T.rs = (imax + 7) & ~7u;
     T.has_dead = 0;
+    T.has_absorb = 0;
     for (uint32_t q = 0; q < nq; q++) T.has_dead |= p.dead[q];
+    for (uint32_t q = 0; q < nq; q++) T.has_absorb |= p.absorbing[q];
     T.stride = p.stride;
     T.win_base = p.win_base;
     T.win_w = p.win_w;
@@ -251,6 +260,7 @@ uint32_t tree_fanin(const dfa_handle *h, int &rank_smem, int &smem_bytes) {
     const uint64_t fixed = (uint64_t)tree_fixed_bytes(T, rank_smem);
     const uint64_t budget = cap - fixed;
     uint32_t F = h->tree_fanin_cap;
+    if (T.rs > 16) F = std::min<uint32_t>(F, h->walk_fanin);  // walk_kernel chains: keep them short
     while (F > 2 && (uint64_t)tree_slice_bytes(T, F) * 8 > budget) F--;
     smem_bytes = (int)(fixed + (uint64_t)tree_slice_bytes(T, F) * 8);
     return F;
@@ -332,7 +342,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
         prof_begin(h, s, 1);
         CK(launch_lanes(T, plan, in, surv, surv_n, surv_pos, h->sfin.as<uint16_t>(), sk, h->dom_of.as<uint16_t>(),
-                        h->convergence, threads, (int)grid, s));
+                        h->convergence, const_cast<uint16_t *>(amap), threads, (int)grid, s));
         prof_end(h, s);
         kernels++;
     }
@@ -394,8 +404,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     tr.e0 = o.chunk0_end;
     tr.dev_final = o.final2;
     tr.status = h->status.as<DevStatus>();
-    {
-        const uint64_t warps = (tr.lv[1].nodes + 0);
+    if (T.rs <= 16) {
+        const uint64_t warps = tr.lv[1].nodes;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_fn(), 256, tree_smem);
         const uint64_t grid = std::min<uint64_t>((warps + 7) / 8, (uint64_t)h->sms * std::max(1, occ));
@@ -403,6 +413,14 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         CK(launch_tree(T, tr, (int)std::max<uint64_t>(1, grid), tree_smem, s));
         prof_end(h, s);
         kernels++;
+    } else {
+        // long rows: one entry-parallel launch per level (small fan-in, see tree_fanin)
+        prof_begin(h, s, 2);
+        for (uint32_t L = 1; L <= tr.nlevels; L++) {
+            CK(launch_walk(T, tr, L, h->sms, s));
+            kernels++;
+        }
+        prof_end(h, s);
     }
     if (o.starts) {
         const uint16_t *rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;

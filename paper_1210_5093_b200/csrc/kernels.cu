@@ -11,6 +11,7 @@
 #include "prep.h"
 
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 namespace dfa {
@@ -21,6 +22,18 @@ constexpr uint32_t kDone = 0xFFu;
 
 __device__ __forceinline__ bool test_bit(const uint32_t *bits, uint32_t q) {
     return (bits[q >> 5] >> (q & 31)) & 1u;
+}
+
+struct U8x32 { uint4 lo, hi; };
+
+// One full 32-byte sector per thread and request (sm_100 256-bit load).
+__device__ __forceinline__ U8x32 ldg32(const void *p) {
+    U8x32 v;
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                   "=r"(v.hi.w)
+                 : "l"(p));
+    return v;
 }
 
 __device__ __forceinline__ uint4 ldg16(const uint4 *p) {
@@ -194,16 +207,17 @@ __device__ __forceinline__ void finish_slot(uint32_t slot, uint32_t state, uint3
 }
 
 // Merge converged lanes, retire absorbing ones, compact.
-__device__ __forceinline__ void checkpoint(const uint32_t *absorb, uint32_t bias, uint32_t (&st)[kLanes],
+__device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_absorb, uint32_t bias,
+                                           uint32_t (&st)[kLanes],
                                            uint32_t (&own)[kLanes], uint32_t &nlive, uint16_t *out) {
     const uint32_t full = (1u << nlive) - 1u;
     uint32_t lm = full;
     if (nlive == 1) {
-        if (test_bit(absorb, st[0] - bias)) { finish_slot(0, st[0] - bias, own, out); lm = 0; }
+        if (has_absorb && test_bit(absorb, st[0] - bias)) { finish_slot(0, st[0] - bias, own, out); lm = 0; }
     } else {
 #pragma unroll
         for (int l = 0; l < kLanes; l++)
-            if (((lm >> l) & 1u) && test_bit(absorb, st[l] - bias)) {
+            if (has_absorb && ((lm >> l) & 1u) && test_bit(absorb, st[l] - bias)) {
                 finish_slot(l, st[l] - bias, own, out);
                 lm &= ~(1u << l);
             }
@@ -253,33 +267,49 @@ __device__ __forceinline__ void step_scalar(const Tab<MODE> &tab, uint32_t b, ui
 }
 
 template <int MODE>
-__device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *absorb, const uint8_t *in, uint64_t pos,
+__device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *absorb, bool has_absorb,
+                                          const uint8_t *in, uint64_t pos,
                           uint64_t end, uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t nl,
                           int convergence, uint16_t *out) {
     uint32_t nlive = nl;
     const uint8_t *ptr = in + pos;
     const uint8_t *endp = in + end;
-    // head: up to 15 bytes until 16-byte alignment
-    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 15u)) step_scalar(tab, *ptr++, st, nlive);
-    uint64_t nblk = (uint64_t)(endp - ptr) >> 4;
-    const uint4 *q = reinterpret_cast<const uint4 *>(ptr);
+    // head: up to 31 bytes until 32-byte alignment
+    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) step_scalar(tab, *ptr++, st, nlive);
+    const uint64_t nblk = (uint64_t)(endp - ptr) >> 5;
     if (nblk) {
-        uint4 cur = ldg16(q);
+        U8x32 cur = ldg32(ptr);
         for (uint64_t bi = 0; bi < nblk; bi++) {
-            uint4 nxt = cur;
-            if (bi + 1 < nblk) nxt = ldg16(q + bi + 1);
-            uint32_t bucket = __reduce_max_sync(__activemask(), nlive);
-            if (bucket <= 1) block16<1>(tab, cur, st);
-            else if (bucket <= 2) block16<2>(tab, cur, st);
-            else if (bucket <= 4) block16<4>(tab, cur, st);
-            else block16<8>(tab, cur, st);
-            if (convergence) {
-                checkpoint(absorb, tab.bias, st, own, nlive, out);
-                if (nlive == 0) return;
+            U8x32 nxt = cur;
+            if (bi + 1 < nblk) nxt = ldg32(ptr + 32 * (bi + 1));
+#pragma unroll
+            for (int half = 0; half < 2; half++) {
+                const uint4 v = half ? cur.hi : cur.lo;
+                // the warp steps max(live lanes) lanes (exact, 1..8): lanes converge fast
+                switch (__reduce_max_sync(__activemask(), nlive)) {
+                case 0:
+                case 1: block16<1>(tab, v, st); break;
+                case 2: block16<2>(tab, v, st); break;
+                case 3: block16<3>(tab, v, st); break;
+                case 4: block16<4>(tab, v, st); break;
+                case 5: block16<5>(tab, v, st); break;
+                case 6: block16<6>(tab, v, st); break;
+                case 7: block16<7>(tab, v, st); break;
+                default: block16<8>(tab, v, st); break;
+                }
+                if (convergence) {
+                    if (nlive > 1) {
+                        checkpoint(absorb, has_absorb, tab.bias, st, own, nlive, out);
+                        if (nlive == 0) return;
+                    } else if (has_absorb && half && (bi & 1) && nlive == 1 && test_bit(absorb, st[0] - tab.bias)) {
+                        finish_slot(0, st[0] - tab.bias, own, out);  // the lane is done
+                        return;
+                    }
+                }
             }
             cur = nxt;
         }
-        ptr += nblk * 16;
+        ptr += nblk * 32;
     }
     while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
     // remaining lanes: final state of the slot that carries them
@@ -299,7 +329,8 @@ __global__ void __launch_bounds__(512) lanes_kernel(DevTables T, Plan p, const u
                                                     const uint8_t *__restrict__ surv_n,
                                                     const uint64_t *__restrict__ surv_pos,
                                                     uint16_t *__restrict__ sfin, uint32_t sk,
-                                                    uint16_t *__restrict__ dom_of, int convergence) {
+                                                    uint16_t *__restrict__ dom_of, int convergence,
+                                                    uint16_t *__restrict__ amap) {
     extern __shared__ uint4 smem4[];
     uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
     __syncthreads();
@@ -331,8 +362,33 @@ __global__ void __launch_bounds__(512) lanes_kernel(DevTables T, Plan p, const u
                     own[l] = kDone;
                 }
             }
-            run_lanes<MODE>(tab, absorb, in, pos, end, st, own, nl, convergence,
+            run_lanes<MODE>(tab, absorb, T.has_absorb != 0, in, pos, end, st, own, nl, convergence,
                             sfin + i * sk + pass * kLanes);
+        }
+        if (surv) {
+            // resolve this sub-chunk's converge_kernel map in place: survivor code
+            // kSurvBase + e -> final state of survivor e (this thread just wrote them)
+            uint32_t fin[kLanes];
+#pragma unroll
+            for (int e = 0; e < kLanes; e++) fin[e] = (uint32_t)e < u ? sfin[i * sk + e] : 0u;
+            const uint32_t du = T.dom_size[dom];
+            uint4 *row = reinterpret_cast<uint4 *>(amap + i * T.rs);
+            for (uint32_t k = 0; k * 8 < du; k++) {
+                uint4 v = row[k];
+                uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int h = 0; h < 8; h++) {
+                    uint32_t a = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+                    if (a >= kSurvBase && a != kNone) {
+                        uint32_t f = 0;
+#pragma unroll
+                        for (int e = 0; e < kLanes; e++) f |= fin[e] & (0u - (uint32_t)(a - kSurvBase == (uint32_t)e));
+                        a = f;
+                    }
+                    w[h >> 1] = (w[h >> 1] & ~(0xFFFFu << (16 * (h & 1)))) | (a << (16 * (h & 1)));
+                }
+                row[k] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
         }
     }
 }
@@ -514,6 +570,19 @@ __device__ __forceinline__ uint32_t tree_child_dom(const Tree &tr, uint32_t Lc, 
     return Lc == 0 ? tr.dom_of[c] : __ldcg(tr.doms + tr.lv[Lc].off + c);
 }
 
+// L_a[j] <- L_b[rank_b(L_a[j])]; error states stay
+__device__ __forceinline__ void tree_compose_entry(const DevTables &T, const Tree &tr, const uint32_t *dead,
+                                                   const uint8_t *rank8, uint16_t *st, uint32_t lrs, uint32_t a,
+                                                   uint32_t b, uint32_t j, uint32_t db) {
+    const uint32_t s = st[(a << lrs) + j];
+    if (T.has_dead && test_bit(dead, s)) return;
+    uint32_t r;
+    if (rank8) { r = rank8[db * T.nq + s]; r = r == 0xFFu ? kNone : r; }
+    else r = __ldg(T.rank + (uint64_t)db * T.nq + s);
+    if (r == kNone) { atomicMax(&tr.status->err, 8u); r = 0; }
+    st[(a << lrs) + j] = st[(b << lrs) + r];
+}
+
 __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
     extern __shared__ uint4 smem4[];
 #ifdef DFA_TREE_TIMING
@@ -561,30 +630,24 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
                     reinterpret_cast<uint4 *>(st + (c << lrs))[k] = __ldcg(tree_child_row(tr, T, L - 1, c0 + c) + k);
             }
             __syncwarp();
-            if (L == 1 && tr.amap) {  // leaves after converge_kernel: resolve survivor codes
-                for (uint32_t t = lane; t < (nc << lrs); t += 32) {
-                    const uint32_t c = t >> lrs, r = t & (rsp - 1);
-                    const uint32_t a = st[t];
-                    if (r < dsz[dch[c]] && a >= kSurvBase && a != kNone)
-                        st[t] = tr.sfin[(uint64_t)(c0 + c) * tr.sk + (a - kSurvBase)];
-                }
-                __syncwarp();
-            }
             // pairwise tree over the children in the warp: in round `step`, map a
             // (a = 0, 2step, ...) absorbs map a+step: L_a <- L_{a+step} o L_a
             for (uint32_t step = 1; step < nc && !(tr.dbg & 1); step *= 2) {
                 const uint32_t npairs = (nc - step + 2 * step - 1) / (2 * step);
-                for (uint32_t t = lane; t < (npairs << lrs); t += 32) {
-                    const uint32_t p = t >> lrs, j = t & (rsp - 1);
-                    const uint32_t a = p * 2 * step, b = a + step;
-                    uint32_t s = st[(a << lrs) + j];
-                    if (j >= dsz[dch[a]] || (T.has_dead && test_bit(dead, s))) continue;
-                    const uint32_t d = dch[b];
-                    uint32_t r;
-                    if (rank8) { r = rank8[d * T.nq + s]; r = r == 0xFFu ? kNone : r; }
-                    else r = __ldg(T.rank + (uint64_t)d * T.nq + s);
-                    if (r == kNone) { atomicMax(&tr.status->err, 8u); r = 0; }
-                    st[(a << lrs) + j] = st[(b << lrs) + r];
+                if (lrs <= 4) {
+                    // short rows: (pair, entry) tasks packed across the lanes
+                    for (uint32_t t = lane; t < (npairs << lrs); t += 32) {
+                        const uint32_t p = t >> lrs, j = t & (rsp - 1);
+                        const uint32_t a = p * 2 * step, b = a + step;
+                        if (j >= dsz[dch[a]]) continue;  // padding of the compact row
+                        tree_compose_entry(T, tr, dead, rank8, st, lrs, a, b, j, dch[b]);
+                    }
+                } else {
+                    // long rows: lanes over the valid entries of one pair at a time
+                    for (uint32_t p = 0; p < npairs; p++) {
+                        const uint32_t a = p * 2 * step, b = a + step, ua = dsz[dch[a]], db = dch[b];
+                        for (uint32_t j = lane; j < ua; j += 32) tree_compose_entry(T, tr, dead, rank8, st, lrs, a, b, j, db);
+                    }
                 }
                 __syncwarp();
             }
@@ -647,6 +710,72 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
             node = parent;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// walk_kernel: one level of the same composition tree for long rows (large
+// I_max), one thread per (node, entry): the entry is pushed through the node's
+// children in order, each step one rank lookup and one row lookup
+// (Eq.MapReduction / Eq.SeqReduction).  One launch per level; the
+// chains are short (the host picks small fan-ins) and there are
+// nodes * I_max independent ones, so the level is latency-hidden by numbers.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) walk_kernel(DevTables T, Tree tr, uint32_t L) {
+    const TreeLevel lv = tr.lv[L];
+    const uint64_t total = (uint64_t)lv.nodes * T.rs;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t node = (uint32_t)(t / T.rs), j = (uint32_t)(t - (uint64_t)node * T.rs);
+        uint32_t c0, c1;
+        group_range(lv, node, c0, c1);
+        const uint32_t d0 = tree_child_dom(tr, L - 1, c0);
+        const uint32_t u = T.dom_size[d0];
+        uint32_t s = kNone;
+        if (j < u) {
+            s = reinterpret_cast<const uint16_t *>(tree_child_row(tr, T, L - 1, c0))[j];
+            for (uint32_t c = c0 + 1; c < c1; c++) {
+                if (T.has_dead && test_bit(T.dead_bits, s)) continue;
+                const uint32_t d = tree_child_dom(tr, L - 1, c);
+                uint32_t r;
+                if (T.rank8) { r = __ldg(T.rank8 + (uint64_t)d * T.nq + s); r = r == 0xFFu ? kNone : r; }
+                else r = __ldg(T.rank + (uint64_t)d * T.nq + s);
+                if (r == kNone) { atomicMax(&tr.status->err, 8u); s = 0; break; }
+                s = reinterpret_cast<const uint16_t *>(tree_child_row(tr, T, L - 1, c))[r];
+            }
+        }
+        tr.rows[(uint64_t)(lv.off + node) * T.rs + j] = (uint16_t)s;
+        if (j == 0) tr.doms[lv.off + node] = (uint16_t)d0;
+        if (L == tr.rep_level) {
+            if (tr.user_rows && node > 0 && j < T.imax_user) {
+                // API row: user entry ju = internal entry xlat[ju]; padding 0xFFFF
+                const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : 0;
+                uint16_t *urow = tr.user_rows + (uint64_t)(node - 1) * T.imax_user;
+                if (j >= du) urow[j] = kNone;
+            }
+            if (tr.user_rows && node > 0 && j < u && d0 < T.nclass) {
+                const uint32_t ju = T.ixlat[(uint64_t)d0 * T.rs + j];
+                if (ju != kNone) tr.user_rows[(uint64_t)(node - 1) * T.imax_user + ju] = (uint16_t)s;
+            }
+            if (tr.e0 && node == 0 && j == 0) tr.e0[0] = (uint16_t)s;
+        }
+        if (L == tr.nlevels && node == 0 && j == 0) {
+            DevStatus *S = tr.status;
+            if (s == T.poison) atomicMax(&S->err, 5u);
+            S->final_state = s;
+            S->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
+            if (tr.dev_final) {
+                tr.dev_final[0] = (uint16_t)s;
+                tr.dev_final[1] = (uint16_t)S->accept;
+            }
+        }
+    }
+}
+
+cudaError_t launch_walk_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
+    const uint64_t total = (uint64_t)tr.lv[L].nodes * T.rs;
+    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
+    walk_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -769,9 +898,10 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
-                         uint16_t *dom_of, int convergence, int threads, int grid, cudaStream_t s) {
+                         uint16_t *dom_of, int convergence, uint16_t *amap, int threads, int grid,
+                         cudaStream_t s) {
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
-                    (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence};
+                    (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap};
     return cudaLaunchKernel(lanes_fn(T.mode), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
 }
 
@@ -789,6 +919,10 @@ extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {
     return 0;
 }
 #endif
+
+cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
+    return launch_walk_level(T, tr, L, sms, s);
+}
 
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s) {
     tree_kernel<<<grid, 256, smem_bytes, s>>>(T, tr);

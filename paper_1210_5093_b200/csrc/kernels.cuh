@@ -36,10 +36,12 @@ struct DevTables {
     const uint32_t *absorb_bits;
     const uint32_t *accept_bits;
     const uint16_t *xlat;       // [nclass * imax_user]
+    const uint16_t *ixlat;      // [nclass * rs]: user index of internal entry j, or 0xFFFF
     const uint16_t *dom_user_size; // [nclass]
     uint32_t nq, nclass, start_dom, imax, imax_user;
     uint32_t rs;                // map row stride: imax rounded up to 8 (16-byte rows)
     uint32_t has_dead;          // internal Z non-empty
+    uint32_t has_absorb;        // some state absorbs every byte
     uint32_t stride, win_base, win_w;
     int mode;
     uint32_t q0, poison;
@@ -114,11 +116,13 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 int converge_smem_bytes(const DevTables &T, int warps_per_cta);
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
-                         uint16_t *dom_of, int convergence, int threads, int grid, cudaStream_t s);
+                         uint16_t *dom_of, int convergence, uint16_t *amap, int threads, int grid,
+                         cudaStream_t s);
 int lanes_smem_bytes(const DevTables &T);
 int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s);
+cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
 int tree_slice_bytes(const DevTables &T, uint32_t F);
 uint32_t tree_lrs(const DevTables &T);
 int tree_fixed_bytes(const DevTables &T, int rank_smem);
