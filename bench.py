@@ -175,7 +175,7 @@ def main():
     a = w.automaton
     n = args.n or w.full_n
     P = args.chunks or w.chunks
-    x = w.input(n) if rank == 0 else W.CONFIGS[args.config](args.seed + rank).input(n)
+    x = w.input(n, segment=rank)
     dx = torch.from_numpy(x).to(dev)
 
     d = D.Dfa(a.table, a.q0, a.accept_bitmap)
@@ -191,13 +191,16 @@ def main():
     stream = torch.cuda.current_stream(dev)
     seg = None
     if world > 1:
+        # weak scaling: this rank's input is segment `rank` of one N-segment string
         from paper_1210_5093_b200 import multi_gpu
-        seg = multi_gpu.SegmentMatcher(d, dx, rank, world, dist)
+        smap, fold = multi_gpu.gpu_ops(d, dx, stream=stream)
+        seg = multi_gpu.SegmentMatcher(rank, world, dist, dx[-1:], smap, fold)
 
     def step():
-        D.dfa_chunk_maps(d.h, dx, P, bounds, e0, maps, None, final, stream=stream)
         if seg is not None:
-            seg.step(stream)
+            seg.step()      # segment map, one all-gather of I_max uint16 per rank, fold
+        else:
+            D.dfa_chunk_maps(d.h, dx, P, bounds, e0, maps, None, final, stream=stream)
 
     for _ in range(max(3, args.warmup)):
         step()

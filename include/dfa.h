@@ -170,6 +170,23 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
                              uint16_t *dev_chunk0_end, uint16_t *dev_maps,
                              uint16_t *dev_chunk_start, uint16_t *dev_final);
 
+/*
+ * Multi-GPU sharding (the paper's two-tier merge, Fig.Merge
+ * P:1530-1647, with NVLink in place of MPI).  A segment g of a longer input
+ * x = x_0 x_1 ... x_{G-1} is matched on its own GPU:
+ * dfa_segment_map writes dev_row[i_max] = the composed map of the segment over
+ * I_sigma of `lookahead` = the last byte of segment g-1 (ascending, 0xFFFF
+ * padded), or, for lookahead = -1 (segment 0), dev_row[0] = delta-hat(q0, x_0).
+ * After the G rows are gathered (one allgather of G*i_max uint16),
+ * dfa_fold_segments folds them in order (Eq.SeqReduction) into dev_final =
+ * {final state, accept} (asynchronous; errors via dfa_get_last_device_error).
+ * dev_lookahead[g] (device, G bytes) = last byte of segment g-1 (entry 0 unused).
+ */
+dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, int32_t lookahead,
+                           void *stream, uint16_t *dev_row);
+dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uint8_t *dev_lookahead,
+                             uint32_t G, void *stream, uint16_t *dev_final);
+
 /* After a stream sync: DFA_ERR_SYMBOL / DFA_ERR_INTERNAL raised by the last
  * asynchronous call's kernels, else DFA_OK.  Clears the flag. */
 dfa_status dfa_get_last_device_error(dfa_handle_t h);

@@ -21,7 +21,7 @@ __all__ = [
     "DfaError", "dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
     "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
     "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
-    "dfa_status_string", "dfa_error_detail", "Dfa", "lib", "EXPORTED",
+    "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments", "Dfa", "lib", "EXPORTED",
 ]
 
 DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
@@ -56,7 +56,7 @@ class DfaError(RuntimeError):
 EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
             "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
             "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
-            "dfa_status_string", "dfa_error_detail"]
+            "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments"]
 
 _lib = None
 
@@ -85,6 +85,8 @@ def lib():
             "dfa_get_last_device_error": [V],
             "dfa_set_option": [V, u32, ctypes.c_int64],
             "dfa_get_stats": [V, V],
+            "dfa_segment_map": [V, V, u64, ctypes.c_int32, V, V],
+            "dfa_fold_segments": [V, V, V, u32, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -218,6 +220,18 @@ def dfa_chunk_maps_at(h, dev_input, P: int, dev_bounds_in, dev_chunk0_end, dev_m
     _ck(lib().dfa_chunk_maps_at(h, _ptr(dev_input), n, int(P), _ptr(dev_bounds_in), _stream(stream),
                                 _ptr(dev_chunk0_end), _ptr(dev_maps), _ptr(dev_chunk_start), _ptr(dev_final)),
         "dfa_chunk_maps_at")
+
+
+def dfa_segment_map(h, dev_input, lookahead: int, dev_row, n: Optional[int] = None, stream=None):
+    """Map of one input segment over I_sigma(lookahead) (lookahead -1: from q0)."""
+    n = dev_input.numel() if n is None else int(n)
+    _ck(lib().dfa_segment_map(h, _ptr(dev_input), n, int(lookahead), _stream(stream), _ptr(dev_row)),
+        "dfa_segment_map")
+
+
+def dfa_fold_segments(h, dev_rows, dev_lookahead, G: int, dev_final, stream=None):
+    _ck(lib().dfa_fold_segments(h, _ptr(dev_rows), _ptr(dev_lookahead), int(G), _stream(stream), _ptr(dev_final)),
+        "dfa_fold_segments")
 
 
 def dfa_get_last_device_error(h) -> int:

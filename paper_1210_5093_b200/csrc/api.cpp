@@ -267,6 +267,8 @@ uint32_t tree_fanin(const dfa_handle *h, int &rank_smem, int &smem_bytes) {
 }
 
 struct Outputs {
+    uint32_t first_dom = 0xFFFFFFFFu; // domain of the first sub-chunk (default: {q0})
+    uint16_t *user_row0 = nullptr;   // [imax_user] map of chunk 0 in the user's order (segments)
     uint16_t *chunk0_end = nullptr;  // [1]
     uint16_t *user_maps = nullptr;   // [(P-1) * imax_user]
     uint16_t *starts = nullptr;      // [P]
@@ -300,7 +302,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     h->stats.input_bytes = 0;
     h->last_stream = s;
     CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
-    Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds};
+    Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
+              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;
@@ -403,6 +406,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     tr.user_rows = o.user_maps;
     tr.e0 = o.chunk0_end;
     tr.dev_final = o.final2;
+    tr.user_row0 = o.user_row0;
     tr.status = h->status.as<DevStatus>();
     if (T.rs <= 16) {
         const uint64_t warps = tr.lv[1].nodes;
@@ -635,7 +639,11 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     h->staging_pending = true;
     uint32_t m0, m;
     plan_split(h, len, P, hb, h->threads, m0, m);
-    Outputs o{dev_chunk0_end, P > 1 ? dev_maps : nullptr, dev_chunk_start, dev_final};
+    Outputs o;
+    o.chunk0_end = dev_chunk0_end;
+    o.user_maps = P > 1 ? dev_maps : nullptr;
+    o.starts = dev_chunk_start;
+    o.final2 = dev_final;
     return run(h, dev_input, len, P, dev_bounds, m0, m, s, o);
 }
 
@@ -654,8 +662,48 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
     if (hb[0] != 0 || hb[P] != len) return DFA_ERR_CHUNKS;
     for (uint32_t k = 0; k < P; k++)
         if (hb[k + 1] <= hb[k]) return DFA_ERR_CHUNKS;
-    Outputs o{dev_chunk0_end, P > 1 ? dev_maps : nullptr, dev_chunk_start, dev_final};
+    Outputs o;
+    o.chunk0_end = dev_chunk0_end;
+    o.user_maps = P > 1 ? dev_maps : nullptr;
+    o.starts = dev_chunk_start;
+    o.final2 = dev_final;
     return run(h, dev_input, len, P, dev_bounds_in, 1, 1, s, o);
+}
+
+dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, int32_t lookahead, void *stream,
+                           uint16_t *dev_row) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    if (!dev_input || !dev_row || len == 0 || lookahead < -1 || lookahead > 255) return DFA_ERR_ARG;
+    if (lookahead >= (int32_t)h->prep.ns) return DFA_ERR_SYMBOL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
+    CK(h->h_bounds.ensure(16));
+    CK(h->bounds.ensure(16));
+    uint64_t *hb = h->h_bounds.as<uint64_t>();
+    hb[0] = 0;
+    hb[1] = len;
+    CK(cudaMemcpyAsync(h->bounds.p, hb, 16, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(h->staging_done, s));
+    h->staging_pending = true;
+    uint32_t m0, m;
+    plan_split(h, len, 1, hb, h->threads, m0, m);
+    Outputs o;
+    o.first_dom = lookahead < 0 ? h->T.start_dom : h->prep.byte_class[lookahead];
+    o.user_row0 = dev_row;
+    return run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), m0, m, s, o);
+}
+
+dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uint8_t *dev_lookahead, uint32_t G,
+                             void *stream, uint16_t *dev_final) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    if (!dev_rows || !dev_lookahead || G == 0) return DFA_ERR_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    h->last_stream = s;
+    CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
+    CK(launch_fold_segments(h->T, dev_rows, dev_lookahead, G, h->status.as<DevStatus>(), dev_final, s));
+    return DFA_OK;
 }
 
 dfa_status dfa_get_last_device_error(dfa_handle_t h) {

@@ -57,9 +57,9 @@ __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s
 
 // Reverse lookahead: the domain of sub-chunk i is I_sigma with
 // sigma the byte before it; the very first sub-chunk starts from {q0}.
-__device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const uint8_t *in, uint64_t i,
+__device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const Plan &p, const uint8_t *in, uint64_t i,
                                                uint64_t start) {
-    return i == 0 ? T.start_dom : (uint32_t)T.byte_class[__ldg(in + start - 1)];
+    return i == 0 ? p.first_dom : (uint32_t)T.byte_class[__ldg(in + start - 1)];
 }
 
 // ---------------------------------------------------------------------------
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(512) lanes_kernel(DevTables T, Plan p, const u
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t start, end;
         sub_range(p, i, start, end);
-        const uint32_t dom = sub_domain(T, in, i, start);
+        const uint32_t dom = sub_domain(T, p, in, i, start);
         dom_of[i] = (uint16_t)dom;
         uint32_t u;
         uint64_t pos;
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
     for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; i < p.NS; i += warps_total) {
         uint64_t start, end;
         sub_range(p, i, start, end);
-        const uint32_t dom = sub_domain(T, in, i, start);
+        const uint32_t dom = sub_domain(T, p, in, i, start);
         const uint32_t u = T.dom_size[dom];
         for (uint32_t e = lane; e < u; e += 32) {
             pool_s[e] = T.dom_list[(uint64_t)dom * T.imax + e];
@@ -440,11 +440,12 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
         __syncwarp();
         while (np > (uint32_t)kLanes && pos < end) {
             // one window: the bytes [pos, min(next 16-byte boundary, end))
-            const uint64_t abase = pos & ~15ull;
+            // window [pos, next 16-byte boundary of the *address*, end)
+            const uint64_t abase = pos - ((reinterpret_cast<uintptr_t>(in) + pos) & 15u);
             const uint32_t k0 = (uint32_t)(pos - abase);
             const uint32_t k1 = (uint32_t)(end - abase < 16 ? end - abase : 16);
             uint4 v;
-            if (abase + 16 <= p.n) {
+            if (abase + 16 <= p.n && abase <= pos) {
                 v = ldg16(reinterpret_cast<const uint4 *>(in + abase));
             } else {  // last partial block of the input: byte loads, never past n
                 uint32_t wv[4] = {0, 0, 0, 0};
@@ -668,6 +669,12 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
                         urow[j] = j < du ? row[T.xlat[(uint64_t)d0 * T.imax_user + j]] : kNone;
                 }
                 if (tr.e0 && node == 0 && lane == 0) tr.e0[0] = row[0];
+                if (tr.user_row0 && node == 0) {
+                    const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+                    for (uint32_t j = lane; j < T.imax_user; j += 32)
+                        tr.user_row0[j] = j < du ? row[d0 < T.nclass ? T.xlat[(uint64_t)d0 * T.imax_user + j] : j]
+                                                 : kNone;
+                }
             }
 #ifdef DFA_TREE_TIMING
             if (lane == 0) atomicMax(&g_tree_t[L], gtimer());
@@ -757,6 +764,14 @@ __global__ void __launch_bounds__(256) walk_kernel(DevTables T, Tree tr, uint32_
                 if (ju != kNone) tr.user_rows[(uint64_t)(node - 1) * T.imax_user + ju] = (uint16_t)s;
             }
             if (tr.e0 && node == 0 && j == 0) tr.e0[0] = (uint16_t)s;
+            if (tr.user_row0 && node == 0) {
+                const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+                if (j < T.imax_user && j >= du) tr.user_row0[j] = kNone;
+                if (j < u) {
+                    const uint32_t ju = d0 < T.nclass ? T.ixlat[(uint64_t)d0 * T.rs + j] : j;
+                    if (ju != kNone) tr.user_row0[ju] = (uint16_t)s;
+                }
+            }
         }
         if (L == tr.nlevels && node == 0 && j == 0) {
             DevStatus *S = tr.status;
@@ -776,6 +791,35 @@ cudaError_t launch_walk_level(const DevTables &T, const Tree &tr, uint32_t L, in
     const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
     walk_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
     return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// fold_segments_kernel: the top of the multi-GPU merge (the
+// master step of Fig.Merge): segment g's map is a row over the
+// user's I_sigma of lookahead byte lookahead[g] (segment 0: over {q0});
+// Eq.SeqReduction over the G rows, then Alg.seqmatch l.4-6.
+// ---------------------------------------------------------------------------
+__global__ void fold_segments_kernel(DevTables T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
+                                     DevStatus *status, uint16_t *dev_final) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t s = rows[0];
+    for (uint32_t g = 1; g < G; g++) {
+        if (s == kNone || test_bit(T.dead_bits, s)) continue;
+        const uint32_t d = T.byte_class[lookahead[g]];
+        const uint32_t r = T.rank[(uint64_t)d * T.nq + s];
+        const uint32_t ju = r == kNone ? kNone : T.ixlat[(uint64_t)d * T.rs + r];
+        if (ju == kNone) { atomicMax(&status->err, 8u); break; }
+        s = rows[(uint64_t)g * T.imax_user + ju];
+    }
+    uint32_t err = status->err;
+    if (s == T.poison) err = max(err, 5u);
+    status->err = err;
+    status->final_state = s;
+    status->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
+    if (dev_final) {
+        dev_final[0] = (uint16_t)s;
+        dev_final[1] = (uint16_t)status->accept;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -919,6 +963,12 @@ extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {
     return 0;
 }
 #endif
+
+cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
+                                 DevStatus *st, uint16_t *dev_final, cudaStream_t s) {
+    fold_segments_kernel<<<1, 32, 0, s>>>(T, rows, lookahead, G, st, dev_final);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
     return launch_walk_level(T, tr, L, sms, s);

@@ -53,6 +53,7 @@ struct Plan {
     uint32_t m0, m;          // sub-chunks in chunk 0 / in every chunk k >= 1
     uint64_t NS;             // m0 + (P-1) m
     const uint64_t *bounds;  // device [P+1]
+    uint32_t first_dom;      // domain of sub-chunk 0: start_dom ({q0}) or a lookahead class
 };
 
 struct DevStatus {
@@ -101,6 +102,7 @@ struct Tree {
     uint32_t *counters;
     // outputs
     uint16_t *user_rows, *e0, *dev_final;
+    uint16_t *user_row0;     // optional API row of reporting chunk 0 (segment maps)
     DevStatus *status;
 };
 
@@ -130,6 +132,8 @@ const void *tree_fn();
 cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s);
 cudaError_t setup_kernel_attributes(const DevTables &T);
+cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
+                                 DevStatus *st, uint16_t *dev_final, cudaStream_t s);
 int probe_dynamic_smem_base(uint32_t *dev_scratch);
 
 } // namespace dfa

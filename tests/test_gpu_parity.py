@@ -327,3 +327,56 @@ def test_tree_fanin(fanin):
         w = W.get(name)
         c = Case(w.automaton, w.input(n), name)
         check_chunk_maps(c, P, opts={D.DFA_OPT_TREE_FANIN: fanin, D.DFA_OPT_SUBCHUNK_TARGET: 5000})
+
+
+@pytest.mark.parametrize("name,G", [("random", 4), ("keyword", 3), ("protein", 2), ("worst", 2), ("tiny", 8)])
+def test_segment_maps_fold(name, G):
+    """Sharded path kernels on one GPU: G segment maps (dfa_segment_map) folded
+    by dfa_fold_segments == the sequential run; rows == the oracle's chunk maps."""
+    w = W.get(name)
+    n = 1 << 19
+    x = w.input(n)
+    c = Case(w.automaton, x, name)
+    rng = np.random.default_rng(G)
+    cuts = np.sort(rng.choice(np.arange(1, n), G - 1, replace=False))
+    b = np.concatenate([[0], cuts, [n]]).astype(np.uint64)
+    d = c.handle()
+    try:
+        imax = d.info["i_max"]
+        dx = torch.from_numpy(x).to(DEV)
+        rows = torch.empty(G, imax, dtype=torch.int16, device=DEV)
+        la = np.zeros(G, np.uint8)
+        for g in range(G):
+            lo, hi = int(b[g]), int(b[g + 1])
+            look = -1 if g == 0 else int(x[lo - 1])
+            la[g] = max(look, 0)
+            D.dfa_segment_map(d.h, dx[lo:hi], look, rows[g])
+        final = torch.empty(2, dtype=torch.int16, device=DEV)
+        D.dfa_fold_segments(d.h, rows, torch.from_numpy(la).to(DEV), G, final)
+        torch.cuda.synchronize()
+        assert D.dfa_get_last_device_error(d.h) == 0
+        r = u16(rows)
+        fin = c.od.run(x)
+        assert u16(final).tolist() == [fin, int(c.a.accepting[fin])]
+        assert r[0][0] == c.od.run(x[:int(b[1])])
+        for g in range(1, G):
+            row, _ = c.od.chunk_map(x, int(b[g]), int(b[g + 1]), imax)
+            assert np.array_equal(r[g], row), g
+    finally:
+        d.close()
+
+
+@pytest.mark.parametrize("off", [1, 5, 15, 31])
+def test_misaligned_input(off):
+    """Input pointers need no alignment (head bytes before the first 32-byte sector)."""
+    for name in ("random", "protein"):
+        w = W.get(name)
+        x = w.input((1 << 18) + 77)
+        full = torch.from_numpy(x).to(DEV)
+        c = Case(w.automaton, x[off:], name)
+        check_chunk_maps(c, 97, dev=full[off:])
+        d = c.handle()
+        try:
+            assert d.match(full[off:])[0] == c.od.run(x[off:])
+        finally:
+            d.close()

@@ -32,9 +32,11 @@ class Workload:
     make_input: Callable[[int], np.ndarray]
     info: Dict = field(default_factory=dict)
 
-    def input(self, n: Optional[int] = None, out=None) -> np.ndarray:
+    def input(self, n: Optional[int] = None, out=None, segment: int = 0) -> np.ndarray:
+        """n input bytes; segment s > 0 draws an independent continuation (same
+        automaton, input seed offset by s) -- segment s of a sharded input."""
         n = self.full_n if n is None else int(n)
-        return self.make_input(n) if out is None else self.make_input(n, out)
+        return self.make_input(n, out, segment)
 
 
 def tiny(seed: int = 0) -> Workload:
@@ -42,13 +44,13 @@ def tiny(seed: int = 0) -> Workload:
     aut = automata.aho_corasick([[0, 1, 2, 0], [1, 3, 3]], 4)
     aut.name = "tiny: AC(abca|bdd) over {a,b,c,d}"
     return Workload("tiny", aut, 4, 1 * MiB, 1 * MiB, 64,
-                    lambda n, out=None: inputs.uniform_over([0, 1, 2, 3], n, seed, out))
+                    lambda n, out=None, sg=0: inputs.uniform_over([0, 1, 2, 3], n, seed + 1000 * sg, out))
 
 
 def random_structured(seed: int = 0) -> Workload:
     aut = automata.random_structured(64, 256, 7, 16, seed)
     return Workload("random", aut, 256, 256 * MiB, 4 * MiB, 4096,
-                    lambda n, out=None: inputs.uniform_bytes(n, seed, out))
+                    lambda n, out=None, sg=0: inputs.uniform_bytes(n, seed + 1000 * sg, out))
 
 
 def keyword(seed: int = 0) -> Workload:
@@ -56,9 +58,9 @@ def keyword(seed: int = 0) -> Workload:
     aut = automata.aho_corasick([list(k) for k in kws], 256)
     aut.name = "keyword: AC of 32 random printable keywords"
 
-    def make(n, out=None):
-        x = inputs.zipf_printable(n, seed, 1.1, out)
-        inputs.plant(x, kws, 1e-6, seed)
+    def make(n, out=None, sg=0):
+        x = inputs.zipf_printable(n, seed + 1000 * sg, 1.1, out)
+        inputs.plant(x, kws, 1e-6, seed + 1000 * sg)
         return x
 
     return Workload("keyword", aut, 256, 1 * GiB, 4 * MiB, 16384, make,
@@ -68,14 +70,14 @@ def keyword(seed: int = 0) -> Workload:
 def protein(seed: int = 0) -> Workload:
     aut, motif, used = automata.protein_motif_dfa(seed)
     return Workload("protein", aut, 256, 4 * GiB, 2 * MiB, 4096,
-                    lambda n, out=None: inputs.uniform_over(automata.RESIDUES, n, seed, out),
+                    lambda n, out=None, sg=0: inputs.uniform_over(automata.RESIDUES, n, seed + 1000 * sg, out),
                     {"motif": automata.motif_text(motif), "motif_seed": used})
 
 
 def worst(seed: int = 0) -> Workload:
     aut = automata.random_structured(512, 256, 240, 128, seed)
     return Workload("worst", aut, 256, 10 * GiB, 1 * MiB, 16384,
-                    lambda n, out=None: inputs.uniform_bytes(n, seed, out))
+                    lambda n, out=None, sg=0: inputs.uniform_bytes(n, seed + 1000 * sg, out))
 
 
 CONFIGS = {
