@@ -59,7 +59,7 @@ struct dfa_handle {
     DevTables T{};
     uint32_t c_num = 1, c_den = 1;
     // options
-    int convergence = 1, profile = 0, threads = 512;
+    int convergence = 1, profile = 0, threads = 512, threads_auto = 1;
     uint32_t tree_fanin_cap = 32;
     uint32_t walk_fanin = 8;
     int64_t subchunk_target = 0;
@@ -275,6 +275,11 @@ struct Outputs {
     uint16_t *final2 = nullptr;      // [2]
 };
 
+int lanes_threads(const dfa_handle *h) {
+    if (h->threads_auto && lanes_occupancy(h->T, 512) < 2) return 1024;
+    return h->threads;
+}
+
 // Sub-chunk counts per reporting chunk from the host copy of the bounds.
 void plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb, int threads, uint32_t &m0,
                 uint32_t &m) {
@@ -340,7 +345,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         surv_pos = h->surv_pos.as<uint64_t>();
     }
     {
-        const int threads = h->threads;
+        // 2 x 512 or 1 x 1024 threads per SM: a big table (one CTA per SM) gets 1024
+        const int threads = lanes_threads(h);
         const int occ = std::max(1, lanes_occupancy(T, threads));
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
         prof_begin(h, s, 1);
@@ -595,7 +601,7 @@ dfa_status dfa_match(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, voi
     CK(cudaEventRecord(h->staging_done, s));
     h->staging_pending = true;
     uint32_t m0, m;
-    plan_split(h, len, 1, hb, h->threads, m0, m);
+    plan_split(h, len, 1, hb, lanes_threads(h), m0, m);
     Outputs o;
     st = run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), m0, m, s, o);
     if (st != DFA_OK) return st;
@@ -638,7 +644,7 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     CK(cudaEventRecord(h->staging_done, s));
     h->staging_pending = true;
     uint32_t m0, m;
-    plan_split(h, len, P, hb, h->threads, m0, m);
+    plan_split(h, len, P, hb, lanes_threads(h), m0, m);
     Outputs o;
     o.chunk0_end = dev_chunk0_end;
     o.user_maps = P > 1 ? dev_maps : nullptr;
@@ -687,7 +693,7 @@ dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t le
     CK(cudaEventRecord(h->staging_done, s));
     h->staging_pending = true;
     uint32_t m0, m;
-    plan_split(h, len, 1, hb, h->threads, m0, m);
+    plan_split(h, len, 1, hb, lanes_threads(h), m0, m);
     Outputs o;
     o.first_dom = lookahead < 0 ? h->T.start_dom : h->prep.byte_class[lookahead];
     o.user_row0 = dev_row;
@@ -726,8 +732,9 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
         h->tree_fanin_cap = (uint32_t)value;
         return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
+        h->threads_auto = value == 0;
         if (value == 0) value = 512;
-        if (value < 32 || value > 512 || value % 32) return DFA_ERR_ARG;
+        if (value < 32 || value > 1024 || value % 32) return DFA_ERR_ARG;
         h->threads = (int)value;
         return DFA_OK;
     }

@@ -324,7 +324,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(512) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                     const uint16_t *__restrict__ surv,
                                                     const uint8_t *__restrict__ surv_n,
                                                     const uint64_t *__restrict__ surv_pos,
