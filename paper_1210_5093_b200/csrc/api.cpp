@@ -308,7 +308,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     h->last_stream = s;
     CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
-              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom};
+              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;

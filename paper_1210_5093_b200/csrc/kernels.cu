@@ -46,13 +46,22 @@ __device__ __forceinline__ uint4 ldg16(const uint4 *p) {
 // Execution sub-chunk i -> [start, end): reporting chunk k is [b_k, b_{k+1})
 // (Eq.StartPosition/EndPosition, half-open, reading R5), split into m_k equal
 // parts (m_0 = m0, m_k = m for k >= 1).
+// Internal split points (j > 0) are moved down to a 32-byte aligned address
+// when the parts are long enough, so that a sub-chunk is whole 32-byte sectors
+// except at reporting-chunk bounds; the split is internal, results unchanged.
+__device__ __forceinline__ uint64_t split_point(const Plan &p, uint64_t b0, uint64_t len, uint64_t j, uint64_t mk) {
+    const uint64_t t = b0 + len * j / mk;
+    if (j == 0 || j == mk || len < 64 * mk) return t;
+    return t - ((p.in_addr + t) & 31u);
+}
+
 __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s, uint64_t &e) {
     uint64_t k, j, mk;
     if (i < p.m0) { k = 0; j = i; mk = p.m0; }
     else { uint64_t t = i - p.m0; k = 1 + t / p.m; j = t % p.m; mk = p.m; }
     uint64_t b0 = p.bounds[k], b1 = p.bounds[k + 1], len = b1 - b0;
-    s = b0 + len * j / mk;
-    e = b0 + len * (j + 1) / mk;
+    s = split_point(p, b0, len, j, mk);
+    e = split_point(p, b0, len, j + 1, mk);
 }
 
 // Reverse lookahead: the domain of sub-chunk i is I_sigma with
@@ -438,12 +447,14 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
         uint32_t np = u;
         uint64_t pos = start;
         __syncwarp();
+        uint32_t wlen = 16;  // merge every 16 bytes (merging is dearer than stepping: measured)
         while (np > (uint32_t)kLanes && pos < end) {
-            // one window: the bytes [pos, min(next 16-byte boundary, end))
-            // window [pos, next 16-byte boundary of the *address*, end)
+            // window [pos, min(pos + wlen, next 16-byte boundary of the *address*, end))
             const uint64_t abase = pos - ((reinterpret_cast<uintptr_t>(in) + pos) & 15u);
             const uint32_t k0 = (uint32_t)(pos - abase);
-            const uint32_t k1 = (uint32_t)(end - abase < 16 ? end - abase : 16);
+            uint32_t k1 = (uint32_t)(end - abase < 16 ? end - abase : 16);
+            k1 = min(k1, k0 + wlen);
+            wlen = min(wlen * 2, 16u);
             uint4 v;
             if (abase + 16 <= p.n && abase <= pos) {
                 v = ldg16(reinterpret_cast<const uint4 *>(in + abase));

@@ -54,6 +54,7 @@ struct Plan {
     uint64_t NS;             // m0 + (P-1) m
     const uint64_t *bounds;  // device [P+1]
     uint32_t first_dom;      // domain of sub-chunk 0: start_dom ({q0}) or a lookahead class
+    uint64_t in_addr;        // device address of the input (split alignment)
 };
 
 struct DevStatus {
