@@ -200,7 +200,9 @@ enum {
     DFA_OPT_CONVERGENCE = 2,     /* 1 = merge converged lanes (default), 0 = off */
     DFA_OPT_PROFILE = 3,         /* 1 = record per-kernel CUDA-event times */
     DFA_OPT_THREADS_PER_CTA = 4, /* match kernel CTA size (0 = auto) */
-    DFA_OPT_TREE_FANIN = 5       /* max children per composition-tree node, 2..64 (default 32) */
+    DFA_OPT_TREE_FANIN = 5,      /* max children per composition-tree node, 2..64 (default 32) */
+    DFA_OPT_FOLD_IN_TREE = 6,    /* 1: fold the chunk maps in tree_kernel instead of fold_rows_kernel */
+    DFA_OPT_WARP_COMPOSE = 7     /* 1 (default): maps of <= 8 entries composed in the match kernel's warps */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 

@@ -29,6 +29,8 @@ DFA_ERR_SYMBOL, DFA_ERR_OOM, DFA_ERR_CUDA, DFA_ERR_INTERNAL = 5, 6, 7, 8
 DFA_CREATE_HOST_ONLY = 1
 DFA_OPT_SUBCHUNK_TARGET, DFA_OPT_CONVERGENCE, DFA_OPT_PROFILE, DFA_OPT_THREADS_PER_CTA = 1, 2, 3, 4
 DFA_OPT_TREE_FANIN = 5
+DFA_OPT_FOLD_IN_TREE = 6
+DFA_OPT_WARP_COMPOSE = 7
 TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16"}
 
 

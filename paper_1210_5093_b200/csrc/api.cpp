@@ -65,7 +65,11 @@ struct dfa_handle {
     int64_t subchunk_target = 0;
     // scratch
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
-    DevBuf lvlA, domA, counters, bounds, input;
+    DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
+    int warp_compose = 1;
+    std::vector<uint64_t> plan_key;
+    struct { uint32_t m0, m, g_log; int threads; } plan_split_c{};
+    int fold_in_tree = 0;
     std::vector<uint64_t> tree_sig;
     HostPinned h_status, h_bounds;
     cudaEvent_t staging_done = nullptr;
@@ -90,7 +94,7 @@ dfa_status cuda_status(cudaError_t e) {
     return DFA_ERR_CUDA;
 }
 
-thread_local char g_detail[256] = "";
+thread_local char g_detail[512] = "";
 
 dfa_status cuda_fail(cudaError_t e, const char *expr, int line) {
     std::snprintf(g_detail, sizeof g_detail, "%s (%s) at api.cpp:%d: %s", cudaGetErrorName(e),
@@ -257,6 +261,7 @@ uint32_t tree_fanin(const dfa_handle *h, int &rank_smem, int &smem_bytes) {
     // stage the uint8 rank table in shared memory when it leaves room for F >= 8
     rank_smem = 0;
     if (T.rank8 && (uint64_t)tree_fixed_bytes(T, 1) + (uint64_t)tree_slice_bytes(T, 8) * 8 <= cap) rank_smem = 1;
+    if (getenv("DFA_TREE_DBG") && (atoi(getenv("DFA_TREE_DBG")) & 4)) rank_smem = 0;
     const uint64_t fixed = (uint64_t)tree_fixed_bytes(T, rank_smem);
     const uint64_t budget = cap - fixed;
     uint32_t F = h->tree_fanin_cap;
@@ -280,29 +285,80 @@ int lanes_threads(const dfa_handle *h) {
     return h->threads;
 }
 
-// Sub-chunk counts per reporting chunk from the host copy of the bounds.
-void plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb, int threads, uint32_t &m0,
-                uint32_t &m) {
+// Execution split of the P reporting chunks (chunk 0 into m0 sub-chunks, the
+// others into m): about one sub-chunk per resident thread.  For maps of <= 8
+// entries the split is in aligned groups of g = 2^g_log sub-chunks (m0, m
+// multiples of g, g | 32 or g = 32) that lanes_kernel composes in the warp.
+struct Split {
+    uint32_t m0 = 1, m = 1, g_log = kNoWarpGroup;
+    int threads = 512;
+};
+
+Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb, bool explicit_bounds) {
+    Split sp;
+    const int base_threads = lanes_threads(h);
+    const int bps = std::max(1, std::min(2, lanes_occupancy(h->T, 512)));
     uint64_t target = h->subchunk_target;
-    if (target <= 0) {
-        int occ = std::max(1, lanes_occupancy(h->T, threads));
-        target = (uint64_t)h->sms * occ * threads;
-    }
-    const uint64_t Ls = std::max<uint64_t>(32, (n + target - 1) / target);
+    if (target <= 0) target = (uint64_t)h->sms * std::max(1, lanes_occupancy(h->T, base_threads)) * base_threads;
     const uint64_t len0 = hb[1] - hb[0];
-    m0 = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (len0 + Ls / 2) / Ls), std::min<uint64_t>(len0, 1u << 30));
-    m = 1;
+    uint64_t minlen = len0, avg = len0;
     if (P > 1) {
-        uint64_t minlen = UINT64_MAX;
+        minlen = UINT64_MAX;
         for (uint32_t k = 1; k < P; k++) minlen = std::min(minlen, hb[k + 1] - hb[k]);
-        const uint64_t avg = (n - len0) / (P - 1);
-        m = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (avg + Ls / 2) / Ls), minlen);
+        avg = (n - len0) / (P - 1);
     }
+    const bool warp_mode = h->T.rs == 8 && h->warp_compose;
+    if (explicit_bounds) {
+        sp.m0 = sp.m = 1;
+        if (warp_mode) sp.g_log = 0;
+    } else if (!warp_mode) {
+        const uint64_t Ls = std::max<uint64_t>(32, (n + target - 1) / target);
+        sp.m0 = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (len0 + Ls / 2) / Ls), std::min<uint64_t>(len0, 1u << 30));
+        sp.m = P > 1 ? (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (avg + Ls / 2) / Ls), minlen) : 1;
+    } else {
+        // sub-chunks of >= 32 bytes; m a multiple of the largest power-of-two group
+        // g <= 32 that keeps >= 95% of the estimated split (whole groups per warp)
+        auto shape = [](uint64_t est) {
+            est = std::max<uint64_t>(est, 1);
+            for (uint64_t g = 32; g > 1; g /= 2)
+                if (est >= g && (est / g * g) * 100 >= est * 95) return (uint32_t)(est / g * g);
+            return (uint32_t)est;
+        };
+        auto group_of = [](uint32_t m) { uint32_t g = 1; while (g < 32 && m % (2 * g) == 0) g *= 2; return g; };
+        uint32_t g;
+        if (P == 1) {
+            sp.m0 = shape(std::min<uint64_t>(target, std::max<uint64_t>(1, len0 / 32)));
+            g = group_of(sp.m0);
+            sp.m = 1;
+        } else {
+            const double c = (double)len0 / (double)std::max<uint64_t>(avg, 1);
+            const uint64_t est = (uint64_t)((double)target / ((double)(P - 1) + c));
+            sp.m = shape(std::min<uint64_t>(est, std::max<uint64_t>(1, minlen / 32)));
+            g = group_of(sp.m);
+            uint64_t m0 = (uint64_t)((double)sp.m * c + 0.5);
+            m0 = std::max<uint64_t>(g, m0 / g * g);
+            while (m0 > len0 && m0 > g) m0 -= g;
+            while (len0 < m0 && g > 1) { g /= 2; m0 = std::max<uint64_t>(g, m0 / 2); }
+            if (sp.m % g) sp.m = std::max<uint32_t>(g, sp.m / g * g);  // chunk 0 too short: smaller groups
+            sp.m0 = (uint32_t)m0;
+        }
+        uint32_t gl = 0;
+        while ((1u << gl) < g) gl++;
+        sp.g_log = gl;
+    }
+    // threads per CTA: spread the sub-chunks evenly over all SMs (one wave when possible)
+    const uint64_t NS = (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m;
+    const int maxt = bps >= 2 ? 512 : 1024;
+    uint64_t t = (NS + (uint64_t)h->sms * bps - 1) / ((uint64_t)h->sms * bps);
+    t = (t + 31) / 32 * 32;
+    sp.threads = h->threads_auto ? (int)std::min<uint64_t>(std::max<uint64_t>(t, 128), (uint64_t)maxt) : base_threads;
+    return sp;
 }
 
 // Core: match `in` under the partition dev_bounds[P+1] (already on the device).
 dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const uint64_t *dev_bounds,
-               uint32_t m0, uint32_t m, cudaStream_t s, const Outputs &o) {
+               const Split &sp, cudaStream_t s, const Outputs &o) {
+    const uint32_t m0 = sp.m0, m = sp.m;
     DevTables &T = h->T;
     h->stats.input_bytes = 0;
     h->last_stream = s;
@@ -344,19 +400,25 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         surv_n = h->surv_n.as<uint8_t>();
         surv_pos = h->surv_pos.as<uint64_t>();
     }
+    const bool grouped = sp.g_log != kNoWarpGroup;
+    if (grouped) {
+        CK(h->leaf_rows.ensure(((NS >> sp.g_log) + 1) * T.rs * 2));
+        CK(h->leaf_dom.ensure(((NS >> sp.g_log) + 1) * 2));
+    }
     {
-        // 2 x 512 or 1 x 1024 threads per SM: a big table (one CTA per SM) gets 1024
-        const int threads = lanes_threads(h);
+        const int threads = sp.threads;
         const int occ = std::max(1, lanes_occupancy(T, threads));
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
         prof_begin(h, s, 1);
         CK(launch_lanes(T, plan, in, surv, surv_n, surv_pos, h->sfin.as<uint16_t>(), sk, h->dom_of.as<uint16_t>(),
-                        h->convergence, const_cast<uint16_t *>(amap), threads, (int)grid, s));
+                        h->convergence, const_cast<uint16_t *>(amap), sp.g_log, h->leaf_rows.as<uint16_t>(),
+                        h->leaf_dom.as<uint16_t>(), h->status.as<DevStatus>(), threads, (int)grid, s));
         prof_end(h, s);
         kernels++;
     }
-    // composition: sub-chunk maps -> reporting maps -> final state, one launch
+    // composition: sub-chunk maps -> reporting maps -> final state
     Tree tr{};
+    bool use_fold_rows = false;
     int tree_smem = 0;
     const uint32_t F = tree_fanin(h, tr.rank_smem, tree_smem);
     tr.F = F;
@@ -365,7 +427,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         uint32_t L = 0;
         uint64_t total = 0;
         struct Sh { uint64_t f, m, S; };
-        Sh cur{m0, P > 1 ? m : 0, P};
+        const uint32_t gl = grouped ? sp.g_log : 0;
+        Sh cur{m0 >> gl, P > 1 ? (m >> gl) : 0, P};
         bool overflow = false;
         auto add = [&](Sh prev, uint32_t G) {
             L++;
@@ -386,26 +449,30 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         if (cur.f == 1 && (cur.S == 1 || cur.m == 1)) cur = add(cur, 1);  // leaves are the chunks
         while (!overflow && !(cur.f == 1 && (cur.S == 1 || cur.m == 1))) cur = add(cur, F);
         tr.rep_level = L;
+        // short rows: the fold above the reporting chunks is fold_rows_kernel
+        // (whole CTAs, pairwise in shared memory); long rows: more tree levels
+        use_fold_rows = T.rs <= 16 && P > 1 && !h->fold_in_tree;
         Sh fold{P, 0, 1};
-        while (!overflow && fold.f > 1) fold = add(fold, F);
+        while (!overflow && !use_fold_rows && fold.f > 1) fold = add(fold, F);
         if (overflow || total >= (1ull << 31) || NS >= (1ull << 31)) return DFA_ERR_INTERNAL;
         tr.nlevels = L;
+        tr.root_final = use_fold_rows ? 0 : 1;
         tr.lrs = tree_lrs(T);
         CK(h->lvlA.ensure(total * T.rs * 2));
         CK(h->domA.ensure(total * 2));
         // arrival counters: valid across calls with the same tree (multiples of
         // the child counts), zeroed when the tree changes
-        std::vector<uint64_t> sig = {total, F, L, (uint64_t)m0, (uint64_t)m, (uint64_t)P};
+        std::vector<uint64_t> sig = {total, F, L, (uint64_t)m0, (uint64_t)m, (uint64_t)P, (uint64_t)gl};
         if (sig != h->tree_sig || h->counters.cap < total * 4) {
             CK(h->counters.ensure(total * 4));
             CK(cudaMemsetAsync(h->counters.p, 0, total * 4, s));
             h->tree_sig = sig;
         }
     }
-    tr.amap = amap;
-    tr.sfin = h->sfin.as<uint16_t>();
-    tr.sk = sk;
-    tr.dom_of = h->dom_of.as<uint16_t>();
+    tr.amap = grouped ? nullptr : amap;
+    tr.sfin = grouped ? h->leaf_rows.as<uint16_t>() : h->sfin.as<uint16_t>();
+    tr.sk = grouped ? T.rs : sk;
+    tr.dom_of = grouped ? h->leaf_dom.as<uint16_t>() : h->dom_of.as<uint16_t>();
     tr.rows = h->lvlA.as<uint16_t>();
     tr.doms = h->domA.as<uint16_t>();
     tr.counters = h->counters.as<uint32_t>();
@@ -421,8 +488,30 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         const uint64_t grid = std::min<uint64_t>((warps + 7) / 8, (uint64_t)h->sms * std::max(1, occ));
         prof_begin(h, s, 2);
         CK(launch_tree(T, tr, (int)std::max<uint64_t>(1, grid), tree_smem, s));
-        prof_end(h, s);
         kernels++;
+        if (use_fold_rows) {
+            const uint32_t lrs = tree_lrs(T);
+            const uint64_t budget = (uint64_t)h->optin_smem - 1024 - 64 - fold_rows_fixed_bytes(T);
+            // spread the rows over many SMs (single-SM issue rate bounds a lone CTA):
+            // about sqrt(P) rows per CTA, the last CTA folds the CTA maps
+            const uint32_t cap = (uint32_t)std::min<uint64_t>(budget / ((2ull << lrs) + 2), 8192);
+            uint32_t per_cta = 16;
+            while ((uint64_t)per_cta * per_cta < P && per_cta < cap) per_cta *= 2;
+            per_cta = std::min(per_cta, cap);
+            const uint32_t grid = (P + per_cta - 1) / per_cta;
+            CK(h->fold_rows.ensure((uint64_t)grid * T.rs * 2 + 256));
+            CK(h->fold_doms.ensure((uint64_t)grid * 2 + 256));
+            if (!h->ticket.p) {
+                CK(h->ticket.ensure(256));
+                CK(cudaMemsetAsync(h->ticket.p, 0, 256, s));
+            }
+            const uint16_t *rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
+            CK(launch_fold_rows(T, rep_rows, tr.doms + tr.lv[tr.rep_level].off, P, per_cta,
+                                h->fold_rows.as<uint16_t>(), h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(),
+                                h->status.as<DevStatus>(), o.final2, s));
+            kernels++;
+        }
+        prof_end(h, s);
     } else {
         // long rows: one entry-parallel launch per level (small fan-in, see tree_fanin)
         prof_begin(h, s, 2);
@@ -519,7 +608,8 @@ dfa_status dfa_destroy(dfa_handle_t h) {
     if (h->device_ready) {
         if (h->last_stream) cudaStreamSynchronize(h->last_stream);
         for (DevBuf *b : {&h->tables, &h->status, &h->sfin, &h->dom_of, &h->surv, &h->surv_n, &h->surv_pos,
-                          &h->amap, &h->lvlA, &h->domA, &h->counters, &h->bounds, &h->input})
+                          &h->amap, &h->lvlA, &h->domA, &h->counters, &h->bounds, &h->input, &h->fold_rows,
+                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds})
             b->release();
         h->h_status.release();
         h->h_bounds.release();
@@ -600,10 +690,9 @@ dfa_status dfa_match(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, voi
     CK(cudaMemcpyAsync(h->bounds.p, hb, 16, cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(h->staging_done, s));
     h->staging_pending = true;
-    uint32_t m0, m;
-    plan_split(h, len, 1, hb, lanes_threads(h), m0, m);
+    const Split sp = plan_split(h, len, 1, hb, false);
     Outputs o;
-    st = run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), m0, m, s, o);
+    st = run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), sp, s, o);
     if (st != DFA_OK) return st;
     DevStatus ds{};
     st = fetch_status(h, s, ds);
@@ -637,20 +726,34 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     if ((unsigned __int128)len * h->c_den < (unsigned __int128)h->c_num + (unsigned __int128)h->c_den * (P - 1))
         return DFA_ERR_CHUNKS;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    st = stage_bounds(h, len, P);
-    if (st != DFA_OK) return st;
-    const uint64_t *hb = h->h_bounds.as<uint64_t>();
-    CK(cudaMemcpyAsync(dev_bounds, hb, (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(h->staging_done, s));
-    h->staging_pending = true;
-    uint32_t m0, m;
-    plan_split(h, len, P, hb, lanes_threads(h), m0, m);
+    // the partition and its execution split depend on (n, P, c, options) only:
+    // computed once, kept on the device, copied device-to-device per call
+    const std::vector<uint64_t> key = {len, P, h->c_num, h->c_den, (uint64_t)h->subchunk_target,
+                                       (uint64_t)h->threads, (uint64_t)h->threads_auto, (uint64_t)h->warp_compose};
+    if (key != h->plan_key) {
+        st = stage_bounds(h, len, P);
+        if (st != DFA_OK) return st;
+        const uint64_t *hb = h->h_bounds.as<uint64_t>();
+        CK(h->plan_bounds.ensure((size_t)(P + 1) * 8));
+        CK(cudaMemcpyAsync(h->plan_bounds.p, hb, (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(h->staging_done, s));
+        h->staging_pending = true;
+        const Split sp0 = plan_split(h, len, P, hb, false);
+        h->plan_split_c = {sp0.m0, sp0.m, sp0.g_log, sp0.threads};
+        h->plan_key = key;
+    }
+    CK(cudaMemcpyAsync(dev_bounds, h->plan_bounds.p, (size_t)(P + 1) * 8, cudaMemcpyDeviceToDevice, s));
+    Split sp;
+    sp.m0 = h->plan_split_c.m0;
+    sp.m = h->plan_split_c.m;
+    sp.g_log = h->plan_split_c.g_log;
+    sp.threads = h->plan_split_c.threads;
     Outputs o;
     o.chunk0_end = dev_chunk0_end;
     o.user_maps = P > 1 ? dev_maps : nullptr;
     o.starts = dev_chunk_start;
     o.final2 = dev_final;
-    return run(h, dev_input, len, P, dev_bounds, m0, m, s, o);
+    return run(h, dev_input, len, P, dev_bounds, sp, s, o);
 }
 
 dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
@@ -673,7 +776,8 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
     o.user_maps = P > 1 ? dev_maps : nullptr;
     o.starts = dev_chunk_start;
     o.final2 = dev_final;
-    return run(h, dev_input, len, P, dev_bounds_in, 1, 1, s, o);
+    const Split sp = plan_split(h, len, P, hb.data(), true);
+    return run(h, dev_input, len, P, dev_bounds_in, sp, s, o);
 }
 
 dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, int32_t lookahead, void *stream,
@@ -692,12 +796,11 @@ dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t le
     CK(cudaMemcpyAsync(h->bounds.p, hb, 16, cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(h->staging_done, s));
     h->staging_pending = true;
-    uint32_t m0, m;
-    plan_split(h, len, 1, hb, lanes_threads(h), m0, m);
+    const Split sp = plan_split(h, len, 1, hb, false);
     Outputs o;
     o.first_dom = lookahead < 0 ? h->T.start_dom : h->prep.byte_class[lookahead];
     o.user_row0 = dev_row;
-    return run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), m0, m, s, o);
+    return run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), sp, s, o);
 }
 
 dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uint8_t *dev_lookahead, uint32_t G,
@@ -730,6 +833,12 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
     case DFA_OPT_TREE_FANIN:
         if (value < 2 || value > 64) return DFA_ERR_ARG;
         h->tree_fanin_cap = (uint32_t)value;
+        return DFA_OK;
+    case DFA_OPT_WARP_COMPOSE:
+        h->warp_compose = value ? 1 : 0;
+        return DFA_OK;
+    case DFA_OPT_FOLD_IN_TREE:
+        h->fold_in_tree = value ? 1 : 0;
         return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         h->threads_auto = value == 0;

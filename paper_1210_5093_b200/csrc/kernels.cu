@@ -19,6 +19,7 @@ namespace dfa {
 namespace {
 
 constexpr uint32_t kDone = 0xFFu;
+constexpr uint32_t kNoGroup = 0xFFFFFFFFu;
 
 __device__ __forceinline__ bool test_bit(const uint32_t *bits, uint32_t q) {
     return (bits[q >> 5] >> (q & 31)) & 1u;
@@ -209,25 +210,25 @@ __device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t 
 // A lane whose slot is `slot` finished: write its final state for every
 // original lane it carries (own[r] == slot).
 __device__ __forceinline__ void finish_slot(uint32_t slot, uint32_t state, uint32_t (&own)[kLanes],
-                                            uint16_t *out) {
+                                            uint32_t (&fin)[kLanes]) {
 #pragma unroll
     for (int r = 0; r < kLanes; r++)
-        if (own[r] == slot) { out[r] = (uint16_t)state; own[r] = kDone; }
+        if (own[r] == slot) { fin[r] = state; own[r] = kDone; }
 }
 
 // Merge converged lanes, retire absorbing ones, compact.
 __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_absorb, uint32_t bias,
                                            uint32_t (&st)[kLanes],
-                                           uint32_t (&own)[kLanes], uint32_t &nlive, uint16_t *out) {
+                                           uint32_t (&own)[kLanes], uint32_t &nlive, uint32_t (&fin)[kLanes]) {
     const uint32_t full = (1u << nlive) - 1u;
     uint32_t lm = full;
     if (nlive == 1) {
-        if (has_absorb && test_bit(absorb, st[0] - bias)) { finish_slot(0, st[0] - bias, own, out); lm = 0; }
+        if (has_absorb && test_bit(absorb, st[0] - bias)) { finish_slot(0, st[0] - bias, own, fin); lm = 0; }
     } else {
 #pragma unroll
         for (int l = 0; l < kLanes; l++)
             if (has_absorb && ((lm >> l) & 1u) && test_bit(absorb, st[l] - bias)) {
-                finish_slot(l, st[l] - bias, own, out);
+                finish_slot(l, st[l] - bias, own, fin);
                 lm &= ~(1u << l);
             }
 #pragma unroll
@@ -279,7 +280,7 @@ template <int MODE>
 __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *absorb, bool has_absorb,
                                           const uint8_t *in, uint64_t pos,
                           uint64_t end, uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t nl,
-                          int convergence, uint16_t *out) {
+                          int convergence, uint32_t (&fin)[kLanes]) {
     uint32_t nlive = nl;
     const uint8_t *ptr = in + pos;
     const uint8_t *endp = in + end;
@@ -308,10 +309,10 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
                 }
                 if (convergence) {
                     if (nlive > 1) {
-                        checkpoint(absorb, has_absorb, tab.bias, st, own, nlive, out);
+                        checkpoint(absorb, has_absorb, tab.bias, st, own, nlive, fin);
                         if (nlive == 0) return;
                     } else if (has_absorb && half && (bi & 1) && nlive == 1 && test_bit(absorb, st[0] - tab.bias)) {
-                        finish_slot(0, st[0] - tab.bias, own, out);  // the lane is done
+                        finish_slot(0, st[0] - tab.bias, own, fin);  // the lane is done
                         return;
                     }
                 }
@@ -328,7 +329,39 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
         uint32_t v = 0;
 #pragma unroll
         for (int l = 0; l < kLanes; l++) v |= st[l] & (0u - (uint32_t)(own[r] == (uint32_t)l));
-        out[r] = (uint16_t)(v - tab.bias);
+        fin[r] = v - tab.bias;
+    }
+}
+
+// Warp-level composition of g = 2^g_log consecutive sub-chunk maps (aligned
+// groups of lanes, one sub-chunk each): in round r, lane t (t % 2^(r+1) == 0)
+// absorbs the map of lane t + 2^r, L_t <- L_{t+2^r} o L_t (Eq.MapReduction),
+// with the partner's map taken by shuffles.  Maps are <= 8 entries in
+// registers; entries >= u are ignored.
+__device__ __forceinline__ void warp_compose(const DevTables &T, uint32_t mask, uint32_t g_log, uint32_t (&fin)[kLanes],
+                                             uint32_t &dom, uint32_t u, DevStatus *status) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t r = 0; r < g_log; r++) {
+        const uint32_t step = 1u << r;
+        uint32_t pm[kLanes];
+#pragma unroll
+        for (int e = 0; e < kLanes; e++) pm[e] = __shfl_down_sync(mask, fin[e], step);
+        const uint32_t pd = __shfl_down_sync(mask, dom, step);
+        if ((lane & ((2u << r) - 1)) != 0) continue;
+#pragma unroll
+        for (int j = 0; j < kLanes; j++) {
+            if ((uint32_t)j >= u) continue;
+            const uint32_t s = fin[j];
+            if (T.has_dead && test_bit(T.dead_bits, s)) continue;
+            uint32_t rr;
+            if (T.rank8) { rr = __ldg(T.rank8 + (uint64_t)pd * T.nq + s); rr = rr == 0xFFu ? kNone : rr; }
+            else rr = __ldg(T.rank + (uint64_t)pd * T.nq + s);
+            if (rr == kNone) { atomicMax(&status->err, 8u); rr = 0; }
+            uint32_t v = 0;
+#pragma unroll
+            for (int e = 0; e < kLanes; e++) v |= pm[e] & (0u - (uint32_t)(rr == (uint32_t)e));
+            fin[j] = v;
+        }
     }
 }
 
@@ -339,7 +372,9 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
                                                     const uint64_t *__restrict__ surv_pos,
                                                     uint16_t *__restrict__ sfin, uint32_t sk,
                                                     uint16_t *__restrict__ dom_of, int convergence,
-                                                    uint16_t *__restrict__ amap) {
+                                                    uint16_t *__restrict__ amap, uint32_t g_log,
+                                                    uint16_t *__restrict__ leaf_rows, uint16_t *__restrict__ leaf_dom,
+                                                    DevStatus *status) {
     extern __shared__ uint4 smem4[];
     uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
     __syncthreads();
@@ -371,8 +406,33 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
                     own[l] = kDone;
                 }
             }
-            run_lanes<MODE>(tab, absorb, T.has_absorb != 0, in, pos, end, st, own, nl, convergence,
-                            sfin + i * sk + pass * kLanes);
+            uint32_t fin[kLanes];
+#pragma unroll
+            for (int l = 0; l < kLanes; l++) fin[l] = kNone;
+            run_lanes<MODE>(tab, absorb, T.has_absorb != 0, in, pos, end, st, own, nl, convergence, fin);
+            if (g_log != kNoGroup) {
+                // maps of <= 8 entries: compose aligned groups of 2^g_log sub-chunks in
+                // the warp and write one leaf per group (no per-sub-chunk map in HBM)
+                const uint64_t wbase = i & ~31ull;
+                const uint32_t mask = wbase + 32 <= p.NS ? 0xffffffffu : ((1u << (uint32_t)(p.NS - wbase)) - 1u);
+                __syncwarp(mask);
+                uint32_t d = dom;
+                warp_compose(T, mask, g_log, fin, d, u, status);
+                if (((threadIdx.x & 31) & ((1u << g_log) - 1)) == 0) {
+                    const uint64_t leaf = i >> g_log;
+                    uint4 v;
+                    v.x = (fin[0] & 0xFFFFu) | (fin[1] << 16);
+                    v.y = (fin[2] & 0xFFFFu) | (fin[3] << 16);
+                    v.z = (fin[4] & 0xFFFFu) | (fin[5] << 16);
+                    v.w = (fin[6] & 0xFFFFu) | (fin[7] << 16);
+                    reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
+                    leaf_dom[leaf] = (uint16_t)d;
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < kLanes; l++)
+                    if ((uint32_t)l < nl) sfin[i * sk + pass * kLanes + l] = (uint16_t)fin[l];
+            }
         }
         if (surv) {
             // resolve this sub-chunk's converge_kernel map in place: survivor code
@@ -582,6 +642,52 @@ __device__ __forceinline__ uint32_t tree_child_dom(const Tree &tr, uint32_t Lc, 
     return Lc == 0 ? tr.dom_of[c] : __ldcg(tr.doms + tr.lv[Lc].off + c);
 }
 
+// One round of the pairwise composition of maps stored in shared memory
+// (row c at st + (c << lrs), domain dch[c]): map a = p * 2^(lstep+1) absorbs
+// map b = a + 2^lstep, L_a <- L_b o L_a (Eq.MapReduction).  Tasks (pair,
+// entry) are spread over nthr threads and batched U deep so that the U
+// dependent load chains (row entry -> rank -> row entry) overlap.  Tasks of a
+// round read b rows and write a rows only, so batching is race-free.
+template <int U>
+__device__ __forceinline__ void pairwise_round(const DevTables &T, const uint8_t *rank8, const uint32_t *dead,
+                                               const uint16_t *dsz, const uint16_t *dch, uint16_t *st,
+                                               uint32_t lrs, uint32_t lstep, uint32_t npairs, uint32_t tid,
+                                               uint32_t nthr, DevStatus *status) {
+    const uint32_t rsp = 1u << lrs, ntasks = npairs << lrs;
+    for (uint32_t t0 = tid; t0 < ntasks; t0 += nthr * U) {
+        uint32_t dst[U], s[U], d[U];
+        bool ok[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const uint32_t t = t0 + q * nthr;
+            const uint32_t p = t >> lrs, j = t & (rsp - 1);
+            const uint32_t a = p << (lstep + 1), b = a + (1u << lstep);
+            ok[q] = t < ntasks && j < dsz[dch[a]];
+            dst[q] = (a << lrs) + j;
+            s[q] = ok[q] ? st[dst[q]] : 0u;
+            d[q] = ok[q] ? ((uint32_t)dch[b] | (b << 16)) : 0u;
+            if (ok[q] && T.has_dead && test_bit(dead, s[q])) ok[q] = false;
+        }
+        uint32_t r[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            if (!ok[q]) { r[q] = 0; continue; }
+            const uint32_t db = d[q] & 0xFFFFu;
+            uint32_t v;
+            if (rank8) { v = rank8[db * T.nq + s[q]]; v = v == 0xFFu ? kNone : v; }
+            else v = __ldg(T.rank + (uint64_t)db * T.nq + s[q]);
+            if (v == kNone) { atomicMax(&status->err, 8u); v = 0; }
+            r[q] = v;
+        }
+        uint32_t out[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) out[q] = ok[q] ? st[((d[q] >> 16) << lrs) + r[q]] : 0u;
+#pragma unroll
+        for (int q = 0; q < U; q++)
+            if (ok[q]) st[dst[q]] = (uint16_t)out[q];
+    }
+}
+
 // L_a[j] <- L_b[rank_b(L_a[j])]; error states stay
 __device__ __forceinline__ void tree_compose_entry(const DevTables &T, const Tree &tr, const uint32_t *dead,
                                                    const uint8_t *rank8, uint16_t *st, uint32_t lrs, uint32_t a,
@@ -647,13 +753,10 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
             for (uint32_t step = 1; step < nc && !(tr.dbg & 1); step *= 2) {
                 const uint32_t npairs = (nc - step + 2 * step - 1) / (2 * step);
                 if (lrs <= 4) {
-                    // short rows: (pair, entry) tasks packed across the lanes
-                    for (uint32_t t = lane; t < (npairs << lrs); t += 32) {
-                        const uint32_t p = t >> lrs, j = t & (rsp - 1);
-                        const uint32_t a = p * 2 * step, b = a + step;
-                        if (j >= dsz[dch[a]]) continue;  // padding of the compact row
-                        tree_compose_entry(T, tr, dead, rank8, st, lrs, a, b, j, dch[b]);
-                    }
+                    // short rows: (pair, entry) tasks packed across the lanes, 4 deep
+                    uint32_t lstep = 0;
+                    while ((1u << lstep) < step) lstep++;
+                    pairwise_round<4>(T, rank8, dead, dsz, dch, st, lrs, lstep, npairs, lane, 32, tr.status);
                 } else {
                     // long rows: lanes over the valid entries of one pair at a time
                     for (uint32_t p = 0; p < npairs; p++) {
@@ -691,8 +794,8 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
             if (lane == 0) atomicMax(&g_tree_t[L], gtimer());
 #endif
             if (L == tr.nlevels) {
-                // root: Alg.seqmatch lines 4-6 on delta-hat(q0, x)
-                if (lane == 0) {
+                // root: Alg.seqmatch lines 4-6 on delta-hat(q0, x) (unless fold_rows_kernel follows)
+                if (lane == 0 && tr.root_final && node == 0) {
                     const uint32_t fs = row[0];
                     DevStatus *S = tr.status;
                     if (fs == T.poison) atomicMax(&S->err, 5u);
@@ -802,6 +905,89 @@ cudaError_t launch_walk_level(const DevTables &T, const Tree &tr, uint32_t L, in
     const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
     walk_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
     return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// fold_rows_kernel: the top of the composition tree for short rows -- P
+// reporting-chunk rows (internal order, stride rs) composed into the final
+// state (Eq.SeqReduction as a tree of Eq.MapReduction).  CTA b stages up to
+// `per_cta` consecutive rows in shared memory and composes them pairwise with
+// all its threads; the last CTA to finish (acq_rel ticket) composes the CTA
+// maps the same way and applies Alg.seqmatch l.4-6.
+// ---------------------------------------------------------------------------
+__device__ void cta_pairwise(const DevTables &T, const uint8_t *rank8, const uint32_t *dead, const uint16_t *dsz,
+                             uint16_t *st, const uint16_t *dch, uint32_t nc, uint32_t lrs, DevStatus *status) {
+    for (uint32_t lstep = 0; (1u << lstep) < nc; lstep++) {
+        const uint32_t step = 1u << lstep;
+        const uint32_t npairs = (nc - step + 2 * step - 1) >> (lstep + 1);
+        pairwise_round<4>(T, rank8, dead, dsz, dch, st, lrs, lstep, npairs, threadIdx.x, blockDim.x, status);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint16_t *rows, const uint16_t *doms,
+                                                         uint32_t P, uint32_t per_cta, uint32_t lrs,
+                                                         uint16_t *cta_rows, uint16_t *cta_doms,
+                                                         uint32_t *ticket, DevStatus *status,
+                                                         uint16_t *dev_final) {
+    extern __shared__ uint4 smem4[];
+    const uint32_t q4 = T.rs >> 3;
+    // shared: [rank table u8][error bits][dom sizes][child doms][rows]
+    uint8_t *rank8 = reinterpret_cast<uint8_t *>(smem4);
+    const uint32_t rank_bytes = T.rank8 ? (((T.nclass + 1) * T.nq + 15) & ~15u) : 0u;
+    uint32_t *dead = reinterpret_cast<uint32_t *>(rank8 + rank_bytes);
+    const uint32_t dead_words = ((T.nq + 31) / 32 + 3) & ~3u;
+    uint16_t *dsz = reinterpret_cast<uint16_t *>(dead + dead_words);
+    const uint32_t dsz_n = (T.nclass + 1 + 7) & ~7u;
+    uint16_t *dch = dsz + dsz_n;
+    uint16_t *st = dch + ((per_cta + 7) & ~7u);
+    for (uint32_t i = threadIdx.x; i < rank_bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(rank8)[i] = __ldg(reinterpret_cast<const uint4 *>(T.rank8) + i);
+    for (uint32_t i = threadIdx.x; i < dead_words; i += blockDim.x) dead[i] = __ldg(T.dead_bits + i);
+    for (uint32_t i = threadIdx.x; i <= T.nclass; i += blockDim.x) dsz[i] = T.dom_size[i];
+    const uint32_t r0 = blockIdx.x * per_cta, nc = min(per_cta, P - r0);
+    for (uint32_t t = threadIdx.x; t < nc; t += blockDim.x) dch[t] = doms[r0 + t];
+    for (uint32_t t = threadIdx.x; t < nc * q4; t += blockDim.x) {
+        const uint32_t c = t / q4, k = t - c * q4;
+        reinterpret_cast<uint4 *>(st + (c << lrs))[k] =
+            __ldcg(reinterpret_cast<const uint4 *>(rows + (uint64_t)(r0 + c) * T.rs) + k);
+    }
+    __syncthreads();
+    cta_pairwise(T, T.rank8 ? rank8 : nullptr, dead, dsz, st, dch, nc, lrs, status);
+    // publish this CTA's map, take a ticket; the last CTA folds the CTA maps
+    for (uint32_t t = threadIdx.x; t < q4; t += blockDim.x)
+        reinterpret_cast<uint4 *>(cta_rows + (uint64_t)blockIdx.x * T.rs)[t] = reinterpret_cast<const uint4 *>(st)[t];
+    if (threadIdx.x == 0) cta_doms[blockIdx.x] = dch[0];
+    __syncthreads();
+    __shared__ uint32_t last;
+    if (threadIdx.x == 0) {
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ticket) : "memory");
+        last = ((prev + 1) % gridDim.x) == 0;
+    }
+    __syncthreads();
+    if (!last) return;
+    const uint32_t G = gridDim.x;
+    if (G > 1) {
+        for (uint32_t t = threadIdx.x; t < G; t += blockDim.x) dch[t] = __ldcg(cta_doms + t);
+        for (uint32_t t = threadIdx.x; t < G * q4; t += blockDim.x) {
+            const uint32_t c = t / q4, k = t - c * q4;
+            reinterpret_cast<uint4 *>(st + (c << lrs))[k] =
+                __ldcg(reinterpret_cast<const uint4 *>(cta_rows + (uint64_t)c * T.rs) + k);
+        }
+        __syncthreads();
+        cta_pairwise(T, T.rank8 ? rank8 : nullptr, dead, dsz, st, dch, G, lrs, status);
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t fs = st[0];
+        if (fs == T.poison) atomicMax(&status->err, 5u);
+        status->final_state = fs;
+        status->accept = fs < T.nq ? (uint32_t)test_bit(T.accept_bits, fs) : 0u;
+        if (dev_final) {
+            dev_final[0] = (uint16_t)fs;
+            dev_final[1] = (uint16_t)status->accept;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -927,6 +1113,8 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute((void *)fold_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute((void *)tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
@@ -953,10 +1141,12 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
-                         uint16_t *dom_of, int convergence, uint16_t *amap, int threads, int grid,
+                         uint16_t *dom_of, int convergence, uint16_t *amap, uint32_t g_log,
+                         uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, int threads, int grid,
                          cudaStream_t s) {
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
-                    (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap};
+                    (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap,
+                    (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status};
     return cudaLaunchKernel(lanes_fn(T.mode), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
 }
 
@@ -978,6 +1168,23 @@ extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {
 cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
                                  DevStatus *st, uint16_t *dev_final, cudaStream_t s) {
     fold_segments_kernel<<<1, 32, 0, s>>>(T, rows, lookahead, G, st, dev_final);
+    return cudaGetLastError();
+}
+
+size_t fold_rows_fixed_bytes(const DevTables &T) {
+    const size_t rank_bytes = T.rank8 ? (((T.nclass + 1) * T.nq + 15) & ~15u) : 0u;
+    const size_t dead_words = ((T.nq + 31) / 32 + 3) & ~3u;
+    return rank_bytes + dead_words * 4 + ((T.nclass + 1 + 7) & ~7u) * 2;
+}
+
+cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uint16_t *doms, uint32_t P,
+                             uint32_t per_cta, uint16_t *cta_rows, uint16_t *cta_doms, uint32_t *ticket,
+                             DevStatus *st, uint16_t *dev_final, cudaStream_t s) {
+    const uint32_t lrs = tree_lrs(T);
+    const uint32_t grid = (P + per_cta - 1) / per_cta;
+    const size_t smem = fold_rows_fixed_bytes(T) + ((per_cta + 7) & ~7u) * 2 + ((size_t)per_cta << lrs) * 2;
+    fold_rows_kernel<<<grid, 1024, smem, s>>>(T, rows, doms, P, per_cta, lrs, cta_rows, cta_doms, ticket, st,
+                                              dev_final);
     return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@ namespace dfa {
 constexpr int kLanes = 8;          // register lanes per thread in lanes_kernel
 constexpr int kConvergeLA = 8;     // lanes per thread per pass in converge_kernel
 constexpr uint32_t kSubWindow = 16;
+constexpr uint32_t kNoWarpGroup = 0xFFFFFFFFu;  // lanes_kernel g_log: per-sub-chunk maps
 
 struct DevTables {
     const uint32_t *image;      // smem image of the transition table (32-bit words)
@@ -93,6 +94,7 @@ struct Tree {
     uint32_t lrs;            // log2 of the shared-memory row stride (>= T.rs)
     int rank_smem;           // uint8 rank table staged in shared memory
     int dbg;                 // debug experiment bits (0 in production)
+    int root_final;          // the top level is the root: write the final state
     TreeLevel lv[kMaxLevels + 1];
     // leaves (lanes kernel output)
     const uint16_t *amap, *sfin;
@@ -119,13 +121,18 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 int converge_smem_bytes(const DevTables &T, int warps_per_cta);
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
-                         uint16_t *dom_of, int convergence, uint16_t *amap, int threads, int grid,
+                         uint16_t *dom_of, int convergence, uint16_t *amap, uint32_t g_log,
+                         uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, int threads, int grid,
                          cudaStream_t s);
 int lanes_smem_bytes(const DevTables &T);
 int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s);
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
+size_t fold_rows_fixed_bytes(const DevTables &T);
+cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uint16_t *doms, uint32_t P,
+                             uint32_t per_cta, uint16_t *cta_rows, uint16_t *cta_doms, uint32_t *ticket,
+                             DevStatus *st, uint16_t *dev_final, cudaStream_t s);
 int tree_slice_bytes(const DevTables &T, uint32_t F);
 uint32_t tree_lrs(const DevTables &T);
 int tree_fixed_bytes(const DevTables &T, int rank_smem);
