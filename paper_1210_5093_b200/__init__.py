@@ -31,6 +31,7 @@ DFA_OPT_SUBCHUNK_TARGET, DFA_OPT_CONVERGENCE, DFA_OPT_PROFILE, DFA_OPT_THREADS_P
 DFA_OPT_TREE_FANIN = 5
 DFA_OPT_FOLD_IN_TREE = 6
 DFA_OPT_WARP_COMPOSE = 7
+DFA_OPT_GRAPHS = 8
 TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16"}
 
 

@@ -68,6 +68,12 @@ struct dfa_handle {
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
     int warp_compose = 1;
     std::vector<uint64_t> plan_key;
+    // CUDA graph of a repeated dfa_chunk_maps call
+    int use_graphs = 1;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    std::vector<uint64_t> graph_key, graph_pending;
+    uint32_t graph_kernels = 0;
     struct { uint32_t m0, m, g_log; int threads; } plan_split_c{};
     int fold_in_tree = 0;
     std::vector<uint64_t> tree_sig;
@@ -84,6 +90,7 @@ struct dfa_handle {
     std::vector<Rec> recs;
     int open_section = -1;
     cudaEvent_t open_event = nullptr;
+    std::vector<Rec> graph_recs;
 };
 
 namespace {
@@ -225,6 +232,14 @@ dfa_status probe(dfa_handle *h, uint32_t &u8_limit) {
     return DFA_OK;
 }
 
+// an event recorded during graph capture must be an external node to be timed later
+void record_event(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+}
+
 const char *const kSections[] = {"converge", "lanes", "compose"};
 constexpr int kNumSections = 3;
 
@@ -240,13 +255,13 @@ void prof_begin(dfa_handle *h, cudaStream_t s, int section) {
     if (!h->profile || h->ev_used + 2 > (1u << 16)) return;
     h->open_event = prof_event(h);
     h->open_section = section;
-    if (h->open_event) cudaEventRecord(h->open_event, s);
+    if (h->open_event) record_event(h->open_event, s);
 }
 void prof_end(dfa_handle *h, cudaStream_t s) {
     if (!h->profile || h->open_section < 0 || !h->open_event) return;
     cudaEvent_t b = prof_event(h);
     if (b) {
-        cudaEventRecord(b, s);
+        record_event(b, s);
         h->recs.push_back({h->open_section, h->open_event, b});
     }
     h->open_section = -1;
@@ -552,6 +567,57 @@ dfa_status fetch_status(dfa_handle *h, cudaStream_t s, DevStatus &out) {
     return DFA_OK;
 }
 
+// Replay a captured CUDA graph of `body` when the same call (gkey) repeats.
+// First call: eager.  Second identical call: captured on an internal stream
+// (the caller's may be the legacy default stream), instantiated, launched on
+// the caller's stream.  Later calls: cudaGraphLaunch only.
+template <class Body>
+dfa_status run_graphed(dfa_handle *h, const std::vector<uint64_t> &gkey, cudaStream_t s, Body body) {
+    if (!h->use_graphs) return body(s);
+    if (h->graph_exec && gkey == h->graph_key) {
+        CK(cudaGraphLaunch(h->graph_exec, s));
+        h->recs = h->graph_recs;
+        h->stats.num_kernels = h->graph_kernels;
+        h->last_stream = s;
+        return DFA_OK;
+    }
+    if (gkey != h->graph_pending) {
+        h->graph_pending = gkey;
+        return body(s);
+    }
+    if (h->graph_exec) { cudaGraphExecDestroy(h->graph_exec); h->graph_exec = nullptr; }
+    if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    h->recs.clear();
+    h->ev_used = 0;
+    CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed));
+    dfa_status st = body(h->cap_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    if (st != DFA_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture", __LINE__);
+    e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(e, "cudaGraphInstantiate", __LINE__); }
+    h->graph_key = gkey;
+    // the graph owns the events it records: take them out of the pool
+    for (auto &gr : h->graph_recs) { cudaEventDestroy(gr.a); cudaEventDestroy(gr.b); }
+    h->graph_recs = h->recs;
+    {
+        std::vector<cudaEvent_t> keep;
+        for (size_t i = 0; i < h->ev_pool.size(); i++) {
+            bool owned = false;
+            for (auto &gr : h->graph_recs) owned |= (gr.a == h->ev_pool[i] || gr.b == h->ev_pool[i]);
+            if (!owned) keep.push_back(h->ev_pool[i]);
+        }
+        h->ev_pool = keep;
+        h->ev_used = 0;
+    }
+    h->graph_kernels = h->stats.num_kernels;
+    CK(cudaGraphLaunch(h->graph_exec, s));
+    h->last_stream = s;
+    return DFA_OK;
+}
+
 } // namespace
 
 extern "C" {
@@ -614,6 +680,9 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         h->h_status.release();
         h->h_bounds.release();
         if (h->staging_done) cudaEventDestroy(h->staging_done);
+        if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+        for (auto &gr : h->graph_recs) { cudaEventDestroy(gr.a); cudaEventDestroy(gr.b); }
+        if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
         for (auto &e : h->ev_pool) if (e) cudaEventDestroy(e);
     }
     delete h;
@@ -742,7 +811,6 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
         h->plan_split_c = {sp0.m0, sp0.m, sp0.g_log, sp0.threads};
         h->plan_key = key;
     }
-    CK(cudaMemcpyAsync(dev_bounds, h->plan_bounds.p, (size_t)(P + 1) * 8, cudaMemcpyDeviceToDevice, s));
     Split sp;
     sp.m0 = h->plan_split_c.m0;
     sp.m = h->plan_split_c.m;
@@ -753,7 +821,18 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     o.user_maps = P > 1 ? dev_maps : nullptr;
     o.starts = dev_chunk_start;
     o.final2 = dev_final;
-    return run(h, dev_input, len, P, dev_bounds, sp, s, o);
+    auto body = [&](cudaStream_t cs) -> dfa_status {
+        CK(cudaMemcpyAsync(dev_bounds, h->plan_bounds.p, (size_t)(P + 1) * 8, cudaMemcpyDeviceToDevice, cs));
+        return run(h, dev_input, len, P, dev_bounds, sp, cs, o);
+    };
+    // repeated identical calls replay a CUDA graph of the whole call (no launch gaps)
+    std::vector<uint64_t> gkey = key;
+    for (uint64_t v : {(uint64_t)(uintptr_t)dev_input, (uint64_t)(uintptr_t)dev_bounds,
+                       (uint64_t)(uintptr_t)dev_chunk0_end, (uint64_t)(uintptr_t)dev_maps,
+                       (uint64_t)(uintptr_t)dev_chunk_start, (uint64_t)(uintptr_t)dev_final, (uint64_t)h->profile,
+                       (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree})
+        gkey.push_back(v);
+    return run_graphed(h, gkey, s, body);
 }
 
 dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
@@ -833,6 +912,9 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
     case DFA_OPT_TREE_FANIN:
         if (value < 2 || value > 64) return DFA_ERR_ARG;
         h->tree_fanin_cap = (uint32_t)value;
+        return DFA_OK;
+    case DFA_OPT_GRAPHS:
+        h->use_graphs = value ? 1 : 0;
         return DFA_OK;
     case DFA_OPT_WARP_COMPOSE:
         h->warp_compose = value ? 1 : 0;

@@ -380,3 +380,25 @@ def test_misaligned_input(off):
             assert d.match(full[off:])[0] == c.od.run(x[off:])
         finally:
             d.close()
+
+
+def test_repeated_calls_graph_replay():
+    """Identical repeated dfa_chunk_maps calls are replayed from a captured CUDA
+    graph: results must stay identical to the oracle, also after changing buffers."""
+    w = W.get("keyword")
+    x = w.input(1 << 20)
+    c = Case(w.automaton, x, "keyword")
+    d = c.handle()
+    try:
+        dx = torch.from_numpy(x).to(DEV)
+        ob = oracle.chunk_bounds_ratio(x.size, 300, 1, 1)
+        oe0, omaps = c.od.maps(x, ob, d.info["i_max"])
+        ofin = c.od.run(x)
+        for rep in range(5):
+            if rep == 3:  # new input buffer: new graph
+                dx = dx.clone()
+            bounds, e0, maps, starts, final = d.chunk_maps(dx, 300)
+            torch.cuda.synchronize()
+            assert u16(e0)[0] == oe0 and np.array_equal(u16(maps), omaps) and u16(final)[0] == ofin, rep
+    finally:
+        d.close()
