@@ -150,6 +150,25 @@ struct Tab {
         else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
         else return __ldg(g + (s << 8) + p.a);
     }
+    // per raw byte b, shared by all lanes stepping on it (scalar paths)
+    __device__ __forceinline__ Pre bpre(uint32_t b) const {
+        if constexpr (MODE == kIdentU8 || MODE == kGlobalU16) return {b, 0u};
+        else if constexpr (MODE == kIdentU16) return {tb + 2u * b, 0u};
+        else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
+            const uint32_t c = min((b - base) & 0xFFu, w);
+            return {tb + (MODE == kWindowU16 ? 2u : 1u) * c, 0u};
+        } else {
+            const uint32_t wc = (b * 171u) >> 9;
+            return {tb + 4u * wc, (b - 3u * wc) * 9u};
+        }
+    }
+    __device__ __forceinline__ uint32_t look_pre(uint32_t s, Pre p) const {
+        if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | p.a);
+        else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
+        else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
+        else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
+        else return __ldg(g + (s << 8) + p.a);
+    }
     // scalar step on an encoded state and a raw byte
     __device__ __forceinline__ uint32_t look_byte(uint32_t s, uint32_t b) const {
         if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | b);
@@ -271,9 +290,10 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_abso
 template <int MODE>
 __device__ __forceinline__ void step_scalar(const Tab<MODE> &tab, uint32_t b, uint32_t (&st)[kLanes],
                                             uint32_t nlive) {
+    const typename Tab<MODE>::Pre pb = tab.bpre(b);
 #pragma unroll
     for (int l = 0; l < kLanes; l++)
-        if ((uint32_t)l < nlive) st[l] = tab.look_byte(st[l], b);
+        if ((uint32_t)l < nlive) st[l] = tab.look_pre(st[l], pb);
 }
 
 template <int MODE>
@@ -534,8 +554,9 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
                     const uint32_t wsel = k >> 2;
                     const uint32_t word = wsel == 0 ? v.x : wsel == 1 ? v.y : wsel == 2 ? v.z : v.w;
                     const uint32_t b = (word >> (8 * (k & 3))) & 0xFFu;
+                    const typename Tab<MODE>::Pre pb = tab.bpre(b);
 #pragma unroll
-                    for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_byte(s[l], b);
+                    for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_pre(s[l], pb);
                 }
 #pragma unroll
                 for (int l = 0; l < kConvergeLA; l++) {
