@@ -2,6 +2,7 @@
 #include "prep.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -155,7 +156,15 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
         if (!(w & 1)) w++;
         return w;
     };
-    if (p.nq <= u8_state_limit) {
+    const char *force = getenv("DFA_TABLE_MODE");  // experiments only
+    const int fm = force ? atoi(force) : 0;
+    if (fm == kIdentU16 && (size_t)p.nq * 512 <= smem_budget) {
+        p.mode = kIdentU16;
+        p.stride = 256;
+    } else if (fm == kPacked9 && p.nq <= 512) {
+        p.mode = kPacked9;
+        p.stride = 87;
+    } else if (p.nq <= u8_state_limit) {
         p.mode = kIdentU8;
         p.stride = 256;
     } else if (W && (size_t)p.nq * window_words_u16(W + 1) * 4 <= smem_budget) {
