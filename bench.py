@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--convergence", type=int, default=1)
     ap.add_argument("--opt", action="append", default=[],
                     help="library option NAME=VALUE (subchunk_target, tree_fanin, threads_per_cta)")
+    ap.add_argument("--profile", choices=["inline", "separate"], default="separate",
+                    help="per-kernel CUDA events inside the timed loop (inline) or in a second loop of the same K steps")
     ap.add_argument("--quiet-json", action="store_true", help="print a one-line summary instead of JSON")
     return ap.parse_args()
 
@@ -207,7 +209,7 @@ def main():
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
-    D.dfa_set_option(d.h, D.DFA_OPT_PROFILE, 1)
+    D.dfa_set_option(d.h, D.DFA_OPT_PROFILE, 1 if args.profile == "inline" else 0)
     D.dfa_get_stats(d.h)  # reset accumulators
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -219,6 +221,12 @@ def main():
         for _ in range(args.steps):
             step()
         t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if args.profile == "separate":
+        D.dfa_set_option(d.h, D.DFA_OPT_PROFILE, 1)
+        D.dfa_get_stats(d.h)
+        for _ in range(args.steps):
+            step()
         torch.cuda.synchronize(dev)
     stats = D.dfa_get_stats(d.h)
     D.dfa_set_option(d.h, D.DFA_OPT_PROFILE, 0)
@@ -279,7 +287,10 @@ def main():
                    "i_max": imax, "gamma": f"{d.info['gamma_num']}/{d.info['gamma_den']}",
                    "table_mode": d.info["table_mode_name"], "chunk_ratio_c": f"{d.info['c_num']}/{d.info['c_den']}",
                    "convergence": bool(args.convergence), "l2": "input 256 MiB+ > 126 MB L2, no flush",
-                   "seed": args.seed, "input_sha256": W.sha256(x)[:16]},
+                   "seed": args.seed, "input_sha256": W.sha256(x)[:16],
+                   "kernel_timing": ("CUDA events around each kernel inside the timed loop" if args.profile == "inline"
+                                     else "CUDA events around each kernel in a second loop of the same K steps "
+                                          "(per-kernel events would break the lanes->compose PDL overlap)")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
                      "kernel": "lanes_kernel", "algorithmic_bytes_per_launch": n, "kernel_ms": lanes_ms,

@@ -432,6 +432,37 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         kernels++;
     }
     // composition: sub-chunk maps -> reporting maps -> final state
+    const uint32_t gl0 = grouped ? sp.g_log : 0;
+    const uint32_t L0 = m0 >> gl0, Lm = P > 1 ? (m >> gl0) : 1;
+    if (grouped && T.rs == 8 && !h->fold_in_tree && L0 >= 1 && L0 <= 256 && Lm >= 1 && Lm <= 256 &&
+        P <= (1u << 20)) {
+        // shuffle path: warp per reporting chunk over its leaves, then the fold
+        CK(h->lvlA.ensure((uint64_t)P * T.rs * 2));
+        CK(h->domA.ensure((uint64_t)P * 2));
+        const uint32_t per_warp = std::max<uint32_t>(1, (P + 32u * h->sms - 1) / (32u * h->sms));
+        const uint32_t cpc = 32 * std::min<uint32_t>(per_warp, 32);  // one wave of 1024-thread CTAs
+        const uint32_t g2 = (P + cpc - 1) / cpc;
+        CK(h->fold_rows.ensure((uint64_t)g2 * T.rs * 2 + 256));
+        CK(h->fold_doms.ensure((uint64_t)g2 * 2 + 256));
+        if (!h->ticket.p) {
+            CK(h->ticket.ensure(256));
+            CK(cudaMemsetAsync(h->ticket.p, 0, 256, s));
+        }
+        uint16_t *rep_rows = h->lvlA.as<uint16_t>(), *rep_doms = h->domA.as<uint16_t>();
+        prof_begin(h, s, 2);
+        CK(launch_compose8(T, h->leaf_rows.as<uint16_t>(), h->leaf_dom.as<uint16_t>(), L0, Lm, P, cpc, rep_rows,
+                           rep_doms, o.user_maps, o.user_row0, o.chunk0_end, h->fold_rows.as<uint16_t>(),
+                           h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(), h->status.as<DevStatus>(), o.final2,
+                           s));
+        prof_end(h, s);
+        kernels += 1;
+        if (o.starts) {
+            CK(launch_starts(T, plan, rep_rows, rep_rows + T.rs, rep_doms, o.starts, h->status.as<DevStatus>(), s));
+            kernels++;
+        }
+        h->stats.num_kernels = kernels;
+        return DFA_OK;
+    }
     Tree tr{};
     bool use_fold_rows = false;
     int tree_smem = 0;

@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <utility>
 #include <cstdint>
 
 namespace dfa {
@@ -20,6 +21,12 @@ namespace {
 
 constexpr uint32_t kDone = 0xFFu;
 constexpr uint32_t kNoGroup = 0xFFFFFFFFu;
+
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// launch_pdl may start while its predecessor drains; it stages what does not
+// depend on it, then waits here for the predecessor's completion and memory.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ bool test_bit(const uint32_t *bits, uint32_t q) {
     return (bits[q >> 5] >> (q & 31)) & 1u;
@@ -395,6 +402,7 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
                                                     uint16_t *__restrict__ amap, uint32_t g_log,
                                                     uint16_t *__restrict__ leaf_rows, uint16_t *__restrict__ leaf_dom,
                                                     DevStatus *status) {
+    pdl_trigger();  // one wave: the composition kernels may take SMs as CTAs retire
     extern __shared__ uint4 smem4[];
     uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
     __syncthreads();
@@ -962,6 +970,9 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
     const uint32_t dsz_n = (T.nclass + 1 + 7) & ~7u;
     uint16_t *dch = dsz + dsz_n;
     uint16_t *st = dch + ((per_cta + 7) & ~7u);
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMin(&g_tree_t[20], gtimer());
+#endif
     for (uint32_t i = threadIdx.x; i < rank_bytes / 16; i += blockDim.x)
         reinterpret_cast<uint4 *>(rank8)[i] = __ldg(reinterpret_cast<const uint4 *>(T.rank8) + i);
     for (uint32_t i = threadIdx.x; i < dead_words; i += blockDim.x) dead[i] = __ldg(T.dead_bits + i);
@@ -974,7 +985,14 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
             __ldcg(reinterpret_cast<const uint4 *>(rows + (uint64_t)(r0 + c) * T.rs) + k);
     }
     __syncthreads();
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[21], gtimer());
+#endif
     cta_pairwise(T, T.rank8 ? rank8 : nullptr, dead, dsz, st, dch, nc, lrs, status);
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[22], gtimer());
+#endif
+
     // publish this CTA's map, take a ticket; the last CTA folds the CTA maps
     for (uint32_t t = threadIdx.x; t < q4; t += blockDim.x)
         reinterpret_cast<uint4 *>(cta_rows + (uint64_t)blockIdx.x * T.rs)[t] = reinterpret_cast<const uint4 *>(st)[t];
@@ -984,10 +1002,14 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
     if (threadIdx.x == 0) {
         uint32_t prev;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ticket) : "memory");
-        last = ((prev + 1) % gridDim.x) == 0;
+        last = prev + 1 == gridDim.x;
+        if (last) atomicExch(ticket, 0u);  // every CTA has its ticket: reset for the next launch
     }
     __syncthreads();
     if (!last) return;
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[23], gtimer());
+#endif
     const uint32_t G = gridDim.x;
     if (G > 1) {
         for (uint32_t t = threadIdx.x; t < G; t += blockDim.x) dch[t] = __ldcg(cta_doms + t);
@@ -999,6 +1021,10 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
         __syncthreads();
         cta_pairwise(T, T.rank8 ? rank8 : nullptr, dead, dsz, st, dch, G, lrs, status);
     }
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[24], gtimer());
+#endif
+
     if (threadIdx.x == 0) {
         const uint32_t fs = st[0];
         if (fs == T.poison) atomicMax(&status->err, 5u);
@@ -1008,6 +1034,309 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
             dev_final[0] = (uint16_t)fs;
             dev_final[1] = (uint16_t)status->accept;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Shuffle composition of maps with <= 8 entries (rows of stride 8): the
+// reporting-chunk maps from the group leaves (seg_fold_kernel) and the fold of
+// the reporting maps into the final state (fold2_kernel).  Entry per lane: a
+// warp holds 4 maps, lane 8g + j = entry j of map g, so composing two maps is
+// one rank lookup and one shuffle per lane (Eq.MapReduction).
+// ---------------------------------------------------------------------------
+
+// rank8 / Z / |I_sigma| / xlat / |I_sigma| (user) staged in shared memory
+// when they fit, else the global copies.
+constexpr int kCompose8Static = 28 * 1024;  // compose8_kernel: crow/cdom/trow/tdom (~23 KB) + reserve
+
+struct RTab {
+    const uint8_t *rank8;
+    const uint32_t *dead;
+    const uint16_t *dsz;
+    const uint16_t *xlat;
+    const uint16_t *dus;
+};
+
+__host__ __device__ __forceinline__ uint32_t rtab_rank_bytes(const DevTables &T) {
+    return ((T.nclass + 1) * T.nq + 15) & ~15u;
+}
+__host__ __device__ __forceinline__ uint32_t rtab_dead_bytes(const DevTables &T) {
+    return ((T.nq + 31) / 32 * 4 + 15) & ~15u;
+}
+__host__ __device__ __forceinline__ uint32_t rtab_dsz_bytes(const DevTables &T) {
+    return ((T.nclass + 1) * 2 + 15) & ~15u;
+}
+__host__ __device__ __forceinline__ uint32_t rtab_xlat_bytes(const DevTables &T) {
+    return (T.nclass * T.imax_user * 2 + 15) & ~15u;
+}
+__host__ __device__ __forceinline__ uint32_t rtab_bytes(const DevTables &T) {
+    return rtab_rank_bytes(T) + rtab_dead_bytes(T) + 2 * rtab_dsz_bytes(T) + rtab_xlat_bytes(T);
+}
+
+__device__ __forceinline__ RTab stage_rtab(const DevTables &T, uint8_t *sm, bool staged) {
+    if (!staged) return RTab{T.rank8, T.dead_bits, T.dom_size, T.xlat, T.dom_user_size};
+    const uint32_t rb = rtab_rank_bytes(T), db = rtab_dead_bytes(T), zb = rtab_dsz_bytes(T);
+    const uint32_t nr = (T.nclass + 1) * T.nq;
+    for (uint32_t i = threadIdx.x; i < rb / 16; i += blockDim.x) {
+        if (i * 16 + 16 <= nr) reinterpret_cast<uint4 *>(sm)[i] = __ldg(reinterpret_cast<const uint4 *>(T.rank8) + i);
+        else for (uint32_t k = i * 16; k < i * 16 + 16; k++) sm[k] = k < nr ? __ldg(T.rank8 + k) : 0xFFu;
+    }
+    uint32_t *dead = reinterpret_cast<uint32_t *>(sm + rb);
+    for (uint32_t i = threadIdx.x; i < db / 4; i += blockDim.x)
+        dead[i] = i < (T.nq + 31) / 32 && T.has_dead ? __ldg(T.dead_bits + i) : 0u;
+    uint16_t *dsz = reinterpret_cast<uint16_t *>(sm + rb + db);
+    for (uint32_t i = threadIdx.x; i <= T.nclass; i += blockDim.x) dsz[i] = __ldg(T.dom_size + i);
+    uint16_t *dus = reinterpret_cast<uint16_t *>(sm + rb + db + zb);
+    for (uint32_t i = threadIdx.x; i < T.nclass; i += blockDim.x) dus[i] = __ldg(T.dom_user_size + i);
+    uint16_t *xl = reinterpret_cast<uint16_t *>(sm + rb + db + 2 * zb);
+    for (uint32_t i = threadIdx.x; i < T.nclass * T.imax_user; i += blockDim.x) xl[i] = __ldg(T.xlat + i);
+    __syncthreads();
+    return RTab{sm, dead, dsz, xl, dus};
+}
+
+// One lane's view of a map: entry v (j = lane & 7), the map's domain and size
+// (replicated over its 8 lanes), ok = the map exists (ragged batches).
+struct LMap {
+    uint32_t v, dom, u, ok;
+};
+
+__device__ __forceinline__ LMap lmap_load(const RTab &R, const uint16_t *rows, const uint16_t *doms, uint64_t r,
+                                          bool ok) {
+    LMap m;
+    const uint32_t j = threadIdx.x & 7;
+    m.ok = ok;
+    m.v = ok ? __ldcg(rows + r * 8 + j) : (uint32_t)kNone;
+    m.dom = ok ? __ldcg(doms + r) : 0u;
+    m.u = ok ? R.dsz[m.dom] : 0u;
+    return m;
+}
+
+// Entry j of map a (domain a.dom) continued through map b: the index to read
+// in b, or j when a's entry stays (padding, error state P:450-454).
+__device__ __forceinline__ bool lmap_step(const DevTables &T, const RTab &R, uint32_t v, uint32_t u, uint32_t j,
+                                          uint32_t bdom, uint32_t &r, DevStatus *status) {
+    if (j >= u) return false;
+    if (T.has_dead && test_bit(R.dead, v)) return false;
+    r = R.rank8[bdom * T.nq + v];
+    if (r >= (uint32_t)kLanes) { atomicMax(&status->err, 8u); r = 0; }
+    return true;
+}
+
+// Tree step over the 4 maps of a warp: group g (g % 2gs == 0) <- group g+gs o g.
+__device__ __forceinline__ void lmap_merge(const DevTables &T, const RTab &R, LMap &m, uint32_t gs, DevStatus *status) {
+    const uint32_t lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+    const uint32_t sb = ((g + gs) & 3) * 8;
+    const uint32_t bdom = __shfl_sync(0xffffffffu, m.dom, sb);
+    const uint32_t bu = __shfl_sync(0xffffffffu, m.u, sb);
+    const uint32_t bok = __shfl_sync(0xffffffffu, m.ok, sb);
+    const bool lead = (g & (2 * gs - 1)) == 0 && bok;
+    uint32_t r = j;
+    bool use = false;
+    if (lead) use = m.ok ? lmap_step(T, R, m.v, m.u, j, bdom, r, status) : true;
+    const uint32_t nv = __shfl_sync(0xffffffffu, m.v, sb + r);
+    if (use) m.v = nv;
+    if (lead && !m.ok) { m.dom = bdom; m.u = bu; m.ok = 1; }
+}
+
+// acc (group 0) <- b (group 0) o acc
+__device__ __forceinline__ void lmap_then(const DevTables &T, const RTab &R, LMap &acc, const LMap &b,
+                                          DevStatus *status) {
+    const uint32_t j = threadIdx.x & 7;
+    const uint32_t bdom = __shfl_sync(0xffffffffu, b.dom, 0);
+    const uint32_t bu = __shfl_sync(0xffffffffu, b.u, 0);
+    const uint32_t bok = __shfl_sync(0xffffffffu, b.ok, 0) && (threadIdx.x & 31) < 8;
+    uint32_t r = j;
+    bool use = false;
+    if (bok) use = acc.ok ? lmap_step(T, R, acc.v, acc.u, j, bdom, r, status) : true;
+    const uint32_t nv = __shfl_sync(0xffffffffu, b.v, r);
+    if (use) acc.v = nv;
+    if (bok && !acc.ok) { acc.dom = bdom; acc.u = bu; acc.ok = 1; }
+}
+
+// acc (group 0) <- maps [a, b) of (rows, doms) o acc, in order; the loads of
+// 16 maps are issued before their compositions.
+template <bool GLOBAL>
+__device__ __forceinline__ void warp_fold_range(const DevTables &T, const RTab &R, const uint16_t *rows,
+                                                const uint16_t *doms, uint32_t a, uint32_t b, LMap &acc,
+                                                DevStatus *status) {
+    const uint32_t g = (threadIdx.x & 31) >> 3, j = threadIdx.x & 7;
+#pragma unroll 1
+    for (uint32_t base = a; base < b; base += 16) {
+        LMap m[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint32_t r = base + 4 * q + g;
+            if (GLOBAL) m[q] = lmap_load(R, rows, doms, r, r < b);
+            else {
+                m[q].ok = r < b;
+                m[q].v = m[q].ok ? rows[r * 8 + j] : (uint32_t)kNone;
+                m[q].dom = m[q].ok ? doms[r] : 0u;
+                m[q].u = m[q].ok ? R.dsz[m[q].dom] : 0u;
+            }
+        }
+        // the 4 batches side by side: within-batch tree, then pairs, then acc
+#pragma unroll
+        for (int q = 0; q < 4; q++) lmap_merge(T, R, m[q], 1, status);
+#pragma unroll
+        for (int q = 0; q < 4; q++) lmap_merge(T, R, m[q], 2, status);
+        lmap_then(T, R, m[0], m[1], status);
+        lmap_then(T, R, m[2], m[3], status);
+        lmap_then(T, R, m[0], m[2], status);
+        lmap_then(T, R, acc, m[0], status);
+    }
+}
+
+// Tree fold of the n >= 1 maps (rows, doms) in shared memory: each level,
+// warp w folds maps 4w..4w+3 into slot w of the other buffer (trows/tdoms,
+// >= ceil(n/4) slots; the two alternate).  Result in warp 0, lanes 0..7.
+__device__ __forceinline__ LMap cta_tree_fold(const DevTables &T, const RTab &R, uint16_t *rows, uint16_t *doms,
+                                              uint16_t *trows, uint16_t *tdoms, uint32_t n, DevStatus *status) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t g = lane >> 3, j = lane & 7;
+    LMap m{kNone, 0, 0, 0};
+    for (;;) {
+        const uint32_t groups = (n + 3) / 4;
+#pragma unroll 1
+        for (uint32_t w = warp; w < groups; w += nw) {
+            const uint32_t r = 4 * w + g;
+            m.ok = r < n;
+            m.v = m.ok ? rows[r * 8 + j] : (uint32_t)kNone;
+            m.dom = m.ok ? doms[r] : 0u;
+            m.u = m.ok ? R.dsz[m.dom] : 0u;
+            lmap_merge(T, R, m, 1, status);
+            lmap_merge(T, R, m, 2, status);
+            if (groups > 1) {
+                if (lane < 8) trows[w * 8 + j] = (uint16_t)(j < m.u ? m.v : kNone);
+                if (lane == 0) tdoms[w] = (uint16_t)m.dom;
+            }
+        }
+        if (groups == 1) break;
+        n = groups;
+        uint16_t *t = rows; rows = trows; trows = t;
+        t = doms; doms = tdoms; tdoms = t;
+        __syncthreads();
+    }
+    return m;
+}
+
+// compose8_kernel: the whole composition for maps of <= 8 entries, one
+// launch (dependent, PDL).  CTA b owns reporting chunks [b cpc, (b+1) cpc):
+// a warp per chunk folds the chunk's group leaves (chunk 0: L0 leaves,
+// others L) into the reporting map (internal row, API row in the user's
+// order, chunk 0's user row, e0); the CTA folds its chunk maps
+// (Eq.SeqReduction), the last CTA (acq_rel ticket) folds the CTA maps and
+// applies Alg.seqmatch lines 4-6.
+__global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint16_t *leaves, const uint16_t *leaf_dom,
+                                                        uint32_t L0, uint32_t L, uint32_t P, uint32_t cpc,
+                                                        uint16_t *rep_rows, uint16_t *rep_doms, uint16_t *user_rows,
+                                                        uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
+                                                        uint16_t *cta_doms, uint32_t *ticket, DevStatus *status,
+                                                        uint16_t *dev_final, int staged) {
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMin(&g_tree_t[10], gtimer());
+#endif
+    extern __shared__ __align__(16) uint8_t rsm[];
+    const RTab RT = stage_rtab(T, rsm, staged);
+    pdl_trigger();
+    pdl_wait();
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[11], gtimer());
+#endif
+    __shared__ __align__(16) uint16_t crow[1024 * 8];
+    __shared__ __align__(16) uint16_t trow[256 * 8];
+    __shared__ uint16_t cdom[1024], tdom[256];
+    __shared__ uint32_t last;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5, j = lane & 7;
+    const uint32_t c0 = blockIdx.x * cpc, c1 = min(P, c0 + cpc);
+#pragma unroll 1
+    for (uint32_t k = c0 + warp; k < c1; k += nw) {
+        const uint32_t a = k == 0 ? 0u : L0 + (k - 1) * L, b = L0 + k * L;
+        LMap acc{kNone, 0, 0, 0};
+        warp_fold_range<true>(T, RT, leaves, leaf_dom, a, b, acc, status);
+        const uint32_t d0 = acc.dom;
+        const uint16_t ev = (uint16_t)(j < acc.u ? acc.v : kNone);
+        if (lane < 8) {
+            rep_rows[(uint64_t)k * 8 + j] = ev;
+            crow[(k - c0) * 8 + j] = ev;
+        }
+        if (lane == 0) {
+            rep_doms[k] = (uint16_t)d0;
+            cdom[k - c0] = (uint16_t)d0;
+        }
+        if (e0 && k == 0 && lane == 0) e0[0] = (uint16_t)acc.v;
+        uint16_t *urow = nullptr;
+        uint32_t du = 0;
+        if (user_rows && k > 0) {
+            urow = user_rows + (uint64_t)(k - 1) * T.imax_user;
+            du = d0 < T.nclass ? RT.dus[d0] : 0u;
+        } else if (user_row0 && k == 0) {
+            urow = user_row0;
+            du = d0 < T.nclass ? RT.dus[d0] : (d0 == T.start_dom ? 1u : 0u);
+        }
+        if (urow) {
+#pragma unroll 1
+            for (uint32_t j0 = 0; j0 < T.imax_user; j0 += 32) {
+                const uint32_t ju = j0 + lane;
+                uint32_t ji = 0;
+                if (ju < du) ji = d0 < T.nclass ? RT.xlat[d0 * T.imax_user + ju] : ju;
+                const uint32_t v = __shfl_sync(0xffffffffu, acc.v, ji & 7);
+                if (ju < T.imax_user) urow[ju] = (uint16_t)(ju < du ? v : kNone);
+            }
+        }
+    }
+    __syncthreads();
+#ifdef DFA_TREE_TIMING
+    unsigned long long tc0 = gtimer();
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[12], tc0);
+#endif
+    // CTA fold of its chunk maps (shared memory), then the last CTA
+    const uint32_t n = c1 - c0;
+    LMap acc = cta_tree_fold(T, RT, crow, cdom, trow, tdom, n, status);
+#ifdef DFA_TREE_TIMING
+    unsigned long long tc1 = gtimer();
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[20], tc1 - tc0);
+#endif
+    if (gridDim.x > 1) {
+        if (warp == 0) {
+            if (lane < 8) cta_rows[(uint64_t)blockIdx.x * 8 + j] = (uint16_t)(j < acc.u ? acc.v : kNone);
+            if (lane == 0) cta_doms[blockIdx.x] = (uint16_t)acc.dom;
+            __syncwarp();
+            if (lane == 0) {
+                uint32_t prev;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ticket) : "memory");
+                last = prev + 1 == gridDim.x;
+                if (last) atomicExch(ticket, 0u);  // every CTA has its ticket: reset for the next launch
+            }
+        }
+        __syncthreads();
+#ifdef DFA_TREE_TIMING
+        unsigned long long tc2 = gtimer();
+        if (threadIdx.x == 0) atomicMax(&g_tree_t[16], tc2);
+        if (threadIdx.x == 0) atomicMax(&g_tree_t[21], tc2 - tc1);
+#endif
+        if (!last) return;
+        for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+            reinterpret_cast<uint4 *>(crow)[i] = __ldcg(reinterpret_cast<const uint4 *>(cta_rows) + i);
+            cdom[i] = __ldcg(cta_doms + i);
+        }
+        __syncthreads();
+        acc = cta_tree_fold(T, RT, crow, cdom, trow, tdom, gridDim.x, status);
+#ifdef DFA_TREE_TIMING
+        if (threadIdx.x == 0) atomicMax(&g_tree_t[22], gtimer() - tc2);
+#endif
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t fs = acc.v;
+        if (fs == T.poison) atomicMax(&status->err, 5u);
+        status->final_state = fs;
+        status->accept = fs < T.nq ? (uint32_t)test_bit(T.accept_bits, fs) : 0u;
+        if (dev_final) {
+            dev_final[0] = (uint16_t)fs;
+            dev_final[1] = (uint16_t)status->accept;
+        }
+#ifdef DFA_TREE_TIMING
+        atomicMax(&g_tree_t[19], gtimer());
+#endif
     }
 }
 
@@ -1046,6 +1375,7 @@ __global__ void fold_segments_kernel(DevTables T, const uint16_t *rows, const ui
 // ---------------------------------------------------------------------------
 __global__ void starts_kernel(DevTables T, Plan p, const uint16_t *row0, const uint16_t *rows, const uint16_t *dom,
                               uint16_t *starts, DevStatus *status) {
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     starts[0] = (uint16_t)T.q0;
     if (p.P < 2) return;
@@ -1136,6 +1466,9 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)fold_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute((void *)compose8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - kCompose8Static);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute((void *)tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
@@ -1179,7 +1512,8 @@ extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {
     if (reset) {
         unsigned long long init[32];
         init[0] = ~0ull;
-        for (int i = 1; i < 32; i++) init[i] = 0;
+        init[20] = ~0ull;
+        for (int i = 1; i < 32; i++) init[i] = (i == 10 || i == 14) ? ~0ull : 0;
         cudaMemcpyToSymbol(g_tree_t, init, sizeof(init));
     }
     return 0;
@@ -1204,9 +1538,43 @@ cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uin
     const uint32_t lrs = tree_lrs(T);
     const uint32_t grid = (P + per_cta - 1) / per_cta;
     const size_t smem = fold_rows_fixed_bytes(T) + ((per_cta + 7) & ~7u) * 2 + ((size_t)per_cta << lrs) * 2;
-    fold_rows_kernel<<<grid, 1024, smem, s>>>(T, rows, doms, P, per_cta, lrs, cta_rows, cta_doms, ticket, st,
+    fold_rows_kernel<<<grid, 256, smem, s>>>(T, rows, doms, P, per_cta, lrs, cta_rows, cta_doms, ticket, st,
                                               dev_final);
     return cudaGetLastError();
+}
+
+// the staged tables fit next to compose8_kernel's static shared memory
+int rtab_staged(const DevTables &T) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return (uint64_t)rtab_bytes(T) + kCompose8Static <= (uint64_t)optin ? 1 : 0;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const uint16_t *leaf_dom, uint32_t L0,
+                            uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
+                            uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
+                            uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final, cudaStream_t s) {
+    const int staged = rtab_staged(T);
+    const uint32_t grid = (P + cpc - 1) / cpc;
+    return launch_pdl(compose8_kernel, dim3(grid), dim3(1024), staged ? rtab_bytes(T) : 0, s, T, leaves, leaf_dom, L0,
+                      L, P, cpc, rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows, cta_doms, ticket, st,
+                      dev_final, staged);
 }
 
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
@@ -1220,8 +1588,7 @@ cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_b
 
 cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s) {
-    starts_kernel<<<1, 32, 0, s>>>(T, p, row0, rows, dom, starts, st);
-    return cudaGetLastError();
+    return launch_pdl(starts_kernel, dim3(1), dim3(32), 0, s, T, p, row0, rows, dom, starts, st);
 }
 
 } // namespace dfa
