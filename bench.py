@@ -57,6 +57,9 @@ def parse():
                     help="library option NAME=VALUE (subchunk_target, tree_fanin, threads_per_cta)")
     ap.add_argument("--profile", choices=["inline", "separate"], default="separate",
                     help="per-kernel CUDA events inside the timed loop (inline) or in a second loop of the same K steps")
+    ap.add_argument("--alg2", action="store_true",
+                    help="N2 ablation: match every sub-chunk from all of Q minus Z (Alg.2, P:753-790)")
+    ap.add_argument("--no-lookahead", action="store_true", help="skip the r-symbol lookahead (N1) report")
     ap.add_argument("--quiet-json", action="store_true", help="print a one-line summary instead of JSON")
     return ap.parse_args()
 
@@ -180,7 +183,7 @@ def main():
     x = w.input(n, segment=rank)
     dx = torch.from_numpy(x).to(dev)
 
-    d = D.Dfa(a.table, a.q0, a.accept_bitmap)
+    d = D.Dfa(a.table, a.q0, a.accept_bitmap, D.DFA_CREATE_FULL_DOMAIN if args.alg2 else 0)
     D.dfa_set_option(d.h, D.DFA_OPT_CONVERGENCE, args.convergence)
     for kv in args.opt:
         k, v = kv.split("=")
@@ -258,6 +261,26 @@ def main():
         e2e_ms = float(t.item())
     e2e = world * n / (e2e_ms * 1e-3) / 1e9
 
+    # N1 report (Tab.ISetMax analog): |I_{s1..sr}| over this input's P-1 chunk
+    # boundaries for r = 1..4 through dfa_lookahead_maps, restricting the last step's maps
+    look = None
+    if world == 1 and P > 1 and not args.no_lookahead:
+        look = {"states": a.nq, "boundaries": P - 1, "r": {}}
+        maps2 = maps.view(P - 1, imax)
+        for r in (1, 2, 3, 4):
+            la0 = torch.cuda.Event(enable_timing=True)
+            la1 = torch.cuda.Event(enable_timing=True)
+            la0.record(stream)
+            doms, sizes, maps_r = d.lookahead_maps(dx, bounds, maps2, r, stream=stream)
+            la1.record(stream)
+            torch.cuda.synchronize(dev)
+            if D.dfa_get_last_device_error(d.h) != 0:
+                raise SystemExit("device error in dfa_lookahead_maps")
+            sz = sizes.cpu().numpy().view(np.uint16).astype(np.int64)
+            look["r"][str(r)] = {"mean_domain": float(sz.mean()), "max_domain": int(sz.max()),
+                                 "mean_pct_of_Q": 100.0 * float(sz.mean()) / a.nq,
+                                 "kernel_ms": la0.elapsed_time(la1)}
+
     if rank != 0:
         dist.barrier() if dist else None
         return 0
@@ -286,7 +309,9 @@ def main():
                    "input_bytes_per_gpu": n, "chunks": P, "states": a.nq, "alphabet": a.ns,
                    "i_max": imax, "gamma": f"{d.info['gamma_num']}/{d.info['gamma_den']}",
                    "table_mode": d.info["table_mode_name"], "chunk_ratio_c": f"{d.info['c_num']}/{d.info['c_den']}",
-                   "convergence": bool(args.convergence), "l2": "input 256 MiB+ > 126 MB L2, no flush",
+                   "convergence": bool(args.convergence),
+                   "domains": "Q minus Z for every sub-chunk (Alg.2 ablation)" if args.alg2 else "I_sigma (Alg.3)",
+                   "l2": "input 256 MiB+ > 126 MB L2, no flush",
                    "seed": args.seed, "input_sha256": W.sha256(x)[:16],
                    "kernel_timing": ("CUDA events around each kernel inside the timed loop" if args.profile == "inline"
                                      else "CUDA events around each kernel in a second loop of the same K steps "
@@ -307,6 +332,8 @@ def main():
         "gpu_launches": int(stats["num_kernels"]) * args.steps,
         "clocks": clocks,
     }
+    if look:
+        line["lookahead"] = look
     if not args.no_cpu_baseline and world == 1:
         import oracle
         od = oracle.Dfa(a.table, a.q0, a.accepting)
@@ -323,8 +350,11 @@ def main():
         line["parity"] = {"final_state_gpu": int(fin_state), "final_state_oracle": int(fin_cpu),
                           "match": int(fin_state) == int(fin_cpu)}
     if args.quiet_json:
-        print(f"{args.config} {' '.join(args.opt)} value={value:.1f} GB/s ms={ms:.4f} "
+        print(f"{args.config}{' alg2' if args.alg2 else ''} {' '.join(args.opt)} value={value:.1f} GB/s ms={ms:.4f} "
               f"kernels={ {k: round(v, 4) for k, v in line['kernels_ms_per_step'].items()} }")
+        if look:
+            print("  lookahead |I_r| mean/max:", {r: (round(v["mean_domain"], 2), v["max_domain"])
+                                                   for r, v in look["r"].items()})
     else:
         print(json.dumps(line))
     if dist:

@@ -95,7 +95,10 @@ enum {
 
 /* dfa_create_ex flags */
 enum {
-    DFA_CREATE_HOST_ONLY = 1  /* analysis only: no device memory touched; compute calls fail */
+    DFA_CREATE_HOST_ONLY = 1,  /* analysis only: no device memory touched; compute calls fail */
+    DFA_CREATE_FULL_DOMAIN = 2 /* Alg.2 ablation: every sub-chunk matched from all of
+                                  Q \ Z instead of I_sigma; results identical, i_max unchanged
+                                  (API rows stay over I_sigma), speed shows the I_sigma win */
 };
 
 /*
@@ -169,6 +172,28 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
                              uint32_t num_chunks, const uint64_t *dev_bounds_in, void *stream,
                              uint16_t *dev_chunk0_end, uint16_t *dev_maps,
                              uint16_t *dev_chunk_start, uint16_t *dev_final);
+
+/*
+ * dfa_lookahead_maps: multiple reverse lookahead symbols (PAPER.md Sec.
+ * "Multiple Reverse Lookahead Symbols"; Eq.istatesm P:1142-1147,
+ * Alg.TwoSymISet).  Restricts the maps of a preceding
+ * dfa_chunk_maps(_at) call (same stream, same input and partition) to the
+ * r-symbol initial-state sets.  For chunk k = 1..P-1, with L = min(r, b_k)
+ * and s1..sL = x[b_k-L .. b_k-1] (matching order):
+ *   dev_domains[(k-1)*i_max + i] = i-th state of I_{s1..sL} = delta-hat(Q, s1..sL) \ Z (ascending)
+ *   dev_maps_r [(k-1)*i_max + i] = delta-hat(that state, C_k), taken from dev_maps
+ *                                  (Lemma 1: I_{s1..sL} is a subset of I_{sL})
+ *   dev_domain_sizes[k-1]        = |I_{s1..sL}|
+ * Unused entries are 0xFFFF.  Inputs (device): dev_input[len], dev_bounds[P+1]
+ * and dev_maps[(P-1)*i_max] as written by the chunk-maps call; outputs
+ * (device): dev_domains and dev_maps_r [(P-1)*i_max], dev_domain_sizes[P-1].
+ * r = 1..16 (r = 1 reproduces I_sigma).  P == 1: nothing to do.  Asynchronous;
+ * a lookahead byte >= |Sigma| is reported by dfa_get_last_device_error.
+ * O(r |Q|) table reads per chunk.
+ */
+dfa_status dfa_lookahead_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
+                              const uint64_t *dev_bounds, const uint16_t *dev_maps, uint32_t r, void *stream,
+                              uint16_t *dev_domains, uint16_t *dev_domain_sizes, uint16_t *dev_maps_r);
 
 /*
  * Multi-GPU sharding (the paper's two-tier merge, Fig.Merge

@@ -60,6 +60,7 @@ def lib():
         L.oracle_initial_states.restype = u32
         L.oracle_initial_states_r.argtypes = [P, u32, u32, P, P, u32, P]
         L.oracle_initial_states_r.restype = u32
+        L.oracle_chunk_map_r.argtypes = [P, u32, u32, P, P, u64, u64, u64, u32, u32, P, P, P]
         L.oracle_imax.argtypes = [P, u32, u32, P]
         L.oracle_imax.restype = u32
         L.oracle_chunk_bounds.argtypes = [u64, u32, u32, P, P]
@@ -159,6 +160,18 @@ class Dfa:
                                       int(begin), int(end), row_len, _p(row), _p(cnt)),
                "oracle_chunk_map")
         return row[:row_len].copy(), int(cnt[0])
+
+    def chunk_map_r(self, x: np.ndarray, begin: int, end: int, r: int, row_len: int):
+        """(domain, row, |domain|) of chunk [begin, end) over I_{s1..sL}, L = min(r, begin)
+        lookahead symbols (Eq.istatesm)."""
+        x = np.ascontiguousarray(x, dtype=np.uint8)
+        row = np.zeros(max(row_len, 1), np.uint16)
+        dom = np.zeros(max(row_len, 1), np.uint16)
+        cnt = np.zeros(1, np.uint32)
+        _check(lib().oracle_chunk_map_r(_p(self.table), self.nq, self.ns, _p(self.dead), _p(x), x.size,
+                                        int(begin), int(end), int(r), row_len, _p(dom), _p(row), _p(cnt)),
+               "oracle_chunk_map_r")
+        return dom[:row_len].copy(), row[:row_len].copy(), int(cnt[0])
 
     def maps(self, x: np.ndarray, bounds: np.ndarray, row_len: int, threads: int = 0):
         """(chunk0_end, maps[(P-1), row_len]) for the partition `bounds` (P+1 entries)."""

@@ -250,6 +250,43 @@ int oracle_chunk_map(const uint16_t *delta, uint32_t nq, uint32_t ns,
     return ORACLE_OK;
 }
 
+/* ------------------------------------------------------------------------
+ * Chunk map with r reverse lookahead symbols (Sec. "Multiple Reverse
+ * Lookahead Symbols"): the domain of chunk [begin, end) is
+ * I_{s1..sL} of Eq.istatesm for the L = min(r, begin) symbols before it,
+ * s1..sL = x[begin-L .. begin-1] in matching order; the row
+ * holds delta-hat(q, x[begin..end)) for every q of that domain (ascending),
+ * dom receives the domain.  Unused entries of both are 0xFFFF.
+ * ------------------------------------------------------------------------ */
+int oracle_chunk_map_r(const uint16_t *delta, uint32_t nq, uint32_t ns,
+                       const uint8_t *dead, const uint8_t *x, uint64_t n,
+                       uint64_t begin, uint64_t end, uint32_t r,
+                       uint32_t row_len, uint16_t *dom, uint16_t *row,
+                       uint32_t *domain_size) {
+    if (begin == 0 || begin > end || end > n || r == 0) return ORACLE_BAD_ARG;
+    uint32_t L = (uint64_t)r < begin ? r : (uint32_t)begin;
+    const uint8_t *syms = x + (begin - L);
+    for (uint32_t i = 0; i < L; i++)
+        if (syms[i] >= ns) return ORACLE_BAD_SYMBOL;
+    uint16_t *I = (uint16_t *)malloc(sizeof(uint16_t) * (nq ? nq : 1));
+    uint32_t count = oracle_initial_states_r(delta, nq, ns, dead, syms, L, I);
+    if (count > row_len) { free(I); return ORACLE_BAD_ARG; }
+    for (uint32_t j = 0; j < row_len; j++) { row[j] = 0xFFFF; dom[j] = 0xFFFF; }
+    for (uint32_t j = 0; j < count; j++) {         /* foreach q in I_{s1..sL} */
+        uint32_t state = I[j];
+        for (uint64_t p = begin; p < end; p++) {  /* for k <- Start to End   */
+            uint32_t c = x[p];
+            if (c >= ns) { free(I); return ORACLE_BAD_SYMBOL; }
+            state = delta[(uint64_t)state * ns + c];
+        }
+        dom[j] = I[j];
+        row[j] = (uint16_t)state;
+    }
+    free(I);
+    if (domain_size) *domain_size = count;
+    return ORACLE_OK;
+}
+
 /* All maps of a partition, chunks 1..P-1 (chunk 0 yields only its end state,
  * P:803-804, 1062-1066), run in parallel over chunks with plain pthreads --
  * the "forpar" of Alg.MatchingInitialStates line 8.  maps has

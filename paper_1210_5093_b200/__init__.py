@@ -21,12 +21,14 @@ __all__ = [
     "DfaError", "dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
     "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
     "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
-    "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments", "Dfa", "lib", "EXPORTED",
+    "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
+    "dfa_lookahead_maps", "Dfa", "lib", "EXPORTED",
 ]
 
 DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
 DFA_ERR_SYMBOL, DFA_ERR_OOM, DFA_ERR_CUDA, DFA_ERR_INTERNAL = 5, 6, 7, 8
 DFA_CREATE_HOST_ONLY = 1
+DFA_CREATE_FULL_DOMAIN = 2
 DFA_OPT_SUBCHUNK_TARGET, DFA_OPT_CONVERGENCE, DFA_OPT_PROFILE, DFA_OPT_THREADS_PER_CTA = 1, 2, 3, 4
 DFA_OPT_TREE_FANIN = 5
 DFA_OPT_FOLD_IN_TREE = 6
@@ -59,7 +61,8 @@ class DfaError(RuntimeError):
 EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_domain",
             "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
             "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
-            "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments"]
+            "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
+            "dfa_lookahead_maps"]
 
 _lib = None
 
@@ -90,6 +93,7 @@ def lib():
             "dfa_get_stats": [V, V],
             "dfa_segment_map": [V, V, u64, ctypes.c_int32, V, V],
             "dfa_fold_segments": [V, V, V, u32, V, V],
+            "dfa_lookahead_maps": [V, V, u64, u32, V, V, u32, V, V, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -225,6 +229,15 @@ def dfa_chunk_maps_at(h, dev_input, P: int, dev_bounds_in, dev_chunk0_end, dev_m
         "dfa_chunk_maps_at")
 
 
+def dfa_lookahead_maps(h, dev_input, P: int, dev_bounds, dev_maps, r: int, dev_domains, dev_domain_sizes,
+                       dev_maps_r, n: Optional[int] = None, stream=None):
+    """Chunk maps restricted to r reverse lookahead symbols (Eq.istatesm)."""
+    n = dev_input.numel() if n is None else int(n)
+    _ck(lib().dfa_lookahead_maps(h, _ptr(dev_input), n, int(P), _ptr(dev_bounds), _ptr(dev_maps), int(r),
+                                 _stream(stream), _ptr(dev_domains), _ptr(dev_domain_sizes), _ptr(dev_maps_r)),
+        "dfa_lookahead_maps")
+
+
 def dfa_segment_map(h, dev_input, lookahead: int, dev_row, n: Optional[int] = None, stream=None):
     """Map of one input segment over I_sigma(lookahead) (lookahead -1: from q0)."""
     n = dev_input.numel() if n is None else int(n)
@@ -300,3 +313,16 @@ class Dfa:
         final = torch.empty(2, dtype=torch.int16, device=dev)
         dfa_chunk_maps(self.h, dev_input, P, bounds, e0, maps, starts, final, stream=stream)
         return bounds, e0, maps.view(max(P - 1, 1), imax)[:P - 1], starts, final
+
+    def lookahead_maps(self, dev_input, bounds, maps, r: int, stream=None):
+        """Restrict chunk_maps() results to r reverse lookahead symbols; returns
+        (domains, sizes, maps_r) as torch tensors ([P-1, i_max], [P-1], [P-1, i_max])."""
+        import torch
+        dev = dev_input.device
+        P = bounds.numel() - 1
+        imax = self.info["i_max"]
+        doms = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=dev)
+        sizes = torch.empty(max(P - 1, 1), dtype=torch.int16, device=dev)
+        maps_r = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=dev)
+        dfa_lookahead_maps(self.h, dev_input, P, bounds, maps, r, doms, sizes, maps_r, stream=stream)
+        return doms.view(max(P - 1, 1), imax)[:P - 1], sizes[:P - 1], maps_r.view(max(P - 1, 1), imax)[:P - 1]

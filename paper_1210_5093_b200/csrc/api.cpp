@@ -151,9 +151,10 @@ dfa_status upload(dfa_handle *h) {
         }
     }
     const uint32_t bw = ((nq + 31) / 32 + 3) & ~3u;
-    std::vector<uint32_t> dead(bw, 0), absorb(bw, 0), accept(bw, 0);
+    std::vector<uint32_t> dead(bw, 0), absorb(bw, 0), accept(bw, 0), dead_user(bw, 0);
     for (uint32_t q = 0; q < nq; q++) {
         if (p.dead[q]) dead[q >> 5] |= 1u << (q & 31);
+        if (q < p.nq_user && p.dead_user[q]) dead_user[q >> 5] |= 1u << (q & 31);
         if (p.absorbing[q]) absorb[q >> 5] |= 1u << (q & 31);
         if (p.accepting[q]) accept[q >> 5] |= 1u << (q & 31);
     }
@@ -173,6 +174,7 @@ dfa_status upload(dfa_handle *h) {
         {dom_user_size.data(), dom_user_size.size() * 2, 0},
         {rank8.data(), rank8.size(), 0},
         {ixlat.data(), ixlat.size() * 2, 0},
+        {dead_user.data(), dead_user.size() * 4, 0},
     };
     size_t total = 0;
     for (auto &s : secs) { s.off = total; total += (s.bytes + 255) & ~size_t(255); }
@@ -196,6 +198,9 @@ dfa_status upload(dfa_handle *h) {
     T.dom_user_size = reinterpret_cast<const uint16_t *>(at(10));
     T.rank8 = rank8.empty() ? nullptr : at(11);
     T.ixlat = reinterpret_cast<const uint16_t *>(at(12));
+    T.dead_user_bits = reinterpret_cast<const uint32_t *>(at(13));
+    T.nq_user = p.nq_user;
+    T.ns = p.ns;
     T.nq = nq;
     T.nclass = nc;
     T.start_dom = p.start_dom;
@@ -685,7 +690,8 @@ dfa_status dfa_create_ex(const uint16_t *table, uint32_t num_states, uint32_t al
         dfa_status ps = probe(h.get(), u8_limit);
         if (ps != DFA_OK) return ps;
     }
-    int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, u8_limit, h->prep);
+    int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, u8_limit, h->prep,
+                     (flags & DFA_CREATE_FULL_DOMAIN) != 0);
     if (st != 0) return (dfa_status)st;
     if (!(flags & DFA_CREATE_HOST_ONLY)) {
         dfa_status ds = upload(h.get());
@@ -888,6 +894,25 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
     o.final2 = dev_final;
     const Split sp = plan_split(h, len, P, hb.data(), true);
     return run(h, dev_input, len, P, dev_bounds_in, sp, s, o);
+}
+
+dfa_status dfa_lookahead_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
+                              const uint64_t *dev_bounds, const uint16_t *dev_maps, uint32_t r, void *stream,
+                              uint16_t *dev_domains, uint16_t *dev_domain_sizes, uint16_t *dev_maps_r) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    const uint32_t P = num_chunks;
+    if (P == 0 || len < P) return DFA_ERR_CHUNKS;
+    if (r < 1 || r > 16) return DFA_ERR_ARG;
+    if (P == 1) return DFA_OK;
+    if (!dev_input || !dev_bounds || !dev_maps || !dev_domains || !dev_domain_sizes || !dev_maps_r)
+        return DFA_ERR_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    h->last_stream = s;
+    CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
+    CK(launch_lookahead(h->T, dev_input, dev_bounds, P, r, dev_maps, dev_domains, dev_domain_sizes, dev_maps_r,
+                        h->status.as<DevStatus>(), h->sms, s));
+    return DFA_OK;
 }
 
 dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, int32_t lookahead, void *stream,

@@ -1370,6 +1370,68 @@ __global__ void fold_segments_kernel(DevTables T, const uint16_t *rows, const ui
 }
 
 // ---------------------------------------------------------------------------
+// lookahead_kernel (N1): the chunk maps restricted to r reverse lookahead
+// symbols (Sec. "Multiple Reverse Lookahead Symbols").  A warp
+// per chunk k >= 1: the image of the user states Q under the L = min(r, b_k)
+// bytes before b_k (Eq.istatesm, O(L |Q|) table reads) marks a bitmap; the
+// chunk's I_sigma (sigma = x[b_k - 1]) is then walked in its ascending order
+// and the marked states kept with their map entries (Lemma 1: the r-symbol
+// set is a subset of I_sigma), compacted with ballots.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lookahead_kernel(DevTables T, const uint8_t *in, const uint64_t *bounds,
+                                                        uint32_t P, uint32_t r, const uint16_t *maps,
+                                                        uint16_t *doms_out, uint16_t *sizes_out, uint16_t *maps_out,
+                                                        DevStatus *status) {
+    extern __shared__ uint32_t lbm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t bw = (T.nq_user + 31) / 32;
+    uint32_t *bm = lbm + warp * bw;
+    const uint32_t imu = T.imax_user;
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t k = 1 + blockIdx.x * (blockDim.x >> 5) + warp; k < P; k += nwarps) {
+        const uint64_t b = bounds[k];
+        const uint32_t L = (uint64_t)r < b ? r : (uint32_t)b;
+        const uint8_t *sy = in + (b - L);
+        for (uint32_t i = lane; i < bw; i += 32) bm[i] = 0;
+        if (lane < L && sy[lane] >= T.ns) atomicMax(&status->err, 5u);
+        __syncwarp();
+        for (uint32_t q = lane; q < T.nq_user; q += 32) {
+            uint32_t st = q;
+            for (uint32_t i = 0; i < L; i++) st = __ldg(T.gtable + (uint64_t)st * 256 + sy[i]);
+            if (st < T.nq_user && !test_bit(T.dead_user_bits, st)) atomicOr(&bm[st >> 5], 1u << (st & 31));
+        }
+        __syncwarp();
+        const uint32_t c = T.byte_class[sy[L - 1]];
+        const uint32_t du = c < T.nclass ? T.dom_user_size[c] : 0u;
+        uint16_t *dout = doms_out + (uint64_t)(k - 1) * imu, *mout = maps_out + (uint64_t)(k - 1) * imu;
+        const uint16_t *min_ = maps + (uint64_t)(k - 1) * imu;
+        uint32_t count = 0;
+        for (uint32_t j0 = 0; j0 < du; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            uint32_t st = 0;
+            bool keep = false;
+            if (j < du) {
+                st = T.dom_list[(uint64_t)c * T.imax + T.xlat[(uint64_t)c * imu + j]];
+                keep = (bm[st >> 5] >> (st & 31)) & 1u;
+            }
+            const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const uint32_t pos = count + __popc(mask & ((1u << lane) - 1u));
+                dout[pos] = (uint16_t)st;
+                mout[pos] = min_[j];
+            }
+            count += __popc(mask);
+        }
+        for (uint32_t i = count + lane; i < imu; i += 32) {
+            dout[i] = kNone;
+            mout[i] = kNone;
+        }
+        if (lane == 0) sizes_out[k - 1] = (uint16_t)count;
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // starts_kernel (optional output): true initial state of every reporting
 // chunk, the prefix of Eq.SeqReduction.  One thread, P dependent steps.
 // ---------------------------------------------------------------------------
@@ -1465,6 +1527,8 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)fold_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute((void *)lookahead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)compose8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              optin - kCompose8Static);
@@ -1575,6 +1639,16 @@ cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const ui
     return launch_pdl(compose8_kernel, dim3(grid), dim3(1024), staged ? rtab_bytes(T) : 0, s, T, leaves, leaf_dom, L0,
                       L, P, cpc, rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows, cta_doms, ticket, st,
                       dev_final, staged);
+}
+
+cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,
+                             const uint16_t *maps, uint16_t *doms_out, uint16_t *sizes_out, uint16_t *maps_out,
+                             DevStatus *st, int sms, cudaStream_t s) {
+    if (P < 2) return cudaSuccess;
+    const uint32_t smem = 8 * ((T.nq_user + 31) / 32) * 4;
+    const uint32_t grid = std::min<uint32_t>((P - 1 + 7) / 8, (uint32_t)sms * 8);
+    lookahead_kernel<<<grid, 256, smem, s>>>(T, in, bounds, P, r, maps, doms_out, sizes_out, maps_out, st);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {

@@ -39,7 +39,9 @@ struct DevTables {
     const uint16_t *xlat;       // [nclass * imax_user]
     const uint16_t *ixlat;      // [nclass * rs]: user index of internal entry j, or 0xFFFF
     const uint16_t *dom_user_size; // [nclass]
+    const uint32_t *dead_user_bits; // user Z (reading R1) over the user states
     uint32_t nq, nclass, start_dom, imax, imax_user;
+    uint32_t nq_user, ns;       // user |Q| and |Sigma|
     uint32_t rs;                // map row stride: imax rounded up to 8 (16-byte rows)
     uint32_t has_dead;          // internal Z non-empty
     uint32_t has_absorb;        // some state absorbs every byte
@@ -129,6 +131,9 @@ int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s);
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
+cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,
+                             const uint16_t *maps, uint16_t *doms_out, uint16_t *sizes_out, uint16_t *maps_out,
+                             DevStatus *st, int sms, cudaStream_t s);
 cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const uint16_t *leaf_dom, uint32_t L0,
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,

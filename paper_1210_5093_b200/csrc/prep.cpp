@@ -41,7 +41,8 @@ uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uin
 }
 
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
-            const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &p) {
+            const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &p,
+            bool full_domain) {
     if (!table || !accept_bitmap) return ST_ARG;
     if (ns == 0 || ns > 256) return ST_ALPHABET;
     if (nq == 0 || nq > kMaxStates || q0 >= nq) return ST_STATES;
@@ -123,15 +124,23 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
     p.dom_user.assign(p.nclass, {});
     p.xlat.assign(p.nclass, {});
     std::vector<uint8_t> mark(p.nq);
+    // Alg.2 ablation (full_domain): every sub-chunk is matched from all states
+    // Q \ Z; the API rows stay over I_sigma, read out of the
+    // full map through xlat.
+    std::vector<uint16_t> full_idx(p.nq, kNone), live;
+    for (uint32_t q = 0; q < p.nq; q++)
+        if (!p.dead[q]) { full_idx[q] = uint16_t(live.size()); live.push_back(uint16_t(q)); }
+    p.full_domain = full_domain;
     for (uint32_t c = 0; c < p.nclass; c++) {
         std::fill(mark.begin(), mark.end(), 0);
         uint32_t b = p.class_rep[c];
         for (uint32_t q = 0; q < p.nq; q++) mark[p.full[(size_t)q * 256 + b]] = 1;
+        if (full_domain) p.dom[c] = live;
         for (uint32_t q = 0; q < p.nq; q++) {
             if (!mark[q]) continue;
-            if (!p.dead[q]) p.dom[c].push_back(uint16_t(q));
+            if (!full_domain && !p.dead[q]) p.dom[c].push_back(uint16_t(q));
             if (!p.dead_user[q]) {
-                p.xlat[c].push_back(uint16_t(p.dom[c].size() - 1));
+                p.xlat[c].push_back(full_domain ? full_idx[q] : uint16_t(p.dom[c].size() - 1));
                 p.dom_user[c].push_back(uint16_t(q));
             }
         }

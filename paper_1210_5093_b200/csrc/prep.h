@@ -57,6 +57,7 @@ struct Prep {
     uint32_t num_dead_user = 0, num_absorbing_user = 0;
     uint16_t first_dead_user = kNone;
     uint32_t nclass_user = 0;        // classes containing a valid symbol
+    bool full_domain = false;        // Alg.2 ablation: dom[c] = Q \ Z for every class
     // device table layout
     int mode = 0;
     uint32_t stride = 0;             // entries per row (u8/u16) or words per row (packed9)
@@ -68,7 +69,8 @@ struct Prep {
 // u8_state_limit: largest internal |Q| for the IdentU8 layout (256 minus the
 // shared-address bias of the table, see Tab<kIdentU8> in kernels.cu).
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
-            const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &out);
+            const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &out,
+            bool full_domain = false);
 
 // Exact c-form partition (header dfa.h), 128-bit integer arithmetic.
 uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uint32_t k);

@@ -30,16 +30,16 @@ class Case:
         self.od = oracle.Dfa(aut.table, aut.q0, aut.accepting)
         self.name = name
 
-    def handle(self, opts=None):
-        d = D.Dfa(self.a.table, self.a.q0, self.a.accept_bitmap)
+    def handle(self, opts=None, flags=0):
+        d = D.Dfa(self.a.table, self.a.q0, self.a.accept_bitmap, flags)
         for k, v in (opts or {}).items():
             D.dfa_set_option(d.h, k, v)
         return d
 
 
-def check_chunk_maps(c: Case, P: int, c_num=1, c_den=1, opts=None, dev=None, maps_rows=None):
+def check_chunk_maps(c: Case, P: int, c_num=1, c_den=1, opts=None, dev=None, maps_rows=None, flags=0):
     """Full parity of bounds, e0, every map entry, true chunk starts, final, accept."""
-    d = c.handle(opts)
+    d = c.handle(opts, flags)
     try:
         D.dfa_set_chunk_ratio(d.h, c_num, c_den)
         x = c.x
@@ -69,8 +69,8 @@ def check_chunk_maps(c: Case, P: int, c_num=1, c_den=1, opts=None, dev=None, map
         d.close()
 
 
-def check_match(c: Case, opts=None):
-    d = c.handle(opts)
+def check_match(c: Case, opts=None, flags=0):
+    d = c.handle(opts, flags)
     try:
         fin, acc = d.match(torch.from_numpy(c.x).to(DEV))
         ofin = c.od.run(c.x)
@@ -402,3 +402,68 @@ def test_repeated_calls_graph_replay():
             assert u16(e0)[0] == oe0 and np.array_equal(u16(maps), omaps) and u16(final)[0] == ofin, rep
     finally:
         d.close()
+
+
+# ------------------------------------------------------------------ N1: r-symbol reverse lookahead
+def check_lookahead(c: Case, P: int, rs=(1, 2, 3, 4), bounds_in=None):
+    """dfa_lookahead_maps against oracle.chunk_map_r, every chunk, every entry."""
+    d = c.handle()
+    try:
+        x = c.x
+        dx = torch.from_numpy(x).to(DEV)
+        imax = d.info["i_max"]
+        if bounds_in is None:
+            bounds, e0, maps, _, _ = d.chunk_maps(dx, P)
+        else:
+            bounds = torch.from_numpy(np.asarray(bounds_in, np.int64)).to(DEV)
+            e0 = torch.empty(1, dtype=torch.int16, device=DEV)
+            maps = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=DEV)
+            D.dfa_chunk_maps_at(d.h, dx, P, bounds, e0, maps)
+            maps = maps.view(max(P - 1, 1), imax)[:P - 1]
+        ob = bounds.cpu().numpy().astype(np.int64)
+        for r in rs:
+            doms, sizes, maps_r = d.lookahead_maps(dx, bounds, maps, r)
+            torch.cuda.synchronize()
+            assert D.dfa_get_last_device_error(d.h) == 0
+            gd, gs, gm = u16(doms), u16(sizes), u16(maps_r)
+            for k in range(1, P):
+                dom, row, cnt = c.od.chunk_map_r(x, int(ob[k]), int(ob[k + 1]), r, imax)
+                assert gs[k - 1] == cnt, f"r={r} chunk {k}: |domain| {gs[k - 1]} != {cnt}"
+                assert np.array_equal(gd[k - 1], dom), f"r={r} chunk {k}: domain"
+                assert np.array_equal(gm[k - 1], row), f"r={r} chunk {k}: map"
+    finally:
+        d.close()
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_lookahead_maps_configs(name):
+    w = W.get(name)
+    x = w.input(1 << 16)
+    check_lookahead(Case(w.automaton, x, name), 97)
+
+
+def test_lookahead_maps_short_prefix():
+    """Chunks starting before offset r use the L = b_k < r available symbols."""
+    w = W.get("keyword")
+    x = w.input(4096)
+    b = [0, 1, 2, 3, 5, 8, 13, 100, 1000, 4096]
+    check_lookahead(Case(w.automaton, x, "keyword"), len(b) - 1, rs=(1, 2, 4, 16), bounds_in=b)
+
+
+def test_lookahead_maps_sink_and_small_alphabet():
+    for seed in range(3):
+        a = automata.random_dfa_with_sink(40, 5, seed)
+        x = np.random.default_rng(seed).integers(0, 5, 3000).astype(np.uint8)
+        check_lookahead(Case(a, x, f"sink{seed}"), 31, rs=(1, 2, 3, 5))
+
+
+# ------------------------------------------------------------------ N2: Alg. 2 ablation (all of Q minus Z)
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_alg2_full_domain_parity(name):
+    """DFA_CREATE_FULL_DOMAIN matches every sub-chunk from Q minus Z (Alg.2):
+    identical results, including the API rows over I_sigma."""
+    w = W.get(name)
+    x = w.input(min(w.small_n, 1 << 20))
+    c = Case(w.automaton, x, name)
+    check_chunk_maps(c, 61, flags=D.DFA_CREATE_FULL_DOMAIN)
+    check_match(c, flags=D.DFA_CREATE_FULL_DOMAIN)

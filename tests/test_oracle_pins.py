@@ -333,3 +333,68 @@ def test_bad_symbol_detected():
     d = Dfa(automata.counter_dfa(5, 4).table, 0, [0])
     with pytest.raises(oracle.OracleError):
         d.run(np.array([0, 1, 4], np.uint8))
+
+
+# --------------------------------------------------------------------------- N1: r-symbol lookahead
+def test_lookahead2_example_golden(golden_dir):
+    """Eq.istatesm / Alg.TwoSymISet on Fig.ExampleDFA, values derived by hand
+    in the fixture; chunk maps over I_{s1 s2} for the Fig.InputString split."""
+    g = load(golden_dir, "fig_example_dfa.json")
+    h = load(golden_dir, "fig_example_lookahead2.json")
+    d = example_dfa(g)
+    sym = g["symbols"]
+    for w, want in h["I2"].items():
+        assert d.initial_states_r([sym[c] for c in w]).tolist() == want
+    assert max(len(v) for v in h["I2"].values()) == h["I_max_2"]
+    x = enc(g["input"], sym)
+    for ch in h["chunks_m2_r2"]:
+        dom, row, cnt = d.chunk_map_r(x, ch["begin"], ch["end"], 2, 2)
+        assert dom[:cnt].tolist() == ch["domain"] and row[:cnt].tolist() == ch["row"]
+        assert (dom[cnt:] == 0xFFFF).all() and (row[cnt:] == 0xFFFF).all()
+
+
+def test_chunk_map_r_properties():
+    """r-symbol maps against brute force: the true state at every chunk start is
+    in the r-domain (unless in Z) and its entry is the true state at the chunk
+    end (sequential run); r = 1 is the I_sigma map; the r-domain shrinks with r
+    (Lemma 1) and its rows are the I_sigma rows restricted (same delta-hat)."""
+    rng = np.random.default_rng(11)
+    for seed in range(6):
+        aut = automata.random_structured(30, 5, 8, 6, seed) if seed % 2 else automata.random_dfa_with_sink(25, 4, seed)
+        d = Dfa(aut.table, aut.q0, aut.accepting)
+        dead = d.dead
+        ns = aut.table.shape[1]
+        x = rng.integers(0, ns, 400).astype(np.uint8)
+        cuts = np.sort(rng.choice(np.arange(1, x.size), 12, replace=False))
+        bounds = np.concatenate([[0], cuts, [x.size]])
+        at, fin = d.run_record(x, bounds[:-1].astype(np.uint64))
+        truth = at.tolist() + [fin]
+        for k in range(1, bounds.size - 1):
+            b, e = int(bounds[k]), int(bounds[k + 1])
+            row1, c1 = d.chunk_map(x, b, e, d.nq)
+            I1 = d.initial_states(int(x[b - 1])).tolist()
+            prev = None
+            for r in range(1, 6):
+                dom, row, cnt = d.chunk_map_r(x, b, e, r, d.nq)
+                D = dom[:cnt].tolist()
+                if r == 1:
+                    assert D == I1 and row[:cnt].tolist() == row1[:c1].tolist()
+                if prev is not None:
+                    assert set(D) <= set(prev)
+                prev = D
+                # brute force domain: the image of every state under the L symbols before b
+                L = min(r, b)
+                img = set()
+                for q in range(d.nq):
+                    s = q
+                    for c in x[b - L:b]:
+                        s = int(aut.table[s, c])
+                    if not dead[s]:
+                        img.add(s)
+                assert D == sorted(img)
+                for i, q in enumerate(D):
+                    assert row[i] == row1[I1.index(q)]
+                t = int(truth[k])
+                if not dead[t]:
+                    assert t in D
+                    assert row[D.index(t)] == truth[k + 1]
