@@ -66,6 +66,7 @@ struct dfa_handle {
     // scratch
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
+    DevBuf cta_start;
     int warp_compose = 1;
     std::vector<uint64_t> plan_key;
     // CUDA graph of a repeated dfa_chunk_maps call
@@ -449,6 +450,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         const uint32_t g2 = (P + cpc - 1) / cpc;
         CK(h->fold_rows.ensure((uint64_t)g2 * T.rs * 2 + 256));
         CK(h->fold_doms.ensure((uint64_t)g2 * 2 + 256));
+        if (o.starts) CK(h->cta_start.ensure((uint64_t)g2 * 2 + 256));
         if (!h->ticket.p) {
             CK(h->ticket.ensure(256));
             CK(cudaMemsetAsync(h->ticket.p, 0, 256, s));
@@ -458,13 +460,9 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         CK(launch_compose8(T, h->leaf_rows.as<uint16_t>(), h->leaf_dom.as<uint16_t>(), L0, Lm, P, cpc, rep_rows,
                            rep_doms, o.user_maps, o.user_row0, o.chunk0_end, h->fold_rows.as<uint16_t>(),
                            h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(), h->status.as<DevStatus>(), o.final2,
-                           s));
+                           h->cta_start.as<uint16_t>(), o.starts, s));
         prof_end(h, s);
-        kernels += 1;
-        if (o.starts) {
-            CK(launch_starts(T, plan, rep_rows, rep_rows + T.rs, rep_doms, o.starts, h->status.as<DevStatus>(), s));
-            kernels++;
-        }
+        kernels += o.starts ? 2 : 1;
         h->stats.num_kernels = kernels;
         return DFA_OK;
     }
@@ -712,7 +710,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->last_stream) cudaStreamSynchronize(h->last_stream);
         for (DevBuf *b : {&h->tables, &h->status, &h->sfin, &h->dom_of, &h->surv, &h->surv_n, &h->surv_pos,
                           &h->amap, &h->lvlA, &h->domA, &h->counters, &h->bounds, &h->input, &h->fold_rows,
-                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds})
+                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds, &h->cta_start})
             b->release();
         h->h_status.release();
         h->h_bounds.release();

@@ -1219,6 +1219,40 @@ __device__ __forceinline__ LMap cta_tree_fold(const DevTables &T, const RTab &R,
     return m;
 }
 
+// One state through one map (row of <= 8 entries over domain dom): error
+// states stay, else the entry at the state's rank.
+__device__ __forceinline__ uint32_t map_step(const DevTables &T, const RTab &R, const uint16_t *row, uint32_t dom,
+                                             uint32_t st, DevStatus *status) {
+    if (T.has_dead && test_bit(R.dead, st)) return st;
+    const uint32_t r = R.rank8[dom * T.nq + st];
+    if (r >= (uint32_t)kLanes) { atomicMax(&status->err, 8u); return st; }
+    return row[r];
+}
+
+// starts8_kernel: true start of every reporting chunk (optional output): CTA b
+// walks its compose8 chunks from cta_start[b].  Launched dependent.
+__global__ void __launch_bounds__(256) starts8_kernel(DevTables T, const uint16_t *rep_rows, const uint16_t *rep_doms,
+                                                     uint32_t P, uint32_t cpc, const uint16_t *cta_start,
+                                                     uint16_t *starts, DevStatus *status, int staged) {
+    extern __shared__ __align__(16) uint8_t rsm[];
+    const RTab RT = stage_rtab(T, rsm, staged);
+    __shared__ __align__(16) uint16_t srow[1024 * 8];
+    __shared__ uint16_t sdom[1024];
+    pdl_wait();
+    const uint32_t c0 = blockIdx.x * cpc, c1 = min(P, c0 + cpc), n = c1 - c0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        reinterpret_cast<uint4 *>(srow)[i] = __ldcg(reinterpret_cast<const uint4 *>(rep_rows) + c0 + i);
+        sdom[i] = __ldcg(rep_doms + c0 + i);
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    uint32_t st = __ldcg(cta_start + blockIdx.x);
+    for (uint32_t i = 0; i < n; i++) {
+        starts[c0 + i] = (uint16_t)st;
+        st = map_step(T, RT, srow + i * 8, sdom[i], st, status);
+    }
+}
+
 // compose8_kernel: the whole composition for maps of <= 8 entries, one
 // launch (dependent, PDL).  CTA b owns reporting chunks [b cpc, (b+1) cpc):
 // a warp per chunk folds the chunk's group leaves (chunk 0: L0 leaves,
@@ -1231,7 +1265,7 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
                                                         uint16_t *rep_rows, uint16_t *rep_doms, uint16_t *user_rows,
                                                         uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
                                                         uint16_t *cta_doms, uint32_t *ticket, DevStatus *status,
-                                                        uint16_t *dev_final, int staged) {
+                                                        uint16_t *dev_final, uint16_t *cta_start, int staged) {
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMin(&g_tree_t[10], gtimer());
 #endif
@@ -1320,11 +1354,20 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
             cdom[i] = __ldcg(cta_doms + i);
         }
         __syncthreads();
+        if (cta_start && threadIdx.x == 0) {
+            // true start of every CTA's first chunk: the prefix of Eq.SeqReduction over the CTA maps
+            uint32_t st = T.q0;
+            for (uint32_t i = 0; i < gridDim.x; i++) {
+                cta_start[i] = (uint16_t)st;
+                st = map_step(T, RT, crow + i * 8, cdom[i], st, status);
+            }
+        }
         acc = cta_tree_fold(T, RT, crow, cdom, trow, tdom, gridDim.x, status);
 #ifdef DFA_TREE_TIMING
         if (threadIdx.x == 0) atomicMax(&g_tree_t[22], gtimer() - tc2);
 #endif
     }
+    if (cta_start && gridDim.x == 1 && threadIdx.x == 0) cta_start[0] = (uint16_t)T.q0;
     if (threadIdx.x == 0) {
         const uint32_t fs = acc.v;
         if (fs == T.poison) atomicMax(&status->err, 5u);
@@ -1433,21 +1476,50 @@ __global__ void __launch_bounds__(256) lookahead_kernel(DevTables T, const uint8
 
 // ---------------------------------------------------------------------------
 // starts_kernel (optional output): true initial state of every reporting
-// chunk, the prefix of Eq.SeqReduction.  One thread, P dependent steps.
+// chunk, the prefix of Eq.SeqReduction.  One CTA: the rank table (when it
+// fits) and blocks of rows are staged in shared memory by all threads, one
+// thread walks the P - 1 dependent steps.
 // ---------------------------------------------------------------------------
-__global__ void starts_kernel(DevTables T, Plan p, const uint16_t *row0, const uint16_t *rows, const uint16_t *dom,
-                              uint16_t *starts, DevStatus *status) {
+__global__ void __launch_bounds__(512) starts_kernel(DevTables T, Plan p, const uint16_t *row0, const uint16_t *rows,
+                                                     const uint16_t *dom, uint16_t *starts, DevStatus *status,
+                                                     uint32_t rank_mode, uint32_t blk) {
+    extern __shared__ __align__(16) uint8_t ssm[];
+    // rank_mode: 0 = global rank, 1 = rank8 in smem, 2 = rank u16 in smem
+    const uint32_t nr = (T.nclass + 1) * T.nq;
+    const uint32_t rbytes = rank_mode == 1 ? ((nr + 15) & ~15u) : rank_mode == 2 ? ((nr * 2 + 15) & ~15u) : 0u;
+    if (rank_mode == 1) for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) ssm[i] = __ldg(T.rank8 + i);
+    if (rank_mode == 2)
+        for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) reinterpret_cast<uint16_t *>(ssm)[i] = __ldg(T.rank + i);
+    uint16_t *srow = reinterpret_cast<uint16_t *>(ssm + rbytes);
+    uint16_t *sdom = srow + (size_t)blk * T.rs;
     pdl_wait();
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    starts[0] = (uint16_t)T.q0;
-    if (p.P < 2) return;
-    uint32_t s = row0[0];
-    for (uint32_t k = 1; k < p.P; k++) {
-        starts[k] = (uint16_t)s;
-        if (test_bit(T.dead_bits, s)) continue;
-        const uint32_t r = T.rank[(uint64_t)dom[k] * T.nq + s];
-        if (r == kNone) { atomicMax(&status->err, 8u); return; }
-        s = rows[(uint64_t)(k - 1) * T.rs + r];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) {
+        starts[0] = (uint16_t)T.q0;
+        carry = p.P > 1 ? row0[0] : 0u;
+    }
+    for (uint32_t k0 = 1; k0 < p.P; k0 += blk) {
+        const uint32_t n = min(blk, p.P - k0);
+        __syncthreads();
+        const uint32_t q = T.rs / 8;  // uint4 per row
+        for (uint32_t i = threadIdx.x; i < n * q; i += blockDim.x)
+            reinterpret_cast<uint4 *>(srow)[i] = __ldcg(reinterpret_cast<const uint4 *>(rows + (uint64_t)(k0 - 1) * T.rs) + i);
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sdom[i] = __ldcg(dom + k0 + i);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t st = carry;
+            for (uint32_t i = 0; i < n; i++) {
+                starts[k0 + i] = (uint16_t)st;
+                if (T.has_dead && test_bit(T.dead_bits, st)) continue;
+                const uint64_t ri = (uint64_t)sdom[i] * T.nq + st;
+                uint32_t r = rank_mode == 1 ? ssm[ri] : rank_mode == 2 ? reinterpret_cast<const uint16_t *>(ssm)[ri]
+                                                                       : __ldg(T.rank + ri);
+                if (rank_mode == 1 && r == 0xFFu) r = kNone;
+                if (r == kNone) { atomicMax(&status->err, 8u); break; }
+                st = srow[(size_t)i * T.rs + r];
+            }
+            carry = st;
+        }
     }
 }
 
@@ -1529,6 +1601,11 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     e = cudaFuncSetAttribute((void *)fold_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)lookahead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute((void *)starts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute((void *)starts8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - kCompose8Static);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)compose8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              optin - kCompose8Static);
@@ -1633,12 +1710,17 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const uint16_t *leaf_dom, uint32_t L0,
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
-                            uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final, cudaStream_t s) {
+                            uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final,
+                            uint16_t *cta_start, uint16_t *starts, cudaStream_t s) {
     const int staged = rtab_staged(T);
     const uint32_t grid = (P + cpc - 1) / cpc;
-    return launch_pdl(compose8_kernel, dim3(grid), dim3(1024), staged ? rtab_bytes(T) : 0, s, T, leaves, leaf_dom, L0,
-                      L, P, cpc, rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows, cta_doms, ticket, st,
-                      dev_final, staged);
+    cudaError_t e = launch_pdl(compose8_kernel, dim3(grid), dim3(1024), staged ? rtab_bytes(T) : 0, s, T, leaves,
+                               leaf_dom, L0, L, P, cpc, rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows,
+                               cta_doms, ticket, st, dev_final, starts ? cta_start : nullptr, staged);
+    if (e != cudaSuccess || !starts) return e;
+    return launch_pdl(starts8_kernel, dim3(grid), dim3(256), staged ? rtab_bytes(T) : 0, s, T,
+                      (const uint16_t *)rep_rows, (const uint16_t *)rep_doms, P, cpc, (const uint16_t *)cta_start,
+                      starts, st, staged);
 }
 
 cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,
@@ -1662,7 +1744,19 @@ cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_b
 
 cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s) {
-    return launch_pdl(starts_kernel, dim3(1), dim3(32), 0, s, T, p, row0, rows, dom, starts, st);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const uint64_t nr = (uint64_t)(T.nclass + 1) * T.nq;
+    const uint64_t budget = (uint64_t)optin - 1024;
+    const uint64_t row_budget = 48 * 1024;
+    uint32_t mode = 0;
+    uint64_t rb = 0;
+    if (T.rank8 && ((nr + 15) & ~15ull) + row_budget <= budget) { mode = 1; rb = (nr + 15) & ~15ull; }
+    else if (((nr * 2 + 15) & ~15ull) + row_budget <= budget) { mode = 2; rb = (nr * 2 + 15) & ~15ull; }
+    const uint32_t blk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(1024, row_budget / (T.rs * 2 + 2)));
+    const size_t smem = rb + (size_t)blk * T.rs * 2 + (size_t)blk * 2 + 16;
+    return launch_pdl(starts_kernel, dim3(1), dim3(512), smem, s, T, p, row0, rows, dom, starts, st, mode, blk);
 }
 
 } // namespace dfa

@@ -137,7 +137,8 @@ cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64
 cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const uint16_t *leaf_dom, uint32_t L0,
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
-                            uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final, cudaStream_t s);
+                            uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final,
+                            uint16_t *cta_start, uint16_t *starts, cudaStream_t s);
 size_t fold_rows_fixed_bytes(const DevTables &T);
 cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uint16_t *doms, uint32_t P,
                              uint32_t per_cta, uint16_t *cta_rows, uint16_t *cta_doms, uint32_t *ticket,
