@@ -242,7 +242,10 @@ __device__ __forceinline__ void finish_slot(uint32_t slot, uint32_t state, uint3
         if (own[r] == slot) { fin[r] = state; own[r] = kDone; }
 }
 
-// Merge converged lanes, retire absorbing ones, compact.
+// Merge converged lanes, retire absorbing ones, compact.  B = the
+// warp's maximum live-lane count (compile time): the pair tests and the
+// compaction cost O(B^2), not O(kLanes^2).
+template <int B>
 __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_absorb, uint32_t bias,
                                            uint32_t (&st)[kLanes],
                                            uint32_t (&own)[kLanes], uint32_t &nlive, uint32_t (&fin)[kLanes]) {
@@ -252,15 +255,15 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_abso
         if (has_absorb && test_bit(absorb, st[0] - bias)) { finish_slot(0, st[0] - bias, own, fin); lm = 0; }
     } else {
 #pragma unroll
-        for (int l = 0; l < kLanes; l++)
+        for (int l = 0; l < B; l++)
             if (has_absorb && ((lm >> l) & 1u) && test_bit(absorb, st[l] - bias)) {
                 finish_slot(l, st[l] - bias, own, fin);
                 lm &= ~(1u << l);
             }
 #pragma unroll
-        for (int a = 0; a < kLanes - 1; a++)
+        for (int a = 0; a < B - 1; a++)
 #pragma unroll
-            for (int b = a + 1; b < kLanes; b++)
+            for (int b = a + 1; b < B; b++)
                 if (((lm >> a) & (lm >> b) & 1u) && st[a] == st[b]) {
                     lm &= ~(1u << b);
 #pragma unroll
@@ -269,17 +272,17 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_abso
                 }
     }
     if (lm == full) return;
-    uint32_t pc[kLanes];
+    uint32_t pc[B];
 #pragma unroll
-    for (int s = 0; s < kLanes; s++) pc[s] = __popc(lm & ((1u << s) - 1u));
+    for (int s = 0; s < B; s++) pc[s] = __popc(lm & ((1u << s) - 1u));
     // ns[t] = st[s] for the live slot s of rank t (branch-free masks keep
     // everything in registers: no dynamically indexed array)
-    uint32_t ns[kLanes];
+    uint32_t ns[B];
 #pragma unroll
-    for (int t = 0; t < kLanes; t++) {
+    for (int t = 0; t < B; t++) {
         uint32_t v = 0, any = 0;
 #pragma unroll
-        for (int s = t; s < kLanes; s++) {
+        for (int s = t; s < B; s++) {
             const uint32_t hit = 0u - (uint32_t)((((lm >> s) & 1u) != 0) & (pc[s] == (uint32_t)t));
             v |= st[s] & hit;
             any |= hit;
@@ -287,11 +290,29 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_abso
         ns[t] = v | (bias & ~any);  // unused slots keep a valid (encoded) state id
     }
 #pragma unroll
-    for (int t = 0; t < kLanes; t++) st[t] = ns[t];
+    for (int t = 0; t < B; t++) st[t] = ns[t];
 #pragma unroll
     for (int r = 0; r < kLanes; r++)
         if (own[r] != kDone) own[r] = __popc(lm & ((1u << own[r]) - 1u));
     nlive = __popc(lm);
+}
+
+// 16 bytes on B lanes, then (convergence on) the checkpoint; true = all lanes done.
+template <int B, int MODE>
+__device__ __forceinline__ bool block_step(const Tab<MODE> &tab, uint4 v, const uint32_t *absorb, bool has_absorb,
+                                           uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t &nlive,
+                                           uint32_t (&fin)[kLanes], int convergence, bool tick) {
+    block16<B, MODE>(tab, v, st);
+    if (!convergence) return false;
+    if (B > 1 && nlive > 1) {
+        checkpoint<B>(absorb, has_absorb, tab.bias, st, own, nlive, fin);
+        return nlive == 0;
+    }
+    if (has_absorb && tick && nlive == 1 && test_bit(absorb, st[0] - tab.bias)) {
+        finish_slot(0, st[0] - tab.bias, own, fin);  // the lane is done
+        return true;
+    }
+    return false;
 }
 
 template <int MODE>
@@ -323,26 +344,20 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
             for (int half = 0; half < 2; half++) {
                 const uint4 v = half ? cur.hi : cur.lo;
                 // the warp steps max(live lanes) lanes (exact, 1..8): lanes converge fast
+                const bool tick = half && (bi & 1);
+                bool done;
                 switch (__reduce_max_sync(__activemask(), nlive)) {
                 case 0:
-                case 1: block16<1>(tab, v, st); break;
-                case 2: block16<2>(tab, v, st); break;
-                case 3: block16<3>(tab, v, st); break;
-                case 4: block16<4>(tab, v, st); break;
-                case 5: block16<5>(tab, v, st); break;
-                case 6: block16<6>(tab, v, st); break;
-                case 7: block16<7>(tab, v, st); break;
-                default: block16<8>(tab, v, st); break;
+                case 1: done = block_step<1>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                case 2: done = block_step<2>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                case 3: done = block_step<3>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                case 4: done = block_step<4>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                case 5: done = block_step<5>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                case 6: done = block_step<6>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                case 7: done = block_step<7>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                default: done = block_step<8>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
                 }
-                if (convergence) {
-                    if (nlive > 1) {
-                        checkpoint(absorb, has_absorb, tab.bias, st, own, nlive, fin);
-                        if (nlive == 0) return;
-                    } else if (has_absorb && half && (bi & 1) && nlive == 1 && test_bit(absorb, st[0] - tab.bias)) {
-                        finish_slot(0, st[0] - tab.bias, own, fin);  // the lane is done
-                        return;
-                    }
-                }
+                if (done) return;
             }
             cur = nxt;
         }
