@@ -66,7 +66,7 @@ struct dfa_handle {
     // scratch
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
-    DevBuf cta_start;
+    DevBuf cta_start, leaf_rows2, leaf_dom2;
     int warp_compose = 1;
     std::vector<uint64_t> plan_key;
     // CUDA graph of a repeated dfa_chunk_maps call
@@ -328,7 +328,7 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         for (uint32_t k = 1; k < P; k++) minlen = std::min(minlen, hb[k + 1] - hb[k]);
         avg = (n - len0) / (P - 1);
     }
-    const bool warp_mode = h->T.rs == 8 && h->warp_compose;
+    const bool warp_mode = h->T.rs == 8 && h->warp_compose && !h->fold_in_tree;
     if (explicit_bounds) {
         sp.m0 = sp.m = 1;
         if (warp_mode) sp.g_log = 0;
@@ -438,15 +438,35 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         kernels++;
     }
     // composition: sub-chunk maps -> reporting maps -> final state
-    const uint32_t gl0 = grouped ? sp.g_log : 0;
-    const uint32_t L0 = m0 >> gl0, Lm = P > 1 ? (m >> gl0) : 1;
-    if (grouped && T.rs == 8 && !h->fold_in_tree && L0 >= 1 && L0 <= 256 && Lm >= 1 && Lm <= 256 &&
-        P <= (1u << 20)) {
-        // shuffle path: warp per reporting chunk over its leaves, then the fold
+    if (grouped) {
+        // rank-space leaves (maps of <= 8 entries): leaf_fold passes while the
+        // chunks hold more than 64 leaves, then compose8_kernel
+        uint32_t L0 = m0 >> sp.g_log, Lm = P > 1 ? (m >> sp.g_log) : 1;
+        if (P > (1u << 20)) return DFA_ERR_INTERNAL;
         CK(h->lvlA.ensure((uint64_t)P * T.rs * 2));
         CK(h->domA.ensure((uint64_t)P * 2));
-        const uint32_t per_warp = std::max<uint32_t>(1, (P + 32u * h->sms - 1) / (32u * h->sms));
-        const uint32_t cpc = 32 * std::min<uint32_t>(per_warp, 32);  // one wave of 1024-thread CTAs
+        uint16_t *lrows = h->leaf_rows.as<uint16_t>(), *ldom = h->leaf_dom.as<uint16_t>();
+        prof_begin(h, s, 2);
+        if (L0 > 64 || Lm > 64) {
+            const uint64_t n1 = (uint64_t)(L0 + 31) / 32 + (uint64_t)(P - 1) * ((Lm + 31) / 32) + 1;
+            CK(h->leaf_rows2.ensure(n1 * T.rs * 2));
+            CK(h->leaf_dom2.ensure(n1 * 2));
+            uint16_t *orows = h->leaf_rows2.as<uint16_t>(), *odom = h->leaf_dom2.as<uint16_t>();
+            while (L0 > 64 || Lm > 64) {
+                CK(launch_leaf_fold(lrows, ldom, L0, Lm, P, orows, odom, h->sms, s));
+                kernels++;
+                L0 = (L0 + 31) / 32;
+                Lm = (Lm + 31) / 32;
+                std::swap(lrows, orows);
+                std::swap(ldom, odom);
+            }
+        }
+        // chunks per compose8 CTA: 4 per warp, spread over the SMs (one round when
+        // P <= 4 * 32 * SMs), at least P / 1024 (the last CTA folds <= 1024 maps)
+        uint32_t cpc = std::max<uint32_t>(4, (P + h->sms - 1) / h->sms);
+        cpc = (cpc + 3) / 4 * 4;
+        if (cpc > 128) cpc = (cpc + 127) / 128 * 128;
+        cpc = std::min<uint32_t>(1024, std::max<uint32_t>(cpc, (P + 1023) / 1024));
         const uint32_t g2 = (P + cpc - 1) / cpc;
         CK(h->fold_rows.ensure((uint64_t)g2 * T.rs * 2 + 256));
         CK(h->fold_doms.ensure((uint64_t)g2 * 2 + 256));
@@ -456,8 +476,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
             CK(cudaMemsetAsync(h->ticket.p, 0, 256, s));
         }
         uint16_t *rep_rows = h->lvlA.as<uint16_t>(), *rep_doms = h->domA.as<uint16_t>();
-        prof_begin(h, s, 2);
-        CK(launch_compose8(T, h->leaf_rows.as<uint16_t>(), h->leaf_dom.as<uint16_t>(), L0, Lm, P, cpc, rep_rows,
+        CK(launch_compose8(T, lrows, ldom, L0, Lm, P, cpc, rep_rows,
                            rep_doms, o.user_maps, o.user_row0, o.chunk0_end, h->fold_rows.as<uint16_t>(),
                            h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(), h->status.as<DevStatus>(), o.final2,
                            h->cta_start.as<uint16_t>(), o.starts, s));
@@ -710,7 +729,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->last_stream) cudaStreamSynchronize(h->last_stream);
         for (DevBuf *b : {&h->tables, &h->status, &h->sfin, &h->dom_of, &h->surv, &h->surv_n, &h->surv_pos,
                           &h->amap, &h->lvlA, &h->domA, &h->counters, &h->bounds, &h->input, &h->fold_rows,
-                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds, &h->cta_start})
+                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds, &h->cta_start, &h->leaf_rows2, &h->leaf_dom2})
             b->release();
         h->h_status.release();
         h->h_bounds.release();

@@ -22,6 +22,15 @@ namespace {
 constexpr uint32_t kDone = 0xFFu;
 constexpr uint32_t kNoGroup = 0xFFFFFFFFu;
 
+#ifdef DFA_TREE_TIMING
+__device__ unsigned long long g_tree_t[32];  // debug phase timestamps (tools/*_timing.py)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // Programmatic dependent launch (sm_90+): a kernel launched with
 // launch_pdl may start while its predecessor drains; it stages what does not
 // depend on it, then waits here for the predecessor's completion and memory.
@@ -375,30 +384,31 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
     }
 }
 
+// Rank-space maps (maps of <= 8 entries, the grouped path): an entry is either
+// a rank code kRank + r = "the r-th state of the NEXT sub-chunk's domain" or
+// an absolute state (error states, which no later byte leaves, and
+// the final states of the input's last sub-chunk); kNone pads.  Composing
+// L_j o L_i is then a pure gather, L_i[x] <- L_j[r] (Eq.MapReduction), with no
+// table lookup: the rank was taken once, where the state was produced.
+constexpr uint32_t kRank = 0xFF00u;
+__device__ __forceinline__ bool is_rank(uint32_t v) { return v - kRank < (uint32_t)kLanes; }
+
 // Warp-level composition of g = 2^g_log consecutive sub-chunk maps (aligned
 // groups of lanes, one sub-chunk each): in round r, lane t (t % 2^(r+1) == 0)
-// absorbs the map of lane t + 2^r, L_t <- L_{t+2^r} o L_t (Eq.MapReduction),
-// with the partner's map taken by shuffles.  Maps are <= 8 entries in
-// registers; entries >= u are ignored.
-__device__ __forceinline__ void warp_compose(const DevTables &T, uint32_t mask, uint32_t g_log, uint32_t (&fin)[kLanes],
-                                             uint32_t &dom, uint32_t u, DevStatus *status) {
+// absorbs the map of lane t + 2^r, L_t <- L_{t+2^r} o L_t, with the partner's
+// map taken by shuffles.
+__device__ __forceinline__ void warp_compose(uint32_t mask, uint32_t g_log, uint32_t (&fin)[kLanes]) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t r = 0; r < g_log; r++) {
         const uint32_t step = 1u << r;
         uint32_t pm[kLanes];
 #pragma unroll
         for (int e = 0; e < kLanes; e++) pm[e] = __shfl_down_sync(mask, fin[e], step);
-        const uint32_t pd = __shfl_down_sync(mask, dom, step);
         if ((lane & ((2u << r) - 1)) != 0) continue;
 #pragma unroll
         for (int j = 0; j < kLanes; j++) {
-            if ((uint32_t)j >= u) continue;
-            const uint32_t s = fin[j];
-            if (T.has_dead && test_bit(T.dead_bits, s)) continue;
-            uint32_t rr;
-            if (T.rank8) { rr = __ldg(T.rank8 + (uint64_t)pd * T.nq + s); rr = rr == 0xFFu ? kNone : rr; }
-            else rr = __ldg(T.rank + (uint64_t)pd * T.nq + s);
-            if (rr == kNone) { atomicMax(&status->err, 8u); rr = 0; }
+            const uint32_t rr = fin[j] - kRank;
+            if (rr >= (uint32_t)kLanes) continue;
             uint32_t v = 0;
 #pragma unroll
             for (int e = 0; e < kLanes; e++) v |= pm[e] & (0u - (uint32_t)(rr == (uint32_t)e));
@@ -418,9 +428,15 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
                                                     uint16_t *__restrict__ leaf_rows, uint16_t *__restrict__ leaf_dom,
                                                     DevStatus *status) {
     pdl_trigger();  // one wave: the composition kernels may take SMs as CTAs retire
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMin(&g_tree_t[25], gtimer());
+#endif
     extern __shared__ uint4 smem4[];
     uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
     __syncthreads();
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[26], gtimer());
+#endif
     Tab<MODE> tab;
     tab.init(T, tsm);
     const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + T.image_words;
@@ -453,14 +469,36 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
 #pragma unroll
             for (int l = 0; l < kLanes; l++) fin[l] = kNone;
             run_lanes<MODE>(tab, absorb, T.has_absorb != 0, in, pos, end, st, own, nl, convergence, fin);
+#ifdef DFA_TREE_TIMING
+            if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[27], gtimer());
+#endif
             if (g_log != kNoGroup) {
                 // maps of <= 8 entries: compose aligned groups of 2^g_log sub-chunks in
                 // the warp and write one leaf per group (no per-sub-chunk map in HBM)
                 const uint64_t wbase = i & ~31ull;
                 const uint32_t mask = wbase + 32 <= p.NS ? 0xffffffffu : ((1u << (uint32_t)(p.NS - wbase)) - 1u);
+                // rank space: final states as ranks in the next sub-chunk's domain
+                // I_sigma, sigma = this sub-chunk's last byte (absolute for error
+                // states and for the input's last sub-chunk)
+                if (i + 1 < p.NS) {
+                    const uint32_t nd = T.byte_class[__ldg(in + end - 1)];
+                    const uint8_t *rk = T.rank8 + (uint64_t)nd * T.nq;
+                    uint32_t rr[kLanes];
+#pragma unroll
+                    for (int l = 0; l < kLanes; l++) rr[l] = (uint32_t)l < u ? __ldg(rk + fin[l]) : 0xFFu;
+#pragma unroll
+                    for (int l = 0; l < kLanes; l++) {
+                        if ((uint32_t)l >= u) continue;
+                        if (rr[l] < (uint32_t)kLanes) fin[l] = kRank + rr[l];
+                        else if (!(T.has_dead && test_bit(T.dead_bits, fin[l]))) atomicMax(&status->err, 8u);
+                    }
+                }
                 __syncwarp(mask);
-                uint32_t d = dom;
-                warp_compose(T, mask, g_log, fin, d, u, status);
+                const uint32_t d = dom;
+                warp_compose(mask, g_log, fin);
+#ifdef DFA_TREE_TIMING
+                if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[28], gtimer());
+#endif
                 if (((threadIdx.x & 31) & ((1u << g_log) - 1)) == 0) {
                     const uint64_t leaf = i >> g_log;
                     uint4 v;
@@ -503,6 +541,9 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
             }
         }
     }
+#ifdef DFA_TREE_TIMING
+    if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[29], gtimer());
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -653,14 +694,6 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
 // Counters are never reset: a node is complete when its count reaches a
 // multiple of its child count (calls on a stream do not overlap).
 // ---------------------------------------------------------------------------
-#ifdef DFA_TREE_TIMING
-__device__ unsigned long long g_tree_t[32];  // [0] kernel start (min), [L] level L done (max)
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#endif
 
 __device__ __forceinline__ void group_range(const TreeLevel &lv, uint32_t g, uint32_t &st, uint32_t &en) {
     if (g < lv.gf) { st = g * lv.G; en = min(lv.f, st + lv.G); return; }
@@ -1053,127 +1086,58 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
 }
 
 // ---------------------------------------------------------------------------
-// Shuffle composition of maps with <= 8 entries (rows of stride 8): the
-// reporting-chunk maps from the group leaves (seg_fold_kernel) and the fold of
-// the reporting maps into the final state (fold2_kernel).  Entry per lane: a
-// warp holds 4 maps, lane 8g + j = entry j of map g, so composing two maps is
-// one rank lookup and one shuffle per lane (Eq.MapReduction).
+// Composition of rank-space maps with <= 8 entries (the grouped path; see
+// kRank): the reporting-chunk maps from the group leaves, the fold of the
+// reporting maps into the final state, and the chunk starts.  Entry per lane:
+// a warp holds 4 maps, lane 8g + j = entry j of map g, so composing two maps
+// is one shuffle per lane (Eq.MapReduction) -- no table lookups at all.
 // ---------------------------------------------------------------------------
-
-// rank8 / Z / |I_sigma| / xlat / |I_sigma| (user) staged in shared memory
-// when they fit, else the global copies.
-constexpr int kCompose8Static = 28 * 1024;  // compose8_kernel: crow/cdom/trow/tdom (~23 KB) + reserve
-
-struct RTab {
-    const uint8_t *rank8;
-    const uint32_t *dead;
-    const uint16_t *dsz;
-    const uint16_t *xlat;
-    const uint16_t *dus;
-};
-
-__host__ __device__ __forceinline__ uint32_t rtab_rank_bytes(const DevTables &T) {
-    return ((T.nclass + 1) * T.nq + 15) & ~15u;
-}
-__host__ __device__ __forceinline__ uint32_t rtab_dead_bytes(const DevTables &T) {
-    return ((T.nq + 31) / 32 * 4 + 15) & ~15u;
-}
-__host__ __device__ __forceinline__ uint32_t rtab_dsz_bytes(const DevTables &T) {
-    return ((T.nclass + 1) * 2 + 15) & ~15u;
-}
-__host__ __device__ __forceinline__ uint32_t rtab_xlat_bytes(const DevTables &T) {
-    return (T.nclass * T.imax_user * 2 + 15) & ~15u;
-}
-__host__ __device__ __forceinline__ uint32_t rtab_bytes(const DevTables &T) {
-    return rtab_rank_bytes(T) + rtab_dead_bytes(T) + 2 * rtab_dsz_bytes(T) + rtab_xlat_bytes(T);
-}
-
-__device__ __forceinline__ RTab stage_rtab(const DevTables &T, uint8_t *sm, bool staged) {
-    if (!staged) return RTab{T.rank8, T.dead_bits, T.dom_size, T.xlat, T.dom_user_size};
-    const uint32_t rb = rtab_rank_bytes(T), db = rtab_dead_bytes(T), zb = rtab_dsz_bytes(T);
-    const uint32_t nr = (T.nclass + 1) * T.nq;
-    for (uint32_t i = threadIdx.x; i < rb / 16; i += blockDim.x) {
-        if (i * 16 + 16 <= nr) reinterpret_cast<uint4 *>(sm)[i] = __ldg(reinterpret_cast<const uint4 *>(T.rank8) + i);
-        else for (uint32_t k = i * 16; k < i * 16 + 16; k++) sm[k] = k < nr ? __ldg(T.rank8 + k) : 0xFFu;
-    }
-    uint32_t *dead = reinterpret_cast<uint32_t *>(sm + rb);
-    for (uint32_t i = threadIdx.x; i < db / 4; i += blockDim.x)
-        dead[i] = i < (T.nq + 31) / 32 && T.has_dead ? __ldg(T.dead_bits + i) : 0u;
-    uint16_t *dsz = reinterpret_cast<uint16_t *>(sm + rb + db);
-    for (uint32_t i = threadIdx.x; i <= T.nclass; i += blockDim.x) dsz[i] = __ldg(T.dom_size + i);
-    uint16_t *dus = reinterpret_cast<uint16_t *>(sm + rb + db + zb);
-    for (uint32_t i = threadIdx.x; i < T.nclass; i += blockDim.x) dus[i] = __ldg(T.dom_user_size + i);
-    uint16_t *xl = reinterpret_cast<uint16_t *>(sm + rb + db + 2 * zb);
-    for (uint32_t i = threadIdx.x; i < T.nclass * T.imax_user; i += blockDim.x) xl[i] = __ldg(T.xlat + i);
-    __syncthreads();
-    return RTab{sm, dead, dsz, xl, dus};
-}
-
-// One lane's view of a map: entry v (j = lane & 7), the map's domain and size
-// (replicated over its 8 lanes), ok = the map exists (ragged batches).
+// One lane's view of a map: entry v (j = lane & 7), the map's domain (its
+// first sub-chunk's, replicated over the 8 lanes), ok = the map exists.
 struct LMap {
-    uint32_t v, dom, u, ok;
+    uint32_t v, dom, ok;
 };
 
-__device__ __forceinline__ LMap lmap_load(const RTab &R, const uint16_t *rows, const uint16_t *doms, uint64_t r,
-                                          bool ok) {
+__device__ __forceinline__ LMap lmap_load(const uint16_t *rows, const uint16_t *doms, uint64_t r, bool ok) {
     LMap m;
     const uint32_t j = threadIdx.x & 7;
     m.ok = ok;
     m.v = ok ? __ldcg(rows + r * 8 + j) : (uint32_t)kNone;
     m.dom = ok ? __ldcg(doms + r) : 0u;
-    m.u = ok ? R.dsz[m.dom] : 0u;
     return m;
 }
 
-// Entry j of map a (domain a.dom) continued through map b: the index to read
-// in b, or j when a's entry stays (padding, error state P:450-454).
-__device__ __forceinline__ bool lmap_step(const DevTables &T, const RTab &R, uint32_t v, uint32_t u, uint32_t j,
-                                          uint32_t bdom, uint32_t &r, DevStatus *status) {
-    if (j >= u) return false;
-    if (T.has_dead && test_bit(R.dead, v)) return false;
-    r = R.rank8[bdom * T.nq + v];
-    if (r >= (uint32_t)kLanes) { atomicMax(&status->err, 8u); r = 0; }
-    return true;
-}
-
 // Tree step over the 4 maps of a warp: group g (g % 2gs == 0) <- group g+gs o g.
-__device__ __forceinline__ void lmap_merge(const DevTables &T, const RTab &R, LMap &m, uint32_t gs, DevStatus *status) {
-    const uint32_t lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+__device__ __forceinline__ void lmap_merge(LMap &m, uint32_t gs) {
+    const uint32_t lane = threadIdx.x & 31, g = lane >> 3;
     const uint32_t sb = ((g + gs) & 3) * 8;
     const uint32_t bdom = __shfl_sync(0xffffffffu, m.dom, sb);
-    const uint32_t bu = __shfl_sync(0xffffffffu, m.u, sb);
     const uint32_t bok = __shfl_sync(0xffffffffu, m.ok, sb);
     const bool lead = (g & (2 * gs - 1)) == 0 && bok;
-    uint32_t r = j;
-    bool use = false;
-    if (lead) use = m.ok ? lmap_step(T, R, m.v, m.u, j, bdom, r, status) : true;
-    const uint32_t nv = __shfl_sync(0xffffffffu, m.v, sb + r);
-    if (use) m.v = nv;
-    if (lead && !m.ok) { m.dom = bdom; m.u = bu; m.ok = 1; }
+    const uint32_t rr = m.v - kRank;
+    const bool take = lead && (!m.ok || rr < (uint32_t)kLanes);
+    const uint32_t nv = __shfl_sync(0xffffffffu, m.v, sb + (m.ok ? (rr & 7u) : (lane & 7u)));
+    if (take) m.v = nv;
+    if (lead && !m.ok) { m.dom = bdom; m.ok = 1; }
 }
 
 // acc (group 0) <- b (group 0) o acc
-__device__ __forceinline__ void lmap_then(const DevTables &T, const RTab &R, LMap &acc, const LMap &b,
-                                          DevStatus *status) {
-    const uint32_t j = threadIdx.x & 7;
+__device__ __forceinline__ void lmap_then(LMap &acc, const LMap &b) {
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t bdom = __shfl_sync(0xffffffffu, b.dom, 0);
-    const uint32_t bu = __shfl_sync(0xffffffffu, b.u, 0);
-    const uint32_t bok = __shfl_sync(0xffffffffu, b.ok, 0) && (threadIdx.x & 31) < 8;
-    uint32_t r = j;
-    bool use = false;
-    if (bok) use = acc.ok ? lmap_step(T, R, acc.v, acc.u, j, bdom, r, status) : true;
-    const uint32_t nv = __shfl_sync(0xffffffffu, b.v, r);
-    if (use) acc.v = nv;
-    if (bok && !acc.ok) { acc.dom = bdom; acc.u = bu; acc.ok = 1; }
+    const uint32_t bok = __shfl_sync(0xffffffffu, b.ok, 0) && lane < 8;
+    const uint32_t rr = acc.v - kRank;
+    const bool take = bok && (!acc.ok || rr < (uint32_t)kLanes);
+    const uint32_t nv = __shfl_sync(0xffffffffu, b.v, acc.ok ? (rr & 7u) : (lane & 7u));
+    if (take) acc.v = nv;
+    if (bok && !acc.ok) { acc.dom = bdom; acc.ok = 1; }
 }
 
 // acc (group 0) <- maps [a, b) of (rows, doms) o acc, in order; the loads of
 // 16 maps are issued before their compositions.
 template <bool GLOBAL>
-__device__ __forceinline__ void warp_fold_range(const DevTables &T, const RTab &R, const uint16_t *rows,
-                                                const uint16_t *doms, uint32_t a, uint32_t b, LMap &acc,
-                                                DevStatus *status) {
+__device__ __forceinline__ void warp_fold_range(const uint16_t *rows, const uint16_t *doms, uint32_t a, uint32_t b,
+                                                LMap &acc) {
     const uint32_t g = (threadIdx.x & 31) >> 3, j = threadIdx.x & 7;
 #pragma unroll 1
     for (uint32_t base = a; base < b; base += 16) {
@@ -1181,34 +1145,33 @@ __device__ __forceinline__ void warp_fold_range(const DevTables &T, const RTab &
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             const uint32_t r = base + 4 * q + g;
-            if (GLOBAL) m[q] = lmap_load(R, rows, doms, r, r < b);
+            if (GLOBAL) m[q] = lmap_load(rows, doms, r, r < b);
             else {
                 m[q].ok = r < b;
                 m[q].v = m[q].ok ? rows[r * 8 + j] : (uint32_t)kNone;
                 m[q].dom = m[q].ok ? doms[r] : 0u;
-                m[q].u = m[q].ok ? R.dsz[m[q].dom] : 0u;
             }
         }
         // the 4 batches side by side: within-batch tree, then pairs, then acc
 #pragma unroll
-        for (int q = 0; q < 4; q++) lmap_merge(T, R, m[q], 1, status);
+        for (int q = 0; q < 4; q++) lmap_merge(m[q], 1);
 #pragma unroll
-        for (int q = 0; q < 4; q++) lmap_merge(T, R, m[q], 2, status);
-        lmap_then(T, R, m[0], m[1], status);
-        lmap_then(T, R, m[2], m[3], status);
-        lmap_then(T, R, m[0], m[2], status);
-        lmap_then(T, R, acc, m[0], status);
+        for (int q = 0; q < 4; q++) lmap_merge(m[q], 2);
+        lmap_then(m[0], m[1]);
+        lmap_then(m[2], m[3]);
+        lmap_then(m[0], m[2]);
+        lmap_then(acc, m[0]);
     }
 }
 
 // Tree fold of the n >= 1 maps (rows, doms) in shared memory: each level,
 // warp w folds maps 4w..4w+3 into slot w of the other buffer (trows/tdoms,
 // >= ceil(n/4) slots; the two alternate).  Result in warp 0, lanes 0..7.
-__device__ __forceinline__ LMap cta_tree_fold(const DevTables &T, const RTab &R, uint16_t *rows, uint16_t *doms,
-                                              uint16_t *trows, uint16_t *tdoms, uint32_t n, DevStatus *status) {
+__device__ __forceinline__ LMap cta_tree_fold(uint16_t *rows, uint16_t *doms, uint16_t *trows, uint16_t *tdoms,
+                                              uint32_t n) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t g = lane >> 3, j = lane & 7;
-    LMap m{kNone, 0, 0, 0};
+    LMap m{kNone, 0, 0};
     for (;;) {
         const uint32_t groups = (n + 3) / 4;
 #pragma unroll 1
@@ -1217,11 +1180,10 @@ __device__ __forceinline__ LMap cta_tree_fold(const DevTables &T, const RTab &R,
             m.ok = r < n;
             m.v = m.ok ? rows[r * 8 + j] : (uint32_t)kNone;
             m.dom = m.ok ? doms[r] : 0u;
-            m.u = m.ok ? R.dsz[m.dom] : 0u;
-            lmap_merge(T, R, m, 1, status);
-            lmap_merge(T, R, m, 2, status);
+            lmap_merge(m, 1);
+            lmap_merge(m, 2);
             if (groups > 1) {
-                if (lane < 8) trows[w * 8 + j] = (uint16_t)(j < m.u ? m.v : kNone);
+                if (lane < 8) trows[w * 8 + j] = (uint16_t)m.v;
                 if (lane == 0) tdoms[w] = (uint16_t)m.dom;
             }
         }
@@ -1234,23 +1196,79 @@ __device__ __forceinline__ LMap cta_tree_fold(const DevTables &T, const RTab &R,
     return m;
 }
 
-// One state through one map (row of <= 8 entries over domain dom): error
-// states stay, else the entry at the state's rank.
-__device__ __forceinline__ uint32_t map_step(const DevTables &T, const RTab &R, const uint16_t *row, uint32_t dom,
-                                             uint32_t st, DevStatus *status) {
-    if (T.has_dead && test_bit(R.dead, st)) return st;
-    const uint32_t r = R.rank8[dom * T.nq + st];
-    if (r >= (uint32_t)kLanes) { atomicMax(&status->err, 8u); return st; }
-    return row[r];
+// A rank-space entry as a state: rank codes index the next map's domain nd.
+__device__ __forceinline__ uint32_t decode_entry(const DevTables &T, uint32_t v, uint32_t nd) {
+    return is_rank(v) ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.imax + (v - kRank)) : v;
+}
+
+// leaf_fold_kernel: one level of leaf reduction for long chunks: the leaves of
+// every chunk (chunk 0: L0, others L) in aligned runs of 32, each run folded
+// by one warp (lane = leaf, shuffle butterfly) into one leaf of the output
+// (chunk 0: ceil(L0/32), others ceil(L/32)).  Launched dependent.
+__global__ void __launch_bounds__(256) leaf_fold_kernel(const uint16_t *in_rows, const uint16_t *in_dom, uint32_t L0,
+                                                        uint32_t L, uint32_t P, uint16_t *out_rows,
+                                                        uint16_t *out_dom) {
+    pdl_trigger();
+    pdl_wait();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t L0n = (L0 + 31) / 32, Ln = (L + 31) / 32;
+    const uint64_t total = (uint64_t)L0n + (uint64_t)(P - 1) * Ln;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t o = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); o < total; o += nwarps) {
+        uint64_t a, e;
+        if (o < L0n) { a = o * 32; e = L0; }
+        else {
+            const uint64_t k = 1 + (o - L0n) / Ln, idx = (o - L0n) % Ln;
+            const uint64_t ck = (uint64_t)L0 + (k - 1) * L;
+            a = ck + idx * 32;
+            e = ck + L;
+        }
+        const uint64_t leaf = a + lane;
+        const bool valid = leaf < e;
+        uint32_t fin[kLanes], dom = 0;
+        if (valid) {
+            const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(in_rows) + leaf);
+            fin[0] = v.x & 0xFFFFu; fin[1] = v.x >> 16; fin[2] = v.y & 0xFFFFu; fin[3] = v.y >> 16;
+            fin[4] = v.z & 0xFFFFu; fin[5] = v.z >> 16; fin[6] = v.w & 0xFFFFu; fin[7] = v.w >> 16;
+            dom = __ldcg(in_dom + leaf);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kLanes; q++) fin[q] = kNone;
+        }
+#pragma unroll
+        for (uint32_t step = 1; step < 32; step *= 2) {
+            uint32_t pm[kLanes];
+#pragma unroll
+            for (int q = 0; q < kLanes; q++) pm[q] = __shfl_down_sync(0xffffffffu, fin[q], step);
+            const bool pv = __shfl_down_sync(0xffffffffu, valid, step);
+            if ((lane & (2 * step - 1)) != 0 || !pv || lane + step >= 32) continue;
+#pragma unroll
+            for (int q = 0; q < kLanes; q++) {
+                const uint32_t rr = fin[q] - kRank;
+                if (rr >= (uint32_t)kLanes) continue;
+                uint32_t v = 0;
+#pragma unroll
+                for (int t = 0; t < kLanes; t++) v |= pm[t] & (0u - (uint32_t)(rr == (uint32_t)t));
+                fin[q] = v;
+            }
+        }
+        if (lane == 0) {
+            uint4 v;
+            v.x = (fin[0] & 0xFFFFu) | (fin[1] << 16);
+            v.y = (fin[2] & 0xFFFFu) | (fin[3] << 16);
+            v.z = (fin[4] & 0xFFFFu) | (fin[5] << 16);
+            v.w = (fin[6] & 0xFFFFu) | (fin[7] << 16);
+            reinterpret_cast<uint4 *>(out_rows)[o] = v;
+            out_dom[o] = (uint16_t)dom;
+        }
+    }
 }
 
 // starts8_kernel: true start of every reporting chunk (optional output): CTA b
-// walks its compose8 chunks from cta_start[b].  Launched dependent.
+// walks its compose8 chunks from the rank code cta_start[b].  Launched dependent.
 __global__ void __launch_bounds__(256) starts8_kernel(DevTables T, const uint16_t *rep_rows, const uint16_t *rep_doms,
                                                      uint32_t P, uint32_t cpc, const uint16_t *cta_start,
-                                                     uint16_t *starts, DevStatus *status, int staged) {
-    extern __shared__ __align__(16) uint8_t rsm[];
-    const RTab RT = stage_rtab(T, rsm, staged);
+                                                     uint16_t *starts) {
     __shared__ __align__(16) uint16_t srow[1024 * 8];
     __shared__ uint16_t sdom[1024];
     pdl_wait();
@@ -1261,31 +1279,28 @@ __global__ void __launch_bounds__(256) starts8_kernel(DevTables T, const uint16_
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    uint32_t st = __ldcg(cta_start + blockIdx.x);
+    uint32_t code = __ldcg(cta_start + blockIdx.x);
     for (uint32_t i = 0; i < n; i++) {
-        starts[c0 + i] = (uint16_t)st;
-        st = map_step(T, RT, srow + i * 8, sdom[i], st, status);
+        starts[c0 + i] = (uint16_t)decode_entry(T, code, sdom[i]);
+        if (is_rank(code)) code = srow[i * 8 + (code - kRank)];
     }
 }
 
-// compose8_kernel: the whole composition for maps of <= 8 entries, one
-// launch (dependent, PDL).  CTA b owns reporting chunks [b cpc, (b+1) cpc):
-// a warp per chunk folds the chunk's group leaves (chunk 0: L0 leaves,
-// others L) into the reporting map (internal row, API row in the user's
-// order, chunk 0's user row, e0); the CTA folds its chunk maps
-// (Eq.SeqReduction), the last CTA (acq_rel ticket) folds the CTA maps and
-// applies Alg.seqmatch lines 4-6.
+// compose8_kernel: the whole composition for rank-space maps, one launch
+// (dependent, PDL).  CTA b owns reporting chunks [b cpc, (b+1) cpc): a warp per
+// chunk folds the chunk's group leaves (chunk 0: L0 leaves, others L) into the
+// reporting map (internal row, API row in the user's order with states, chunk
+// 0's user row, e0); the CTA folds its chunk maps (Eq.SeqReduction), the last
+// CTA (acq_rel ticket) folds the CTA maps and applies Alg.seqmatch lines 4-6.
 __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint16_t *leaves, const uint16_t *leaf_dom,
                                                         uint32_t L0, uint32_t L, uint32_t P, uint32_t cpc,
                                                         uint16_t *rep_rows, uint16_t *rep_doms, uint16_t *user_rows,
                                                         uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
                                                         uint16_t *cta_doms, uint32_t *ticket, DevStatus *status,
-                                                        uint16_t *dev_final, uint16_t *cta_start, int staged) {
+                                                        uint16_t *dev_final, uint16_t *cta_start) {
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMin(&g_tree_t[10], gtimer());
 #endif
-    extern __shared__ __align__(16) uint8_t rsm[];
-    const RTab RT = stage_rtab(T, rsm, staged);
     pdl_trigger();
     pdl_wait();
 #ifdef DFA_TREE_TIMING
@@ -1297,41 +1312,67 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
     __shared__ uint32_t last;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5, j = lane & 7;
     const uint32_t c0 = blockIdx.x * cpc, c1 = min(P, c0 + cpc);
+    const uint32_t g = lane >> 3, gb = lane & ~7u;
+    // chunk phase: each warp takes 4 chunks at a time, one per 8-lane group,
+    // and folds the chunk's leaves in order (group-local shuffles)
 #pragma unroll 1
-    for (uint32_t k = c0 + warp; k < c1; k += nw) {
+    for (uint32_t kb = c0 + warp * 4; kb < c1; kb += nw * 4) {
+        const uint32_t k = kb + g;
+        const bool has = k < c1;
         const uint32_t a = k == 0 ? 0u : L0 + (k - 1) * L, b = L0 + k * L;
-        LMap acc{kNone, 0, 0, 0};
-        warp_fold_range<true>(T, RT, leaves, leaf_dom, a, b, acc, status);
-        const uint32_t d0 = acc.dom;
-        const uint16_t ev = (uint16_t)(j < acc.u ? acc.v : kNone);
-        if (lane < 8) {
-            rep_rows[(uint64_t)k * 8 + j] = ev;
-            crow[(k - c0) * 8 + j] = ev;
-        }
-        if (lane == 0) {
-            rep_doms[k] = (uint16_t)d0;
-            cdom[k - c0] = (uint16_t)d0;
-        }
-        if (e0 && k == 0 && lane == 0) e0[0] = (uint16_t)acc.v;
-        uint16_t *urow = nullptr;
-        uint32_t du = 0;
-        if (user_rows && k > 0) {
-            urow = user_rows + (uint64_t)(k - 1) * T.imax_user;
-            du = d0 < T.nclass ? RT.dus[d0] : 0u;
-        } else if (user_row0 && k == 0) {
-            urow = user_row0;
-            du = d0 < T.nclass ? RT.dus[d0] : (d0 == T.start_dom ? 1u : 0u);
-        }
-        if (urow) {
+        const uint32_t nk = has ? b - a : 0u;
+        // the next chunk's domain (its first leaf's) decodes this chunk's rank codes
+        const uint32_t nd = has && k + 1 < P ? (uint32_t)__ldcg(leaf_dom + b) : 0u;
+        const uint32_t d0 = has ? (uint32_t)__ldcg(leaf_dom + a) : 0u;
+        const uint32_t nmax = __reduce_max_sync(0xffffffffu, nk);
+        uint32_t av = kNone, aok = 0;
+        uint32_t dl = kNone, xl = 0, du = 0;
 #pragma unroll 1
-            for (uint32_t j0 = 0; j0 < T.imax_user; j0 += 32) {
-                const uint32_t ju = j0 + lane;
-                uint32_t ji = 0;
-                if (ju < du) ji = d0 < T.nclass ? RT.xlat[d0 * T.imax_user + ju] : ju;
-                const uint32_t v = __shfl_sync(0xffffffffu, acc.v, ji & 7);
-                if (ju < T.imax_user) urow[ju] = (uint16_t)(ju < du ? v : kNone);
+        for (uint32_t t0 = 0; t0 < nmax; t0 += 16) {
+            uint32_t lv[16];
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+                lv[q] = t0 + q < nk ? (uint32_t)__ldcg(leaves + (uint64_t)(a + t0 + q) * 8 + j) : kNone;
+            if (t0 == 0 && has) {
+                // decode and user-order rows, loaded while the leaves are in flight
+                if (k + 1 < P) dl = __ldg(T.dom_list + (uint64_t)nd * T.imax + j);
+                if (d0 < T.nclass) {
+                    du = T.dom_user_size[d0];
+                    if (j < T.imax_user) xl = T.xlat[(uint64_t)d0 * T.imax_user + j];
+                } else {
+                    du = d0 == T.start_dom ? 1u : 0u;
+                    xl = j;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+                const bool bok = t0 + q < nk;
+                const uint32_t rr = av - kRank;
+                const bool take = bok && (!aok || rr < (uint32_t)kLanes);
+                const uint32_t nv = __shfl_sync(0xffffffffu, lv[q], gb + (aok ? (rr & 7u) : j));
+                if (take) av = nv;
+                aok |= bok;
             }
         }
+        if (has) {
+            rep_rows[(uint64_t)k * 8 + j] = (uint16_t)av;
+            crow[(k - c0) * 8 + j] = (uint16_t)av;
+            if (j == 0) {
+                rep_doms[k] = (uint16_t)d0;
+                cdom[k - c0] = (uint16_t)d0;
+            }
+        }
+        // the map with states: rank codes through the next domain's list
+        const uint32_t rr = av - kRank;
+        const uint32_t dv = __shfl_sync(0xffffffffu, dl, gb + (rr & 7u));
+        const uint32_t sv = rr < (uint32_t)kLanes ? dv : av;
+        if (e0 && has && k == 0 && j == 0) e0[0] = (uint16_t)sv;
+        uint16_t *urow = nullptr;
+        if (has && user_rows && k > 0) urow = user_rows + (uint64_t)(k - 1) * T.imax_user;
+        else if (has && user_row0 && k == 0) urow = user_row0;
+        // user row: imax_user <= 8 entries (rs == 8), lane j of the group writes entry j
+        const uint32_t v = __shfl_sync(0xffffffffu, sv, gb + (xl & 7u));
+        if (urow && j < T.imax_user) urow[j] = (uint16_t)(j < du ? v : kNone);
     }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
@@ -1340,14 +1381,14 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
 #endif
     // CTA fold of its chunk maps (shared memory), then the last CTA
     const uint32_t n = c1 - c0;
-    LMap acc = cta_tree_fold(T, RT, crow, cdom, trow, tdom, n, status);
+    LMap acc = cta_tree_fold(crow, cdom, trow, tdom, n);
 #ifdef DFA_TREE_TIMING
     unsigned long long tc1 = gtimer();
     if (threadIdx.x == 0) atomicMax(&g_tree_t[20], tc1 - tc0);
 #endif
     if (gridDim.x > 1) {
         if (warp == 0) {
-            if (lane < 8) cta_rows[(uint64_t)blockIdx.x * 8 + j] = (uint16_t)(j < acc.u ? acc.v : kNone);
+            if (lane < 8) cta_rows[(uint64_t)blockIdx.x * 8 + j] = (uint16_t)acc.v;
             if (lane == 0) cta_doms[blockIdx.x] = (uint16_t)acc.dom;
             __syncwarp();
             if (lane == 0) {
@@ -1370,22 +1411,24 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
         }
         __syncthreads();
         if (cta_start && threadIdx.x == 0) {
-            // true start of every CTA's first chunk: the prefix of Eq.SeqReduction over the CTA maps
-            uint32_t st = T.q0;
+            // rank code of every CTA's first chunk start: the prefix of
+            // Eq.SeqReduction over the CTA maps (chunk 0 starts at rank 0 of {q0})
+            uint32_t code = kRank;
             for (uint32_t i = 0; i < gridDim.x; i++) {
-                cta_start[i] = (uint16_t)st;
-                st = map_step(T, RT, crow + i * 8, cdom[i], st, status);
+                cta_start[i] = (uint16_t)code;
+                if (is_rank(code)) code = crow[i * 8 + (code - kRank)];
             }
         }
-        acc = cta_tree_fold(T, RT, crow, cdom, trow, tdom, gridDim.x, status);
+        acc = cta_tree_fold(crow, cdom, trow, tdom, gridDim.x);
 #ifdef DFA_TREE_TIMING
         if (threadIdx.x == 0) atomicMax(&g_tree_t[22], gtimer() - tc2);
 #endif
     }
-    if (cta_start && gridDim.x == 1 && threadIdx.x == 0) cta_start[0] = (uint16_t)T.q0;
+    if (cta_start && gridDim.x == 1 && threadIdx.x == 0) cta_start[0] = (uint16_t)kRank;
     if (threadIdx.x == 0) {
-        const uint32_t fs = acc.v;
+        const uint32_t fs = acc.v;  // absolute: the input's last sub-chunk ends in states
         if (fs == T.poison) atomicMax(&status->err, 5u);
+        if (is_rank(fs)) atomicMax(&status->err, 8u);
         status->final_state = fs;
         status->accept = fs < T.nq ? (uint32_t)test_bit(T.accept_bits, fs) : 0u;
         if (dev_final) {
@@ -1619,12 +1662,7 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)starts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute((void *)starts8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             optin - kCompose8Static);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute((void *)compose8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             optin - kCompose8Static);
-    if (e != cudaSuccess) return e;
+
     return cudaFuncSetAttribute((void *)tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
@@ -1669,7 +1707,7 @@ extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {
         unsigned long long init[32];
         init[0] = ~0ull;
         init[20] = ~0ull;
-        for (int i = 1; i < 32; i++) init[i] = (i == 10 || i == 14) ? ~0ull : 0;
+        for (int i = 1; i < 32; i++) init[i] = (i == 10 || i == 14 || i == 25) ? ~0ull : 0;
         cudaMemcpyToSymbol(g_tree_t, init, sizeof(init));
     }
     return 0;
@@ -1699,14 +1737,6 @@ cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uin
     return cudaGetLastError();
 }
 
-// the staged tables fit next to compose8_kernel's static shared memory
-int rtab_staged(const DevTables &T) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return (uint64_t)rtab_bytes(T) + kCompose8Static <= (uint64_t)optin ? 1 : 0;
-}
-
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};
@@ -1722,20 +1752,27 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+cudaError_t launch_leaf_fold(const uint16_t *in_rows, const uint16_t *in_dom, uint32_t L0, uint32_t L, uint32_t P,
+                             uint16_t *out_rows, uint16_t *out_dom, int sms, cudaStream_t s) {
+    const uint64_t total = (uint64_t)(L0 + 31) / 32 + (uint64_t)(P - 1) * ((L + 31) / 32);
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((total + 7) / 8, (uint64_t)sms * 8);
+    return launch_pdl(leaf_fold_kernel, dim3(grid), dim3(256), 0, s, in_rows, in_dom, L0, L, P, out_rows, out_dom);
+}
+
 cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const uint16_t *leaf_dom, uint32_t L0,
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
                             uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final,
                             uint16_t *cta_start, uint16_t *starts, cudaStream_t s) {
-    const int staged = rtab_staged(T);
+    // 4 chunks per warp per round: about one round per SM-resident CTA, cpc <= 1024
+    const uint32_t warps = std::min<uint32_t>(32, std::max<uint32_t>(1, (cpc + 3) / 4));
     const uint32_t grid = (P + cpc - 1) / cpc;
-    cudaError_t e = launch_pdl(compose8_kernel, dim3(grid), dim3(1024), staged ? rtab_bytes(T) : 0, s, T, leaves,
-                               leaf_dom, L0, L, P, cpc, rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows,
-                               cta_doms, ticket, st, dev_final, starts ? cta_start : nullptr, staged);
+    cudaError_t e = launch_pdl(compose8_kernel, dim3(grid), dim3(warps * 32), 0, s, T, leaves, leaf_dom, L0, L, P, cpc,
+                               rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows, cta_doms, ticket, st,
+                               dev_final, starts ? cta_start : nullptr);
     if (e != cudaSuccess || !starts) return e;
-    return launch_pdl(starts8_kernel, dim3(grid), dim3(256), staged ? rtab_bytes(T) : 0, s, T,
-                      (const uint16_t *)rep_rows, (const uint16_t *)rep_doms, P, cpc, (const uint16_t *)cta_start,
-                      starts, st, staged);
+    return launch_pdl(starts8_kernel, dim3(grid), dim3(256), 0, s, T, (const uint16_t *)rep_rows,
+                      (const uint16_t *)rep_doms, P, cpc, (const uint16_t *)cta_start, starts);
 }
 
 cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,

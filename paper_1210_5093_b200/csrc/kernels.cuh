@@ -134,6 +134,8 @@ cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms,
 cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,
                              const uint16_t *maps, uint16_t *doms_out, uint16_t *sizes_out, uint16_t *maps_out,
                              DevStatus *st, int sms, cudaStream_t s);
+cudaError_t launch_leaf_fold(const uint16_t *in_rows, const uint16_t *in_dom, uint32_t L0, uint32_t L, uint32_t P,
+                             uint16_t *out_rows, uint16_t *out_dom, int sms, cudaStream_t s);
 cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const uint16_t *leaf_dom, uint32_t L0,
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
