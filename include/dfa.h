@@ -226,8 +226,10 @@ enum {
     DFA_OPT_PROFILE = 3,         /* 1 = record per-kernel CUDA-event times */
     DFA_OPT_THREADS_PER_CTA = 4, /* match kernel CTA size (0 = auto) */
     DFA_OPT_TREE_FANIN = 5,      /* max children per composition-tree node, 2..64 (default 32) */
-    DFA_OPT_FOLD_IN_TREE = 6,    /* 1: fold the chunk maps in tree_kernel instead of fold_rows_kernel */
-    DFA_OPT_WARP_COMPOSE = 7,    /* 1 (default): maps of <= 8 entries composed in the match kernel's warps */
+    DFA_OPT_FOLD_IN_TREE = 6,    /* 1: maps of <= 16 entries go through tree_kernel (also for the final
+                                    fold) instead of the rank-space compose8 / fold_rows paths */
+    DFA_OPT_WARP_COMPOSE = 7,    /* 1 (default): maps of <= 8 entries composed in rank space: in the match
+                                    kernel's warps, leaf_fold_kernel and compose8_kernel; 0: tree path */
     DFA_OPT_GRAPHS = 8           /* 1 (default): replay a CUDA graph when a dfa_chunk_maps call repeats */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
