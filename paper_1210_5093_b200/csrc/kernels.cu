@@ -343,12 +343,13 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
     const uint8_t *endp = in + end;
     // head: up to 31 bytes until 32-byte alignment
     while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) step_scalar(tab, *ptr++, st, nlive);
-    const uint64_t nblk = (uint64_t)(endp - ptr) >> 5;
+    const uint32_t nblk = (uint32_t)((uint64_t)(endp - ptr) >> 5);  // sub-chunks < 128 GiB
     if (nblk) {
         U8x32 cur = ldg32(ptr);
-        for (uint64_t bi = 0; bi < nblk; bi++) {
+        const uint8_t *nptr = ptr + 32;
+        for (uint32_t bi = 0; bi < nblk; bi++, nptr += 32) {
             U8x32 nxt = cur;
-            if (bi + 1 < nblk) nxt = ldg32(ptr + 32 * (bi + 1));
+            if (bi + 1 < nblk) nxt = ldg32(nptr);
 #pragma unroll
             for (int half = 0; half < 2; half++) {
                 const uint4 v = half ? cur.hi : cur.lo;
@@ -370,7 +371,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
             }
             cur = nxt;
         }
-        ptr += nblk * 32;
+        ptr += (uint64_t)nblk * 32;
     }
     while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
     // remaining lanes: final state of the slot that carries them
