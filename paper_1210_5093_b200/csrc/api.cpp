@@ -152,7 +152,22 @@ dfa_status upload(dfa_handle *h) {
         }
     }
     const uint32_t bw = ((nq + 31) / 32 + 3) & ~3u;
-    std::vector<uint32_t> dead(bw, 0), absorb(bw, 0), accept(bw, 0), dead_user(bw, 0);
+    std::vector<uint32_t> dead(bw, 0), absorb(bw, 0), accept(bw, 0), dead_user(bw, 0), sticky(bw, 0);
+    {
+        // universal kill bytes: every state goes to Z; sticky: not in Z, not absorbing,
+        // and every other byte keeps the state (see checkpoint() in kernels.cu)
+        std::vector<uint8_t> kill(256, 1);
+        for (uint32_t b = 0; b < 256; b++)
+            for (uint32_t q = 0; q < nq && kill[b]; q++)
+                if (!p.dead[p.full[(size_t)q * 256 + b]]) kill[b] = 0;
+        for (uint32_t q = 0; q < nq; q++) {
+            if (p.dead[q] || p.absorbing[q]) continue;
+            bool st = true;
+            for (uint32_t b = 0; b < 256 && st; b++)
+                if (!kill[b] && p.full[(size_t)q * 256 + b] != q) st = false;
+            if (st) sticky[q >> 5] |= 1u << (q & 31);
+        }
+    }
     for (uint32_t q = 0; q < nq; q++) {
         if (p.dead[q]) dead[q >> 5] |= 1u << (q & 31);
         if (q < p.nq_user && p.dead_user[q]) dead_user[q >> 5] |= 1u << (q & 31);
@@ -176,6 +191,7 @@ dfa_status upload(dfa_handle *h) {
         {rank8.data(), rank8.size(), 0},
         {ixlat.data(), ixlat.size() * 2, 0},
         {dead_user.data(), dead_user.size() * 4, 0},
+        {sticky.data(), sticky.size() * 4, 0},
     };
     size_t total = 0;
     for (auto &s : secs) { s.off = total; total += (s.bytes + 255) & ~size_t(255); }
@@ -200,6 +216,10 @@ dfa_status upload(dfa_handle *h) {
     T.rank8 = rank8.empty() ? nullptr : at(11);
     T.ixlat = reinterpret_cast<const uint16_t *>(at(12));
     T.dead_user_bits = reinterpret_cast<const uint32_t *>(at(13));
+    T.sticky_bits = reinterpret_cast<const uint32_t *>(at(14));
+    T.has_sticky = 0;
+    for (uint32_t w : sticky) T.has_sticky |= w != 0;
+    if (getenv("DFA_NO_STICKY")) T.has_sticky = 0;  // experiments only
     T.nq_user = p.nq_user;
     T.ns = p.ns;
     T.nq = nq;

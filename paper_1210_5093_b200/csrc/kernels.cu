@@ -254,10 +254,21 @@ __device__ __forceinline__ void finish_slot(uint32_t slot, uint32_t state, uint3
 // Merge converged lanes, retire absorbing ones, compact.  B = the
 // warp's maximum live-lane count (compile time): the pair tests and the
 // compaction cost O(B^2), not O(kLanes^2).
+// Sticky-lane suspension: a state A is sticky when every byte either keeps A
+// or is a universal kill byte (every state -> Z; e.g. a motif-found state
+// over residues, foreign bytes -> the dead sink).  While another lane of the
+// thread stays live, a lane in A is parked (Pend: A, the original lanes it
+// carries, the 32-byte-aligned offset where it was parked): a kill byte would
+// also kill the live lane, so A survives exactly while some live lane does.
+// If all live lanes end, the parked lanes resume from the parking offset.
+constexpr uint32_t kNoPend = 0xFFFFFFFFu;
+
 template <int B>
 __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_absorb, uint32_t bias,
                                            uint32_t (&st)[kLanes],
-                                           uint32_t (&own)[kLanes], uint32_t &nlive, uint32_t (&fin)[kLanes]) {
+                                           uint32_t (&own)[kLanes], uint32_t &nlive, uint32_t (&fin)[kLanes],
+                                           const uint32_t *sticky, bool suspend, uint32_t &pend,
+                                           uint32_t &pend_off, uint32_t cur_off) {
     const uint32_t full = (1u << nlive) - 1u;
     uint32_t lm = full;
     if (nlive == 1) {
@@ -279,6 +290,30 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_abso
                     for (int r = 0; r < kLanes; r++)
                         if (own[r] == (uint32_t)b) own[r] = a;
                 }
+        if (suspend) {
+            uint32_t pstate = pend == kNoPend ? kNone : (pend & 0xFFFFu), sm = 0;
+#pragma unroll
+            for (int l = 0; l < B; l++) {
+                if (!((lm >> l) & 1u)) continue;
+                const uint32_t q = st[l] - bias;
+                if (!test_bit(sticky, q)) continue;
+                if (pstate == kNone) pstate = q;
+                if (q == pstate) sm |= 1u << l;
+            }
+            if (sm && sm != lm) {  // keep at least one live lane as the witness
+                uint32_t mask = pend == kNoPend ? 0u : (pend >> 16);
+#pragma unroll
+                for (int l = 0; l < B; l++) {
+                    if (!((sm >> l) & 1u)) continue;
+#pragma unroll
+                    for (int r = 0; r < kLanes; r++)
+                        if (own[r] == (uint32_t)l) { mask |= 1u << r; own[r] = kDone; }
+                }
+                if (pend == kNoPend) pend_off = cur_off;
+                pend = pstate | (mask << 16);
+                lm &= ~sm;
+            }
+        }
     }
     if (lm == full) return;
     uint32_t pc[B];
@@ -310,11 +345,13 @@ __device__ __forceinline__ void checkpoint(const uint32_t *absorb, bool has_abso
 template <int B, int MODE>
 __device__ __forceinline__ bool block_step(const Tab<MODE> &tab, uint4 v, const uint32_t *absorb, bool has_absorb,
                                            uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t &nlive,
-                                           uint32_t (&fin)[kLanes], int convergence, bool tick) {
+                                           uint32_t (&fin)[kLanes], int convergence, bool tick,
+                                           const uint32_t *sticky, bool suspend, uint32_t &pend, uint32_t &pend_off,
+                                           uint32_t cur_off) {
     block16<B, MODE>(tab, v, st);
     if (!convergence) return false;
     if (B > 1 && nlive > 1) {
-        checkpoint<B>(absorb, has_absorb, tab.bias, st, own, nlive, fin);
+        checkpoint<B>(absorb, has_absorb, tab.bias, st, own, nlive, fin, sticky, suspend, pend, pend_off, cur_off);
         return nlive == 0;
     }
     if (has_absorb && tick && nlive == 1 && test_bit(absorb, st[0] - tab.bias)) {
@@ -333,47 +370,90 @@ __device__ __forceinline__ void step_scalar(const Tab<MODE> &tab, uint32_t b, ui
         if ((uint32_t)l < nlive) st[l] = tab.look_pre(st[l], pb);
 }
 
-template <int MODE>
+// Parked lanes resume as one live slot (the state's encoding) carrying them.
+__device__ __forceinline__ void resume_pend(uint32_t &pend, uint32_t bias, uint32_t (&st)[kLanes],
+                                            uint32_t (&own)[kLanes], uint32_t &nlive) {
+    const uint32_t mask = pend >> 16, q = pend & 0xFFFFu;
+#pragma unroll
+    for (int l = 0; l < kLanes; l++)
+        if ((uint32_t)l == nlive) st[l] = q + bias;
+#pragma unroll
+    for (int r = 0; r < kLanes; r++)
+        if ((mask >> r) & 1u) own[r] = nlive;
+    nlive++;
+    pend = kNoPend;
+}
+
+template <int MODE, bool STICKY>
 __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *absorb, bool has_absorb,
+                                          const uint32_t *sticky, const uint32_t *deadb,
                                           const uint8_t *in, uint64_t pos,
                           uint64_t end, uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t nl,
                           int convergence, uint32_t (&fin)[kLanes]) {
     uint32_t nlive = nl;
-    const uint8_t *ptr = in + pos;
+    const uint8_t *s0 = in + pos;
+    const uint8_t *ptr = s0;
     const uint8_t *endp = in + end;
+    uint32_t pend = kNoPend, pend_off = 0;
+    const bool susp = STICKY && convergence;
     // head: up to 31 bytes until 32-byte alignment
     while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) step_scalar(tab, *ptr++, st, nlive);
-    const uint32_t nblk = (uint32_t)((uint64_t)(endp - ptr) >> 5);  // sub-chunks < 128 GiB
-    if (nblk) {
-        U8x32 cur = ldg32(ptr);
-        const uint8_t *nptr = ptr + 32;
-        for (uint32_t bi = 0; bi < nblk; bi++, nptr += 32) {
-            U8x32 nxt = cur;
-            if (bi + 1 < nblk) nxt = ldg32(nptr);
+    for (;;) {
+        bool restart = false;
+        const uint32_t nblk = (uint32_t)((uint64_t)(endp - ptr) >> 5);  // sub-chunks < 128 GiB
+        if (nblk) {
+            U8x32 cur = ldg32(ptr);
+            const uint8_t *nptr = ptr + 32;
+            for (uint32_t bi = 0; bi < nblk && !restart; bi++, nptr += 32) {
+                U8x32 nxt = cur;
+                if (bi + 1 < nblk) nxt = ldg32(nptr);
 #pragma unroll
-            for (int half = 0; half < 2; half++) {
-                const uint4 v = half ? cur.hi : cur.lo;
-                // the warp steps max(live lanes) lanes (exact, 1..8): lanes converge fast
-                const bool tick = half && (bi & 1);
-                bool done;
-                switch (__reduce_max_sync(__activemask(), nlive)) {
-                case 0:
-                case 1: done = block_step<1>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                case 2: done = block_step<2>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                case 3: done = block_step<3>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                case 4: done = block_step<4>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                case 5: done = block_step<5>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                case 6: done = block_step<6>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                case 7: done = block_step<7>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
-                default: done = block_step<8>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick); break;
+                for (int half = 0; half < 2; half++) {
+                    const uint4 v = half ? cur.hi : cur.lo;
+                    // the warp steps max(live lanes) lanes (exact, 1..8): lanes converge fast
+                    const bool tick = half && (bi & 1);
+                    const bool sp = susp && half;
+                    const uint32_t co = (uint32_t)(nptr - s0);
+                    bool done;
+                    switch (__reduce_max_sync(__activemask(), nlive)) {
+                    case 0:
+                    case 1: done = block_step<1>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    case 2: done = block_step<2>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    case 3: done = block_step<3>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    case 4: done = block_step<4>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    case 5: done = block_step<5>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    case 6: done = block_step<6>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    case 7: done = block_step<7>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    default: done = block_step<8>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, sticky, sp, pend, pend_off, co); break;
+                    }
+                    if (done) {
+                        if (pend == kNoPend) return;
+                        restart = true;  // no live witness left: the parked lanes resume
+                        break;
+                    }
                 }
-                if (done) return;
+                cur = nxt;
             }
-            cur = nxt;
+            if (!restart) ptr += (uint64_t)nblk * 32;
         }
-        ptr += (uint64_t)nblk * 32;
+        if (!restart) {
+            while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
+            if (pend == kNoPend) break;
+            bool alive = false;  // a live, non-error lane witnesses that no kill byte came
+#pragma unroll
+            for (int l = 0; l < kLanes; l++)
+                if ((uint32_t)l < nlive && !test_bit(deadb, st[l] - tab.bias)) alive = true;
+            if (alive) {
+                const uint32_t mask = pend >> 16, q = pend & 0xFFFFu;
+#pragma unroll
+                for (int r = 0; r < kLanes; r++)
+                    if ((mask >> r) & 1u) fin[r] = q;
+                break;
+            }
+        }
+        ptr = s0 + pend_off;
+        resume_pend(pend, tab.bias, st, own, nlive);
     }
-    while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
     // remaining lanes: final state of the slot that carries them
 #pragma unroll
     for (int r = 0; r < kLanes; r++) {
@@ -418,7 +498,7 @@ __device__ __forceinline__ void warp_compose(uint32_t mask, uint32_t g_log, uint
     }
 }
 
-template <int MODE>
+template <int MODE, bool STICKY>
 __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                     const uint16_t *__restrict__ surv,
                                                     const uint8_t *__restrict__ surv_n,
@@ -434,6 +514,16 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
 #endif
     extern __shared__ uint4 smem4[];
     uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
+    // sticky and error-state bitmaps after the absorbing one (sticky variant only)
+    const uint32_t bw = bits_words(T.nq);
+    uint32_t *sticky_s = reinterpret_cast<uint32_t *>(tsm) + T.image_words + bw;
+    uint32_t *dead_s = sticky_s + bw;
+    if (STICKY) {
+        for (uint32_t i = threadIdx.x; i < bw; i += blockDim.x) {
+            sticky_s[i] = __ldg(T.sticky_bits + i);
+            dead_s[i] = __ldg(T.dead_bits + i);
+        }
+    }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[26], gtimer());
@@ -469,7 +559,8 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
             uint32_t fin[kLanes];
 #pragma unroll
             for (int l = 0; l < kLanes; l++) fin[l] = kNone;
-            run_lanes<MODE>(tab, absorb, T.has_absorb != 0, in, pos, end, st, own, nl, convergence, fin);
+            run_lanes<MODE, STICKY>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
+                                    convergence, fin);
 #ifdef DFA_TREE_TIMING
             if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[27], gtimer());
 #endif
@@ -1583,18 +1674,19 @@ __global__ void __launch_bounds__(512) starts_kernel(DevTables T, Plan p, const 
 }
 
 template <int MODE>
-void *lanes_ptr() { return (void *)lanes_kernel<MODE>; }
+void *lanes_ptr(bool sticky) { return sticky ? (void *)lanes_kernel<MODE, true> : (void *)lanes_kernel<MODE, false>; }
 template <int MODE>
 void *converge_ptr() { return (void *)converge_kernel<MODE>; }
 
-void *lanes_fn(int mode) {
-    switch (mode) {
-    case kIdentU8: return lanes_ptr<kIdentU8>();
-    case kIdentU16: return lanes_ptr<kIdentU16>();
-    case kWindowU8: return lanes_ptr<kWindowU8>();
-    case kWindowU16: return lanes_ptr<kWindowU16>();
-    case kPacked9: return lanes_ptr<kPacked9>();
-    default: return lanes_ptr<kGlobalU16>();
+void *lanes_fn(const DevTables &T) {
+    const bool st = T.has_sticky != 0;
+    switch (T.mode) {
+    case kIdentU8: return lanes_ptr<kIdentU8>(st);
+    case kIdentU16: return lanes_ptr<kIdentU16>(st);
+    case kWindowU8: return lanes_ptr<kWindowU8>(st);
+    case kWindowU16: return lanes_ptr<kWindowU16>(st);
+    case kPacked9: return lanes_ptr<kPacked9>(st);
+    default: return lanes_ptr<kGlobalU16>(st);
     }
 }
 void *converge_fn(int mode) {
@@ -1626,7 +1718,9 @@ int probe_dynamic_smem_base(uint32_t *dev_scratch) {
     return (int)v;
 }
 
-int lanes_smem_bytes(const DevTables &T) { return (int)(256 + T.image_words * 4 + bits_words_host(T.nq) * 4); }
+int lanes_smem_bytes(const DevTables &T) {
+    return (int)(256 + T.image_words * 4 + (T.has_sticky ? 3 : 1) * bits_words_host(T.nq) * 4);
+}
 
 int converge_smem_bytes(const DevTables &T, int warps_per_cta) {
     const uint32_t scr = (4 * T.imax + T.nq + 7) & ~7u;
@@ -1653,7 +1747,7 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaError_t e = cudaFuncSetAttribute(lanes_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaError_t e = cudaFuncSetAttribute(lanes_fn(T), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
@@ -1669,7 +1763,7 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
 
 int lanes_occupancy(const DevTables &T, int threads) {
     int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lanes_fn(T.mode), threads, lanes_smem_bytes(T));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lanes_fn(T), threads, lanes_smem_bytes(T));
     return blocks;
 }
 
@@ -1696,7 +1790,7 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
                     (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap,
                     (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status};
-    return cudaLaunchKernel(lanes_fn(T.mode), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
+    return cudaLaunchKernel(lanes_fn(T), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
 }
 
 const void *tree_fn() { return (const void *)tree_kernel; }

@@ -40,11 +40,13 @@ struct DevTables {
     const uint16_t *ixlat;      // [nclass * rs]: user index of internal entry j, or 0xFFFF
     const uint16_t *dom_user_size; // [nclass]
     const uint32_t *dead_user_bits; // user Z (reading R1) over the user states
+    const uint32_t *sticky_bits;    // states kept by every byte that is not a universal kill byte
     uint32_t nq, nclass, start_dom, imax, imax_user;
     uint32_t nq_user, ns;       // user |Q| and |Sigma|
     uint32_t rs;                // map row stride: imax rounded up to 8 (16-byte rows)
     uint32_t has_dead;          // internal Z non-empty
     uint32_t has_absorb;        // some state absorbs every byte
+    uint32_t has_sticky;        // some non-absorbing state is sticky (lanes_kernel parks it)
     uint32_t stride, win_base, win_w;
     int mode;
     uint32_t q0, poison;

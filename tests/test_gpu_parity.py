@@ -467,3 +467,40 @@ def test_alg2_full_domain_parity(name):
     c = Case(w.automaton, x, name)
     check_chunk_maps(c, 61, flags=D.DFA_CREATE_FULL_DOMAIN)
     check_match(c, flags=D.DFA_CREATE_FULL_DOMAIN)
+
+
+# ------------------------------------------------------------------ sticky-lane parking (lanes_kernel)
+def sticky_dfa(nq: int, seed: int, n_kill: int = 6, die_rate: float = 0.05):
+    """Random DFA over 256 bytes with a dead sink (state nq-1), universal kill bytes
+    (the last n_kill byte values send every state to the sink), a sticky state 0
+    (every other byte keeps it) and random states that also die on some ordinary bytes."""
+    rng = np.random.default_rng(seed)
+    sink = nq - 1
+    t = rng.integers(1, nq - 1, size=(nq, 256)).astype(np.uint16)
+    t[rng.random((nq, 256)) < die_rate] = sink
+    t[0, :] = 0
+    t[:, 256 - n_kill:] = sink
+    t[sink, :] = sink
+    # make state 0 reachable from many states on a few bytes
+    t[:, 10] = np.where(np.arange(nq) == sink, sink, 0)
+    acc = [0, 3]
+    return automata.Automaton(t, 0 if seed % 2 else 1, np.array([q in acc for q in range(nq)]),
+                              f"sticky{seed}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sticky_parking(seed):
+    """Parked lanes survive while a witness lives, die with it on a kill byte, and
+    resume from the parking offset when the witness ends on an ordinary byte."""
+    a = sticky_dfa(12 + 5 * seed, seed)
+    rng = np.random.default_rng(100 + seed)
+    n = 1 << 18
+    x = rng.integers(0, 250, n).astype(np.uint8)
+    # sparse kill bytes and dense runs of the byte that enters the sticky state
+    kills = rng.choice(n, 8 + seed * 4, replace=False)
+    x[kills] = rng.integers(250, 256, kills.size)
+    x[rng.choice(n, 2000, replace=False)] = 10
+    c = Case(a, x, f"sticky{seed}")
+    for P in (1, 7, 333):
+        check_chunk_maps(c, P)
+    check_match(c)
