@@ -340,7 +340,14 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
     const int base_threads = lanes_threads(h);
     const int bps = std::max(1, std::min(2, lanes_occupancy(h->T, 512)));
     uint64_t target = h->subchunk_target;
-    if (target <= 0) target = (uint64_t)h->sms * std::max(1, lanes_occupancy(h->T, base_threads)) * base_threads;
+    if (target <= 0) {
+        target = (uint64_t)h->sms * std::max(1, lanes_occupancy(h->T, base_threads)) * base_threads;
+        // converge_kernel costs ~ NS * |I_sigma| while a lanes kernel held to one CTA per SM
+        // by a large table is pipe-bound at ~16 warps per SM (Worst, measured: 95k
+        // sub-chunks 1499 GB/s, 151k 1388 GB/s): fewer, longer sub-chunks there
+        if (h->convergence && h->T.imax > (uint32_t)kLanes && lanes_occupancy(h->T, 512) < 2)
+            target = target * 5 / 8;
+    }
     const uint64_t len0 = hb[1] - hb[0];
     uint64_t minlen = len0, avg = len0;
     if (P > 1) {
