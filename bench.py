@@ -64,7 +64,8 @@ def parse():
     return ap.parse_args()
 
 
-OPTS = {"subchunk_target": 1, "convergence": 2, "threads_per_cta": 4, "tree_fanin": 5, "fold_in_tree": 6, "warp_compose": 7, "graphs": 8}
+OPTS = {"subchunk_target": 1, "convergence": 2, "threads_per_cta": 4, "tree_fanin": 5, "fold_in_tree": 6, "warp_compose": 7, "graphs": 8,
+        "max_lanes": 9}
 
 
 def peaks():

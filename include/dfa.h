@@ -230,7 +230,10 @@ enum {
                                     fold) instead of the rank-space compose8 / fold_rows paths */
     DFA_OPT_WARP_COMPOSE = 7,    /* 1 (default): maps of <= 8 entries composed in rank space: in the match
                                     kernel's warps, leaf_fold_kernel and compose8_kernel; 0: tree path */
-    DFA_OPT_GRAPHS = 8           /* 1 (default): replay a CUDA graph when a dfa_chunk_maps call repeats */
+    DFA_OPT_GRAPHS = 8,          /* 1 (default): replay a CUDA graph when a dfa_chunk_maps call repeats */
+    DFA_OPT_MAX_LANES = 9        /* lanes per thread in the match kernel, 1..8 (default 8): converge_kernel
+                                    runs until at most this many lanes survive; larger domains without
+                                    the converge stage take several passes */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 

@@ -34,6 +34,7 @@ DFA_OPT_TREE_FANIN = 5
 DFA_OPT_FOLD_IN_TREE = 6
 DFA_OPT_WARP_COMPOSE = 7
 DFA_OPT_GRAPHS = 8
+DFA_OPT_MAX_LANES = 9
 TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16"}
 
 

@@ -77,6 +77,7 @@ struct dfa_handle {
     uint32_t graph_kernels = 0;
     struct { uint32_t m0, m, g_log; int threads; } plan_split_c{};
     int fold_in_tree = 0;
+    int max_lanes = kLanes;       // lanes per thread (DFA_OPT_MAX_LANES, 1..8)
     std::vector<uint64_t> tree_sig;
     HostPinned h_status, h_bounds;
     cudaEvent_t staging_done = nullptr;
@@ -440,7 +441,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + wpc - 1) / wpc);
         prof_begin(h, s, 0);
         CK(launch_converge(T, plan, in, h->surv.as<uint16_t>(), h->surv_n.as<uint8_t>(), h->surv_pos.as<uint64_t>(),
-                           h->amap.as<uint16_t>(), wpc, (int)grid, s));
+                           h->amap.as<uint16_t>(), (uint32_t)h->max_lanes, wpc, (int)grid, s));
         prof_end(h, s);
         kernels++;
         amap = h->amap.as<uint16_t>();
@@ -460,7 +461,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         prof_begin(h, s, 1);
         CK(launch_lanes(T, plan, in, surv, surv_n, surv_pos, h->sfin.as<uint16_t>(), sk, h->dom_of.as<uint16_t>(),
                         h->convergence, const_cast<uint16_t *>(amap), sp.g_log, h->leaf_rows.as<uint16_t>(),
-                        h->leaf_dom.as<uint16_t>(), h->status.as<DevStatus>(), threads, (int)grid, s));
+                        h->leaf_dom.as<uint16_t>(), h->status.as<DevStatus>(), (uint32_t)h->max_lanes, threads,
+                        (int)grid, s));
         prof_end(h, s);
         kernels++;
     }
@@ -911,7 +913,9 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     for (uint64_t v : {(uint64_t)(uintptr_t)dev_input, (uint64_t)(uintptr_t)dev_bounds,
                        (uint64_t)(uintptr_t)dev_chunk0_end, (uint64_t)(uintptr_t)dev_maps,
                        (uint64_t)(uintptr_t)dev_chunk_start, (uint64_t)(uintptr_t)dev_final, (uint64_t)h->profile,
-                       (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree})
+                       (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
+                       (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
+                       (uint64_t)h->threads})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
 }
@@ -1007,6 +1011,10 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
     if (!h) return DFA_ERR_ARG;
     switch (key) {
     case DFA_OPT_SUBCHUNK_TARGET: if (value < 0) return DFA_ERR_ARG; h->subchunk_target = value; return DFA_OK;
+    case DFA_OPT_MAX_LANES:
+        if (value < 1 || value > kLanes) return DFA_ERR_ARG;
+        h->max_lanes = (int)value;
+        return DFA_OK;
     case DFA_OPT_CONVERGENCE: h->convergence = value ? 1 : 0; return DFA_OK;
     case DFA_OPT_PROFILE: h->profile = value ? 1 : 0; return DFA_OK;
     case DFA_OPT_TREE_FANIN:

@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
                                                     uint16_t *__restrict__ dom_of, int convergence,
                                                     uint16_t *__restrict__ amap, uint32_t g_log,
                                                     uint16_t *__restrict__ leaf_rows, uint16_t *__restrict__ leaf_dom,
-                                                    DevStatus *status) {
+                                                    DevStatus *status, uint32_t cap) {
     pdl_trigger();  // one wave: the composition kernels may take SMs as CTAs retire
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMin(&g_tree_t[25], gtimer());
@@ -542,12 +542,52 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
         uint64_t pos;
         if (surv) { u = surv_n[i]; pos = surv_pos[i]; }
         else { u = T.dom_size[dom]; pos = start; }
-        for (uint32_t pass = 0; pass * kLanes < u; pass++) {
-            const uint32_t nl = min((uint32_t)kLanes, u - pass * kLanes);
-            uint32_t st[kLanes], own[kLanes];
+        // the grouped (rank-space) epilogue: convert, compose the warp's groups, write leaves
+        auto grouped_epilogue = [&](uint32_t (&fin)[kLanes]) {
+            const uint64_t wbase = i & ~31ull;
+            const uint32_t mask = wbase + 32 <= p.NS ? 0xffffffffu : ((1u << (uint32_t)(p.NS - wbase)) - 1u);
+            // rank space: final states as ranks in the next sub-chunk's domain
+            // I_sigma, sigma = this sub-chunk's last byte (absolute for error
+            // states and for the input's last sub-chunk)
+            if (i + 1 < p.NS) {
+                const uint32_t nd = T.byte_class[__ldg(in + end - 1)];
+                const uint8_t *rk = T.rank8 + (uint64_t)nd * T.nq;
+                uint32_t rr[kLanes];
+#pragma unroll
+                for (int l = 0; l < kLanes; l++) rr[l] = (uint32_t)l < u ? __ldg(rk + fin[l]) : 0xFFu;
+#pragma unroll
+                for (int l = 0; l < kLanes; l++) {
+                    if ((uint32_t)l >= u) continue;
+                    if (rr[l] < (uint32_t)kLanes) fin[l] = kRank + rr[l];
+                    else if (!(T.has_dead && test_bit(T.dead_bits, fin[l]))) atomicMax(&status->err, 8u);
+                }
+            }
+            __syncwarp(mask);
+            warp_compose(mask, g_log, fin);
+#ifdef DFA_TREE_TIMING
+            if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[28], gtimer());
+#endif
+            if (((threadIdx.x & 31) & ((1u << g_log) - 1)) == 0) {
+                const uint64_t leaf = i >> g_log;
+                uint4 v;
+                v.x = (fin[0] & 0xFFFFu) | (fin[1] << 16);
+                v.y = (fin[2] & 0xFFFFu) | (fin[3] << 16);
+                v.z = (fin[4] & 0xFFFFu) | (fin[5] << 16);
+                v.w = (fin[6] & 0xFFFFu) | (fin[7] << 16);
+                reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
+                leaf_dom[leaf] = (uint16_t)dom;
+            }
+        };
+        // grouped with cap = 8 (u <= 8): one pass, the map stays in registers and every
+        // thread of the warp reaches the epilogue's shuffles (also u = 0); otherwise
+        // passes of <= cap lanes whose finals go through sfin
+        const bool single = g_log != kNoGroup && cap >= (uint32_t)kLanes;
+        for (uint32_t pass = 0;; pass++) {
+            const uint32_t nl = u > pass * cap ? min(cap, u - pass * cap) : 0u;
+            uint32_t st[kLanes], own[kLanes], fin[kLanes];
 #pragma unroll
             for (int l = 0; l < kLanes; l++) {
-                const uint32_t r = pass * kLanes + l;
+                const uint32_t r = pass * cap + l;
                 if ((uint32_t)l < nl) {
                     st[l] = tab.enc(surv ? surv[i * kLanes + r] : T.dom_list[(uint64_t)dom * T.imax + r]);
                     own[l] = l;
@@ -555,57 +595,27 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
                     st[l] = tab.enc(0);
                     own[l] = kDone;
                 }
+                fin[l] = kNone;
             }
-            uint32_t fin[kLanes];
-#pragma unroll
-            for (int l = 0; l < kLanes; l++) fin[l] = kNone;
-            run_lanes<MODE, STICKY>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
-                                    convergence, fin);
+            if (nl) run_lanes<MODE, STICKY>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
+                                            convergence, fin);
 #ifdef DFA_TREE_TIMING
             if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[27], gtimer());
 #endif
-            if (g_log != kNoGroup) {
-                // maps of <= 8 entries: compose aligned groups of 2^g_log sub-chunks in
-                // the warp and write one leaf per group (no per-sub-chunk map in HBM)
-                const uint64_t wbase = i & ~31ull;
-                const uint32_t mask = wbase + 32 <= p.NS ? 0xffffffffu : ((1u << (uint32_t)(p.NS - wbase)) - 1u);
-                // rank space: final states as ranks in the next sub-chunk's domain
-                // I_sigma, sigma = this sub-chunk's last byte (absolute for error
-                // states and for the input's last sub-chunk)
-                if (i + 1 < p.NS) {
-                    const uint32_t nd = T.byte_class[__ldg(in + end - 1)];
-                    const uint8_t *rk = T.rank8 + (uint64_t)nd * T.nq;
-                    uint32_t rr[kLanes];
-#pragma unroll
-                    for (int l = 0; l < kLanes; l++) rr[l] = (uint32_t)l < u ? __ldg(rk + fin[l]) : 0xFFu;
-#pragma unroll
-                    for (int l = 0; l < kLanes; l++) {
-                        if ((uint32_t)l >= u) continue;
-                        if (rr[l] < (uint32_t)kLanes) fin[l] = kRank + rr[l];
-                        else if (!(T.has_dead && test_bit(T.dead_bits, fin[l]))) atomicMax(&status->err, 8u);
-                    }
-                }
-                __syncwarp(mask);
-                const uint32_t d = dom;
-                warp_compose(mask, g_log, fin);
-#ifdef DFA_TREE_TIMING
-                if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[28], gtimer());
-#endif
-                if (((threadIdx.x & 31) & ((1u << g_log) - 1)) == 0) {
-                    const uint64_t leaf = i >> g_log;
-                    uint4 v;
-                    v.x = (fin[0] & 0xFFFFu) | (fin[1] << 16);
-                    v.y = (fin[2] & 0xFFFFu) | (fin[3] << 16);
-                    v.z = (fin[4] & 0xFFFFu) | (fin[5] << 16);
-                    v.w = (fin[6] & 0xFFFFu) | (fin[7] << 16);
-                    reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
-                    leaf_dom[leaf] = (uint16_t)d;
-                }
-            } else {
-#pragma unroll
-                for (int l = 0; l < kLanes; l++)
-                    if ((uint32_t)l < nl) sfin[i * sk + pass * kLanes + l] = (uint16_t)fin[l];
+            if (single) {
+                grouped_epilogue(fin);
+                break;
             }
+#pragma unroll
+            for (int l = 0; l < kLanes; l++)
+                if ((uint32_t)l < nl) sfin[i * sk + pass * cap + l] = (uint16_t)fin[l];
+            if ((pass + 1) * cap >= u) break;
+        }
+        if (g_log != kNoGroup && !single) {
+            uint32_t fin[kLanes];
+#pragma unroll
+            for (int e = 0; e < kLanes; e++) fin[e] = (uint32_t)e < u ? sfin[i * sk + e] : (uint32_t)kNone;
+            grouped_epilogue(fin);
         }
         if (surv) {
             // resolve this sub-chunk's converge_kernel map in place: survivor code
@@ -653,7 +663,7 @@ template <int MODE>
 __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                        uint16_t *__restrict__ surv, uint8_t *__restrict__ surv_n,
                                                        uint64_t *__restrict__ surv_pos,
-                                                       uint16_t *__restrict__ amap) {
+                                                       uint16_t *__restrict__ amap, uint32_t cap) {
     extern __shared__ uint4 smem4[];
     const uint32_t bw = bits_words(T.nq);
     uint8_t *tsm = load_tables<MODE>(T, smem4, bw);
@@ -684,7 +694,7 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
         uint64_t pos = start;
         __syncwarp();
         uint32_t wlen = 16;  // merge every 16 bytes (merging is dearer than stepping: measured)
-        while (np > (uint32_t)kLanes && pos < end) {
+        while (np > cap && pos < end) {
             // window [pos, min(pos + wlen, next 16-byte boundary of the *address*, end))
             const uint64_t abase = pos - ((reinterpret_cast<uintptr_t>(in) + pos) & 15u);
             const uint32_t k0 = (uint32_t)(pos - abase);
@@ -1775,9 +1785,10 @@ int converge_occupancy(const DevTables &T, int warps_per_cta) {
 }
 
 cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in, uint16_t *surv, uint8_t *surv_n,
-                            uint64_t *surv_pos, uint16_t *amap, int warps_per_cta, int grid, cudaStream_t s) {
+                            uint64_t *surv_pos, uint16_t *amap, uint32_t cap, int warps_per_cta, int grid,
+                            cudaStream_t s) {
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
-                    (void *)&amap};
+                    (void *)&amap, (void *)&cap};
     return cudaLaunchKernel(converge_fn(T.mode), dim3(grid), dim3(warps_per_cta * 32), args,
                             converge_smem_bytes(T, warps_per_cta), s);
 }
@@ -1785,11 +1796,11 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
                          uint16_t *dom_of, int convergence, uint16_t *amap, uint32_t g_log,
-                         uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, int threads, int grid,
-                         cudaStream_t s) {
+                         uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, uint32_t cap, int threads,
+                         int grid, cudaStream_t s) {
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
                     (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap,
-                    (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status};
+                    (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status, (void *)&cap};
     return cudaLaunchKernel(lanes_fn(T), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
 }
 

@@ -120,14 +120,14 @@ struct LaunchCfg {
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in, uint16_t *surv,
-                            uint8_t *surv_n, uint64_t *surv_pos, uint16_t *amap, int warps_per_cta,
+                            uint8_t *surv_n, uint64_t *surv_pos, uint16_t *amap, uint32_t cap, int warps_per_cta,
                             int grid, cudaStream_t s);
 int converge_smem_bytes(const DevTables &T, int warps_per_cta);
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
                          uint16_t *dom_of, int convergence, uint16_t *amap, uint32_t g_log,
-                         uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, int threads, int grid,
-                         cudaStream_t s);
+                         uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, uint32_t cap, int threads,
+                         int grid, cudaStream_t s);
 int lanes_smem_bytes(const DevTables &T);
 int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);

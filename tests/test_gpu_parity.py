@@ -504,3 +504,14 @@ def test_sticky_parking(seed):
     for P in (1, 7, 333):
         check_chunk_maps(c, P)
     check_match(c)
+
+
+@pytest.mark.parametrize("cap", [1, 3, 5])
+@pytest.mark.parametrize("name", ["random", "keyword", "protein", "worst"])
+def test_max_lanes(name, cap):
+    """DFA_OPT_MAX_LANES (the Worst config's lanes-per-thread sweep): converge to
+    <= cap survivors / several passes of <= cap lanes; same results."""
+    w = W.get(name)
+    x = w.input(min(w.small_n, 1 << 19))
+    c = Case(w.automaton, x, name)
+    check_chunk_maps(c, 129, opts={D.DFA_OPT_MAX_LANES: cap})
