@@ -132,13 +132,14 @@ dfa_status upload(dfa_handle *h) {
     const uint32_t nq = p.nq, nc = p.nclass, imax = p.imax, imu = p.imax_user_stride;
     std::vector<uint32_t> image = p.image;
     while (image.size() % 4) image.push_back(0);
-    std::vector<uint16_t> dom_list((size_t)(nc + 1) * imax, kNone), dom_size(nc + 1, 0);
+    const uint32_t dls = (imax + 7) & ~7u;  // dom_list row stride = rs (16-byte rows)
+    std::vector<uint16_t> dom_list((size_t)(nc + 1) * dls, kNone), dom_size(nc + 1, 0);
     std::vector<uint16_t> rank((size_t)(nc + 1) * nq, kNone);
     std::vector<uint8_t> rank8(imax < 255 ? (size_t)(nc + 1) * nq : 0, 0xFF);
     for (uint32_t c = 0; c <= nc; c++) {
         dom_size[c] = (uint16_t)p.dom[c].size();
         for (uint32_t j = 0; j < p.dom[c].size(); j++) {
-            dom_list[(size_t)c * imax + j] = p.dom[c][j];
+            dom_list[(size_t)c * dls + j] = p.dom[c][j];
             rank[(size_t)c * nq + p.dom[c][j]] = (uint16_t)j;
             if (!rank8.empty()) rank8[(size_t)c * nq + p.dom[c][j]] = (uint8_t)j;
         }

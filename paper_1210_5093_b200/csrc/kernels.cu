@@ -550,15 +550,18 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
             // I_sigma, sigma = this sub-chunk's last byte (absolute for error
             // states and for the input's last sub-chunk)
             if (i + 1 < p.NS) {
+                // rank = position in the next domain's row (<= 8 entries, one 16-byte load)
                 const uint32_t nd = T.byte_class[__ldg(in + end - 1)];
-                const uint8_t *rk = T.rank8 + (uint64_t)nd * T.nq;
-                uint32_t rr[kLanes];
-#pragma unroll
-                for (int l = 0; l < kLanes; l++) rr[l] = (uint32_t)l < u ? __ldg(rk + fin[l]) : 0xFFu;
+                const uint4 nr = __ldg(reinterpret_cast<const uint4 *>(T.dom_list + (uint64_t)nd * 8));
+                const uint32_t w[4] = {nr.x, nr.y, nr.z, nr.w};
 #pragma unroll
                 for (int l = 0; l < kLanes; l++) {
                     if ((uint32_t)l >= u) continue;
-                    if (rr[l] < (uint32_t)kLanes) fin[l] = kRank + rr[l];
+                    uint32_t rr = kNone;
+#pragma unroll
+                    for (int e = 0; e < kLanes; e++)
+                        if (((w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu) == fin[l]) rr = e;
+                    if (rr != kNone) fin[l] = kRank + rr;
                     else if (!(T.has_dead && test_bit(T.dead_bits, fin[l]))) atomicMax(&status->err, 8u);
                 }
             }
@@ -585,11 +588,18 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
         for (uint32_t pass = 0;; pass++) {
             const uint32_t nl = u > pass * cap ? min(cap, u - pass * cap) : 0u;
             uint32_t st[kLanes], own[kLanes], fin[kLanes];
+            uint32_t dw[4] = {0, 0, 0, 0};
+            if (single && !surv) {  // rows of stride 8 when rs == 8: the domain in one 16-byte load
+                const uint4 r4 = __ldg(reinterpret_cast<const uint4 *>(T.dom_list + (uint64_t)dom * 8));
+                dw[0] = r4.x; dw[1] = r4.y; dw[2] = r4.z; dw[3] = r4.w;
+            }
 #pragma unroll
             for (int l = 0; l < kLanes; l++) {
                 const uint32_t r = pass * cap + l;
                 if ((uint32_t)l < nl) {
-                    st[l] = tab.enc(surv ? surv[i * kLanes + r] : T.dom_list[(uint64_t)dom * T.imax + r]);
+                    const uint32_t q = single && !surv ? (dw[l >> 1] >> (16 * (l & 1))) & 0xFFFFu
+                                                      : (surv ? surv[i * kLanes + r] : T.dom_list[(uint64_t)dom * T.rs + r]);
+                    st[l] = tab.enc(q);
                     own[l] = l;
                 } else {
                     st[l] = tab.enc(0);
@@ -685,7 +695,7 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
         const uint32_t dom = sub_domain(T, p, in, i, start);
         const uint32_t u = T.dom_size[dom];
         for (uint32_t e = lane; e < u; e += 32) {
-            pool_s[e] = T.dom_list[(uint64_t)dom * T.imax + e];
+            pool_s[e] = T.dom_list[(uint64_t)dom * T.rs + e];
             pool_id[e] = (uint16_t)e;
             parent[e] = (uint16_t)e;
             res[e] = kNone;
@@ -1300,7 +1310,7 @@ __device__ __forceinline__ LMap cta_tree_fold(uint16_t *rows, uint16_t *doms, ui
 
 // A rank-space entry as a state: rank codes index the next map's domain nd.
 __device__ __forceinline__ uint32_t decode_entry(const DevTables &T, uint32_t v, uint32_t nd) {
-    return is_rank(v) ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.imax + (v - kRank)) : v;
+    return is_rank(v) ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.rs + (v - kRank)) : v;
 }
 
 // leaf_fold_kernel: one level of leaf reduction for long chunks: the leaves of
@@ -1437,7 +1447,7 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
                 lv[q] = t0 + q < nk ? (uint32_t)__ldcg(leaves + (uint64_t)(a + t0 + q) * 8 + j) : kNone;
             if (t0 == 0 && has) {
                 // decode and user-order rows, loaded while the leaves are in flight
-                if (k + 1 < P) dl = __ldg(T.dom_list + (uint64_t)nd * T.imax + j);
+                if (k + 1 < P) dl = __ldg(T.dom_list + (uint64_t)nd * T.rs + j);
                 if (d0 < T.nclass) {
                     du = T.dom_user_size[d0];
                     if (j < T.imax_user) xl = T.xlat[(uint64_t)d0 * T.imax_user + j];
@@ -1614,7 +1624,7 @@ __global__ void __launch_bounds__(256) lookahead_kernel(DevTables T, const uint8
             uint32_t st = 0;
             bool keep = false;
             if (j < du) {
-                st = T.dom_list[(uint64_t)c * T.imax + T.xlat[(uint64_t)c * imu + j]];
+                st = T.dom_list[(uint64_t)c * T.rs + T.xlat[(uint64_t)c * imu + j]];
                 keep = (bm[st >> 5] >> (st & 31)) & 1u;
             }
             const uint32_t mask = __ballot_sync(0xffffffffu, keep);

@@ -29,7 +29,7 @@ struct DevTables {
     uint32_t image_words;
     const uint16_t *gtable;     // [nq][256] byte-indexed table (global)
     const uint8_t *byte_class;  // [256]
-    const uint16_t *dom_list;   // [(nclass+1) * imax] internal I_sigma, ascending
+    const uint16_t *dom_list;   // [(nclass+1) * rs] internal I_sigma, ascending, rows padded 0xFFFF
     const uint16_t *dom_size;   // [nclass+1]
     const uint16_t *rank;       // [(nclass+1) * nq] index in dom_list or 0xFFFF
     const uint8_t *rank8;       // same as uint8 (0xFF = none) when imax < 255, else null
