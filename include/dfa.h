@@ -144,8 +144,15 @@ dfa_status dfa_match(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, voi
 
 /*
  * dfa_match_host: the same call for an input in HOST memory (pinned for
- * full speed): copies it to the device inside the call, overlapping the
- * copy of piece i+1 with the matching of piece i, then synchronises.
+ * full speed; the handle keeps a device copy buffer of len bytes).  Inputs
+ * longer than one piece (DFA_OPT_HOST_PIECE, default 32 MiB) are pipelined:
+ * piece g+1 is copied on an internal stream while piece g is matched on
+ * `stream` as a segment map (dfa_segment_map) folded into the running state.
+ * Early exit (DFA_OPT_EARLY_EXIT, default on): once
+ * a finished piece leaves the run in a state that absorbs every byte (an
+ * absorbing accept of a suffix-closed language, or an error state), the
+ * remaining pieces are neither copied nor matched -- the result cannot
+ * change.  Synchronises `stream`; dfa_get_stats().host_bytes = bytes copied.
  */
 dfa_status dfa_match_host(dfa_handle_t h, const uint8_t *host_input, uint64_t len, void *stream,
                           uint16_t *final_state, int *accept);
@@ -231,9 +238,11 @@ enum {
     DFA_OPT_WARP_COMPOSE = 7,    /* 1 (default): maps of <= 8 entries composed in rank space: in the match
                                     kernel's warps, leaf_fold_kernel and compose8_kernel; 0: tree path */
     DFA_OPT_GRAPHS = 8,          /* 1 (default): replay a CUDA graph when a dfa_chunk_maps call repeats */
-    DFA_OPT_MAX_LANES = 9        /* lanes per thread in the match kernel, 1..8 (default 8): converge_kernel
+    DFA_OPT_MAX_LANES = 9,       /* lanes per thread in the match kernel, 1..8 (default 8): converge_kernel
                                     runs until at most this many lanes survive; larger domains without
                                     the converge stage take several passes */
+    DFA_OPT_HOST_PIECE = 10,     /* dfa_match_host piece size in bytes (>= 1 MiB, default 32 MiB) */
+    DFA_OPT_EARLY_EXIT = 11      /* 1 (default): dfa_match_host stops at an absorbing running state */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 
@@ -250,6 +259,7 @@ typedef struct {
     uint32_t profiled;         /* calls accumulated in kernel_ms */
     float kernel_ms[8];        /* summed section durations (DFA_OPT_PROFILE) */
     char kernel_name[8][32];
+    uint64_t host_bytes;       /* bytes dfa_match_host copied to the device in its last call */
 } dfa_stats;
 dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out);
 

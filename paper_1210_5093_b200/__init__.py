@@ -35,6 +35,8 @@ DFA_OPT_FOLD_IN_TREE = 6
 DFA_OPT_WARP_COMPOSE = 7
 DFA_OPT_GRAPHS = 8
 DFA_OPT_MAX_LANES = 9
+DFA_OPT_HOST_PIECE = 10
+DFA_OPT_EARLY_EXIT = 11
 TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16"}
 
 
@@ -48,7 +50,7 @@ class DfaStats(ctypes.Structure):
     _fields_ = [("input_bytes", ctypes.c_uint64), ("num_subchunks", ctypes.c_uint64),
                 ("num_kernels", ctypes.c_uint32),
                 ("profiled", ctypes.c_uint32), ("kernel_ms", ctypes.c_float * 8),
-                ("kernel_name", (ctypes.c_char * 32) * 8)]
+                ("kernel_name", (ctypes.c_char * 32) * 8), ("host_bytes", ctypes.c_uint64)]
 
 
 class DfaError(RuntimeError):
@@ -265,7 +267,7 @@ def dfa_get_stats(h) -> dict:
     s = DfaStats()
     _ck(lib().dfa_get_stats(h, ctypes.byref(s)), "dfa_get_stats")
     d = {"input_bytes": s.input_bytes, "num_subchunks": s.num_subchunks,
-         "num_kernels": s.num_kernels, "profiled_calls": s.profiled}
+         "num_kernels": s.num_kernels, "profiled_calls": s.profiled, "host_bytes": s.host_bytes}
     if s.profiled:
         d["kernel_ms"] = {bytes(s.kernel_name[i]).split(b"\0")[0].decode(): s.kernel_ms[i]
                           for i in range(8) if s.kernel_name[i][0]}

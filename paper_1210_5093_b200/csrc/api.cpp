@@ -93,6 +93,13 @@ struct dfa_handle {
     int open_section = -1;
     cudaEvent_t open_event = nullptr;
     std::vector<Rec> graph_recs;
+    // dfa_match_host pipeline: pieces copied on copy_stream, matched on the caller's
+    uint64_t host_piece = 32ull << 20;
+    int early_exit = 1;
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> hm_ev;  // [2 * pieces]: copied, done
+    DevBuf hm_rows, hm_bounds, hm_la, hm_final;
+    HostPinned h_hm;
 };
 
 namespace {
@@ -768,6 +775,10 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         for (auto &gr : h->graph_recs) { cudaEventDestroy(gr.a); cudaEventDestroy(gr.b); }
         if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
         for (auto &e : h->ev_pool) if (e) cudaEventDestroy(e);
+        if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
+        for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
+        for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final}) b->release();
+        h->h_hm.release();
     }
     delete h;
     return DFA_OK;
@@ -864,8 +875,100 @@ dfa_status dfa_match_host(dfa_handle_t h, const uint8_t *host_input, uint64_t le
     if (len == 0) return dfa_match(h, nullptr, 0, stream, final_state, accept);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     CK(h->input.ensure(len));
-    CK(cudaMemcpyAsync(h->input.p, host_input, len, cudaMemcpyHostToDevice, s));
-    return dfa_match(h, h->input.as<uint8_t>(), len, stream, final_state, accept);
+    const uint64_t piece = h->host_piece;
+    const uint32_t G = (uint32_t)((len + piece - 1) / piece);
+    if (G == 1) {
+        h->stats.host_bytes = len;
+        CK(cudaMemcpyAsync(h->input.p, host_input, len, cudaMemcpyHostToDevice, s));
+        return dfa_match(h, h->input.as<uint8_t>(), len, stream, final_state, accept);
+    }
+    // Pieces g = 0..G-1: piece g is copied on copy_stream while piece g-1 is
+    // matched on s as a segment map over I_sigma of the byte before it
+    // (dfa_segment_map), and the rows so far are folded (Eq.SeqReduction) into
+    // the running state, read back per piece.  Early exit: once a finished
+    // piece leaves the run in a state that absorbs every byte, the remaining
+    // pieces cannot change the result and are neither copied nor matched.
+    if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    while (h->hm_ev.size() < 2 * (size_t)G + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->hm_ev.push_back(e);
+    }
+    const uint32_t imu = h->T.imax_user;
+    CK(h->hm_rows.ensure((size_t)G * imu * 2));
+    CK(h->hm_bounds.ensure((size_t)G * 16));
+    CK(h->hm_la.ensure(G));
+    CK(h->hm_final.ensure((size_t)G * 4));
+    const size_t o_la = (size_t)G * 16, o_st = o_la + ((G + 15) & ~15u), o_fin = o_st + (size_t)G * sizeof(DevStatus);
+    CK(h->h_hm.ensure(o_fin + (size_t)G * 4));
+    uint8_t *hp = h->h_hm.as<uint8_t>();
+    // the pinned staging of a previous call may still be in flight
+    CK(cudaStreamSynchronize(s));
+    uint64_t *hb = reinterpret_cast<uint64_t *>(hp);
+    uint8_t *hla = hp + o_la;
+    DevStatus *hst = reinterpret_cast<DevStatus *>(hp + o_st);
+    uint16_t *hfin = reinterpret_cast<uint16_t *>(hp + o_fin);
+    for (uint32_t g = 0; g < G; g++) {
+        const uint64_t off = (uint64_t)g * piece, sz = std::min<uint64_t>(piece, len - off);
+        hb[2 * g] = 0;
+        hb[2 * g + 1] = sz;
+        hla[g] = g ? host_input[off - 1] : 0;
+        if (g && hla[g] >= h->prep.ns) return DFA_ERR_SYMBOL;
+    }
+    CK(cudaMemcpyAsync(h->hm_bounds.p, hb, (size_t)G * 16, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->hm_la.p, hla, G, cudaMemcpyHostToDevice, s));
+    // earlier work on s may still read h->input: the copies start after it
+    CK(cudaEventRecord(h->hm_ev[2 * G], s));
+    CK(cudaStreamWaitEvent(h->copy_stream, h->hm_ev[2 * G], 0));
+    uint16_t *rows = h->hm_rows.as<uint16_t>();
+    uint32_t issued = 0, checked = 0;
+    int exit_piece = -1;
+    uint64_t copied = 0;
+    for (uint32_t g = 0; g < G; g++) {
+        if (h->early_exit && g >= 2) {
+            // at most 3 pieces in flight (copy of g overlaps the match of g-1, g-2), so
+            // that a finished piece's running state is seen while there is input left
+            if (g >= 3) CK(cudaEventSynchronize(h->hm_ev[2 * (g - 3) + 1]));
+            // pieces finish in order on s: look at the newly finished ones
+            while (checked + 1 < g && cudaEventQuery(h->hm_ev[2 * checked + 1]) == cudaSuccess) {
+                const uint32_t q = hfin[2 * checked];
+                if (q < h->prep.nq && h->prep.absorbing[q]) { exit_piece = (int)checked; break; }
+                checked++;
+            }
+            if (exit_piece >= 0) break;
+        }
+        const uint64_t off = (uint64_t)g * piece, sz = std::min<uint64_t>(piece, len - off);
+        CK(cudaMemcpyAsync(h->input.as<uint8_t>() + off, host_input + off, sz, cudaMemcpyHostToDevice,
+                           h->copy_stream));
+        copied += sz;
+        CK(cudaEventRecord(h->hm_ev[2 * g], h->copy_stream));
+        CK(cudaStreamWaitEvent(s, h->hm_ev[2 * g], 0));
+        const uint64_t hb2[2] = {0, sz};
+        const Split sp = plan_split(h, sz, 1, hb2, false);
+        Outputs o;
+        o.first_dom = g ? h->prep.byte_class[hla[g]] : h->T.start_dom;
+        o.user_row0 = rows + (size_t)g * imu;
+        st = run(h, h->input.as<uint8_t>() + off, sz, 1, h->hm_bounds.as<uint64_t>() + 2 * g, sp, s, o);
+        if (st != DFA_OK) return st;
+        CK(cudaMemcpyAsync(hst + g, h->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+        CK(launch_fold_segments(h->T, rows, h->hm_la.as<uint8_t>(), g + 1, h->status.as<DevStatus>(),
+                                h->hm_final.as<uint16_t>() + 2 * g, s));
+        CK(cudaMemcpyAsync(hfin + 2 * g, h->hm_final.as<uint16_t>() + 2 * g, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(h->hm_ev[2 * g + 1], s));
+        issued = g + 1;
+    }
+    CK(cudaStreamSynchronize(s));
+    h->last_stream = s;
+    h->stats.host_bytes = copied;
+    const uint32_t last = exit_piece >= 0 ? (uint32_t)exit_piece : issued - 1;
+    uint32_t err = 0;
+    for (uint32_t g = 0; g <= last; g++) err = std::max(err, hst[g].err);
+    if (err) return (dfa_status)err;
+    *final_state = hfin[2 * last];
+    *accept = (int)hfin[2 * last + 1];
+    if (*final_state == h->prep.poison) return DFA_ERR_SYMBOL;
+    return DFA_OK;
 }
 
 dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks, void *stream,
@@ -1012,6 +1115,11 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
     if (!h) return DFA_ERR_ARG;
     switch (key) {
     case DFA_OPT_SUBCHUNK_TARGET: if (value < 0) return DFA_ERR_ARG; h->subchunk_target = value; return DFA_OK;
+    case DFA_OPT_HOST_PIECE:
+        if (value < (1 << 20)) return DFA_ERR_ARG;
+        h->host_piece = (uint64_t)value;
+        return DFA_OK;
+    case DFA_OPT_EARLY_EXIT: h->early_exit = value ? 1 : 0; return DFA_OK;
     case DFA_OPT_MAX_LANES:
         if (value < 1 || value > kLanes) return DFA_ERR_ARG;
         h->max_lanes = (int)value;

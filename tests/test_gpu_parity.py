@@ -515,3 +515,48 @@ def test_max_lanes(name, cap):
     x = w.input(min(w.small_n, 1 << 19))
     c = Case(w.automaton, x, name)
     check_chunk_maps(c, 129, opts={D.DFA_OPT_MAX_LANES: cap})
+
+
+# ------------------------------------------------------------------ dfa_match_host pipeline + early exit (N4)
+@pytest.mark.parametrize("name", ["random", "keyword", "protein", "tiny"])
+@pytest.mark.parametrize("early", [0, 1])
+def test_match_host_pipelined(name, early):
+    """Pieces of 1 MiB (the last ragged): same final/accept as the oracle; with early
+    exit the bytes copied stop once the running state absorbs every byte."""
+    w = W.get(name)
+    x = w.input((5 << 20) + 12345)
+    c = Case(w.automaton, x, name)
+    d = c.handle({D.DFA_OPT_HOST_PIECE: 1 << 20, D.DFA_OPT_EARLY_EXIT: early})
+    try:
+        pinned = torch.from_numpy(x).pin_memory()
+        fin, acc = D.dfa_match_host(d.h, pinned)
+        ofin = c.od.run(x)
+        assert (fin, acc) == (ofin, bool(c.a.accepting[ofin]))
+        copied = D.dfa_get_stats(d.h)["host_bytes"]
+        assert copied <= x.size
+        if not early:
+            assert copied == x.size
+    finally:
+        d.close()
+
+
+def test_match_host_early_exit_stops():
+    """Keyword DFA (absorbing accept): a keyword in the first piece ends the copy early;
+    a bad-free input without keywords is copied whole."""
+    w = W.get("keyword")
+    a = w.automaton
+    kw = np.frombuffer(w.info["keywords"][0].encode("latin1"), np.uint8)
+    x = np.full((8 << 20) + 7, 0x20, np.uint8)  # spaces: no keyword
+    c = Case(a, x, "kw-none")
+    d = c.handle({D.DFA_OPT_HOST_PIECE: 1 << 20})
+    try:
+        fin, acc = D.dfa_match_host(d.h, x)
+        assert (fin, acc) == (c.od.run(x), bool(a.accepting[c.od.run(x)]))
+        assert D.dfa_get_stats(d.h)["host_bytes"] == x.size
+        y = x.copy()
+        y[1000:1000 + kw.size] = kw
+        fin, acc = D.dfa_match_host(d.h, y)
+        assert acc and fin == c.od.run(y)
+        assert D.dfa_get_stats(d.h)["host_bytes"] < y.size
+    finally:
+        d.close()
