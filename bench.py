@@ -59,6 +59,7 @@ def parse():
                     help="per-kernel CUDA events inside the timed loop (inline) or in a second loop of the same K steps")
     ap.add_argument("--alg2", action="store_true",
                     help="N2 ablation: match every sub-chunk from all of Q minus Z (Alg.2, P:753-790)")
+    ap.add_argument("--no-batch", action="store_true", help="skip the multi-input batch (N4) report")
     ap.add_argument("--no-lookahead", action="store_true", help="skip the r-symbol lookahead (N1) report")
     ap.add_argument("--quiet-json", action="store_true", help="print a one-line summary instead of JSON")
     return ap.parse_args()
@@ -285,6 +286,31 @@ def main():
                                  "mean_pct_of_Q": 100.0 * float(sz.mean()) / a.nq,
                                  "kernel_ms": la0.elapsed_time(la1)}
 
+    # N4 multi-input batching: many short inputs (the first n bytes cut into 1 KiB records),
+    # one dfa_match_batch call per step, device-resident
+    batch = None
+    if world == 1 and not args.no_batch:
+        rec = 1024
+        cnt = min(n // rec, 1 << 18)
+        offs = np.arange(cnt + 1, dtype=np.uint64) * rec
+        bfin = torch.empty(cnt, dtype=torch.int16, device=dev)
+        bacc = torch.empty(cnt, dtype=torch.uint8, device=dev)
+        for _ in range(3):
+            D.dfa_match_batch(d.h, dx, offs, bfin, bacc, stream=stream)
+        torch.cuda.synchronize(dev)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bsteps = 20
+        b0.record(stream)
+        for _ in range(bsteps):
+            D.dfa_match_batch(d.h, dx, offs, bfin, bacc, stream=stream)
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        if D.dfa_get_last_device_error(d.h) != 0:
+            raise SystemExit("device error in dfa_match_batch")
+        bms = b0.elapsed_time(b1) / bsteps
+        batch = {"api": "dfa_match_batch", "inputs": cnt, "bytes_each": rec, "ms_per_call": bms,
+                 "GB/s": cnt * rec / (bms * 1e-3) / 1e9, "inputs_per_s": cnt / (bms * 1e-3)}
+
     if rank != 0:
         dist.barrier() if dist else None
         return 0
@@ -357,6 +383,8 @@ def main():
     }
     if look:
         line["lookahead"] = look
+    if batch:
+        line["batch"] = batch
     if not args.no_cpu_baseline and world == 1:
         import oracle
         od = oracle.Dfa(a.table, a.q0, a.accepting)
@@ -375,6 +403,9 @@ def main():
     if args.quiet_json:
         print(f"{args.config}{' alg2' if args.alg2 else ''} {' '.join(args.opt)} value={value:.1f} GB/s ms={ms:.4f} "
               f"kernels={ {k: round(v, 4) for k, v in line['kernels_ms_per_step'].items()} }")
+        if batch:
+            print(f"  batch: {batch['inputs']} x {batch['bytes_each']} B in {batch['ms_per_call']:.4f} ms = "
+                  f"{batch['GB/s']:.1f} GB/s")
         if look:
             print("  lookahead |I_r| mean/max:", {r: (round(v["mean_domain"], 2), v["max_domain"])
                                                    for r, v in look["r"].items()})

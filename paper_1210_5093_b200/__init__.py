@@ -22,7 +22,7 @@ __all__ = [
     "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
     "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
     "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
-    "dfa_lookahead_maps", "Dfa", "lib", "EXPORTED",
+    "dfa_lookahead_maps", "dfa_match_batch", "Dfa", "lib", "EXPORTED",
 ]
 
 DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
@@ -65,7 +65,7 @@ EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_d
             "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
             "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
             "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
-            "dfa_lookahead_maps"]
+            "dfa_lookahead_maps", "dfa_match_batch"]
 
 _lib = None
 
@@ -97,6 +97,7 @@ def lib():
             "dfa_segment_map": [V, V, u64, ctypes.c_int32, V, V],
             "dfa_fold_segments": [V, V, V, u32, V, V],
             "dfa_lookahead_maps": [V, V, u64, u32, V, V, u32, V, V, V, V],
+            "dfa_match_batch": [V, V, V, u32, V, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -239,6 +240,14 @@ def dfa_lookahead_maps(h, dev_input, P: int, dev_bounds, dev_maps, r: int, dev_d
     _ck(lib().dfa_lookahead_maps(h, _ptr(dev_input), n, int(P), _ptr(dev_bounds), _ptr(dev_maps), int(r),
                                  _stream(stream), _ptr(dev_domains), _ptr(dev_domain_sizes), _ptr(dev_maps_r)),
         "dfa_lookahead_maps")
+
+
+def dfa_match_batch(h, dev_data, offsets, dev_final, dev_accept, stream=None):
+    """Independent inputs dev_data[offsets[j]:offsets[j+1]] (offsets: host uint64 array of
+    count+1 entries) matched from q0; finals -> dev_final (uint16), accept -> dev_accept (uint8)."""
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+    _ck(lib().dfa_match_batch(h, _ptr(dev_data), off.ctypes.data, int(off.size - 1), _stream(stream),
+                              _ptr(dev_final), _ptr(dev_accept)), "dfa_match_batch")
 
 
 def dfa_segment_map(h, dev_input, lookahead: int, dev_row, n: Optional[int] = None, stream=None):

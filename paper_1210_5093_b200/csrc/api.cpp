@@ -100,6 +100,11 @@ struct dfa_handle {
     std::vector<cudaEvent_t> hm_ev;  // [2 * pieces]: copied, done
     DevBuf hm_rows, hm_bounds, hm_la, hm_final;
     HostPinned h_hm;
+    // reporting rows of the last run (batch outputs read them)
+    const uint16_t *rep_rows = nullptr;
+    uint32_t rep_rs = 8;
+    DevBuf batch_bounds, batch_kidx;
+    HostPinned h_batch;
 };
 
 namespace {
@@ -328,6 +333,7 @@ struct Outputs {
     uint16_t *user_maps = nullptr;   // [(P-1) * imax_user]
     uint16_t *starts = nullptr;      // [P]
     uint16_t *final2 = nullptr;      // [2]
+    bool indep = false;              // batch: chunks are independent inputs, no fold
 };
 
 int lanes_threads(const dfa_handle *h) {
@@ -421,7 +427,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     h->last_stream = s;
     CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
-              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in};
+              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in, o.indep ? 1u : 0u};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;
@@ -513,6 +519,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
             CK(cudaMemsetAsync(h->ticket.p, 0, 256, s));
         }
         uint16_t *rep_rows = h->lvlA.as<uint16_t>(), *rep_doms = h->domA.as<uint16_t>();
+        h->rep_rows = rep_rows;
+        h->rep_rs = 8;
         CK(launch_compose8(T, lrows, ldom, L0, Lm, P, cpc, rep_rows,
                            rep_doms, o.user_maps, o.user_row0, o.chunk0_end, h->fold_rows.as<uint16_t>(),
                            h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(), h->status.as<DevStatus>(), o.final2,
@@ -556,12 +564,12 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         tr.rep_level = L;
         // short rows: the fold above the reporting chunks is fold_rows_kernel
         // (whole CTAs, pairwise in shared memory); long rows: more tree levels
-        use_fold_rows = T.rs <= 16 && P > 1 && !h->fold_in_tree;
+        use_fold_rows = T.rs <= 16 && P > 1 && !h->fold_in_tree && !o.indep;
         Sh fold{P, 0, 1};
-        while (!overflow && !use_fold_rows && fold.f > 1) fold = add(fold, F);
+        while (!overflow && !use_fold_rows && !o.indep && fold.f > 1) fold = add(fold, F);
         if (overflow || total >= (1ull << 31) || NS >= (1ull << 31)) return DFA_ERR_INTERNAL;
         tr.nlevels = L;
-        tr.root_final = use_fold_rows ? 0 : 1;
+        tr.root_final = use_fold_rows || o.indep ? 0 : 1;
         tr.lrs = tree_lrs(T);
         CK(h->lvlA.ensure(total * T.rs * 2));
         CK(h->domA.ensure(total * 2));
@@ -626,6 +634,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         }
         prof_end(h, s);
     }
+    h->rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
+    h->rep_rs = T.rs;
     if (o.starts) {
         const uint16_t *rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
         CK(launch_starts(T, plan, rep_rows, rep_rows + T.rs, tr.doms + tr.lv[tr.rep_level].off, o.starts,
@@ -777,8 +787,10 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         for (auto &e : h->ev_pool) if (e) cudaEventDestroy(e);
         if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
         for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
-        for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final}) b->release();
+        for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx})
+            b->release();
         h->h_hm.release();
+        h->h_batch.release();
     }
     delete h;
     return DFA_OK;
@@ -1046,6 +1058,56 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
     o.final2 = dev_final;
     const Split sp = plan_split(h, len, P, hb.data(), true);
     return run(h, dev_input, len, P, dev_bounds_in, sp, s, o);
+}
+
+dfa_status dfa_match_batch(dfa_handle_t h, const uint8_t *dev_data, const uint64_t *host_offsets, uint32_t count,
+                           void *stream, uint16_t *dev_final, uint8_t *dev_accept) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    if (count == 0) return DFA_OK;
+    if (!host_offsets || !dev_final || !dev_accept) return DFA_ERR_ARG;
+    for (uint32_t j = 0; j < count; j++)
+        if (host_offsets[j + 1] < host_offsets[j]) return DFA_ERR_ARG;
+    const uint64_t base = host_offsets[0], n = host_offsets[count] - base;
+    if (n && !dev_data) return DFA_ERR_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // the non-empty inputs are the reporting chunks of one partition of [base, base + n)
+    if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
+    CK(h->h_batch.ensure((size_t)(count + 1) * 8 + (size_t)count * 4 + 64));
+    CK(cudaStreamSynchronize(s));  // the pinned staging of a previous call may still be in flight
+    uint64_t *hb = h->h_batch.as<uint64_t>();
+    int32_t *hk = reinterpret_cast<int32_t *>(hb + count + 1);
+    uint32_t P = 0;
+    hb[0] = 0;
+    for (uint32_t j = 0; j < count; j++) {
+        if (host_offsets[j + 1] > host_offsets[j]) {
+            hk[j] = (int32_t)P++;
+            hb[P] = host_offsets[j + 1] - base;
+        } else {
+            hk[j] = -1;
+        }
+    }
+    CK(h->batch_kidx.ensure((size_t)count * 4));
+    CK(cudaMemcpyAsync(h->batch_kidx.p, hk, (size_t)count * 4, cudaMemcpyHostToDevice, s));
+    h->last_stream = s;
+    if (P == 0) {
+        CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
+        CK(launch_batch_out(h->T, nullptr, 8, h->batch_kidx.as<int32_t>(), count, dev_final, dev_accept,
+                            h->status.as<DevStatus>(), s));
+        return DFA_OK;
+    }
+    CK(h->batch_bounds.ensure((size_t)(P + 1) * 8));
+    CK(cudaMemcpyAsync(h->batch_bounds.p, hb, (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
+    // many inputs: one sub-chunk each (the batch itself is the parallelism); few: split them
+    const Split sp = plan_split(h, n, P, hb, P >= 4096);
+    Outputs o;
+    o.indep = true;
+    st = run(h, dev_data + base, n, P, h->batch_bounds.as<uint64_t>(), sp, s, o);
+    if (st != DFA_OK) return st;
+    CK(launch_batch_out(h->T, h->rep_rows, h->rep_rs, h->batch_kidx.as<int32_t>(), count, dev_final, dev_accept,
+                        h->status.as<DevStatus>(), s));
+    h->stats.num_kernels++;
+    return DFA_OK;
 }
 
 dfa_status dfa_lookahead_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,

@@ -83,9 +83,15 @@ __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s
 
 // Reverse lookahead: the domain of sub-chunk i is I_sigma with
 // sigma the byte before it; the very first sub-chunk starts from {q0}.
+__device__ __forceinline__ bool chunk_first_sub(const Plan &p, uint64_t i) {
+    return i == 0 || (i >= p.m0 && (i - p.m0) % p.m == 0);
+}
+
 __device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const Plan &p, const uint8_t *in, uint64_t i,
                                                uint64_t start) {
-    return i == 0 ? p.first_dom : (uint32_t)T.byte_class[__ldg(in + start - 1)];
+    if (i == 0) return p.first_dom;
+    if (p.indep && chunk_first_sub(p, i)) return T.start_dom;  // batch: every input starts at q0
+    return (uint32_t)T.byte_class[__ldg(in + start - 1)];
 }
 
 // ---------------------------------------------------------------------------
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
             // rank space: final states as ranks in the next sub-chunk's domain
             // I_sigma, sigma = this sub-chunk's last byte (absolute for error
             // states and for the input's last sub-chunk)
-            if (i + 1 < p.NS) {
+            if (i + 1 < p.NS && !(p.indep && chunk_first_sub(p, i + 1))) {
                 // rank = position in the next domain's row (<= 8 entries, one 16-byte load)
                 const uint32_t nd = T.byte_class[__ldg(in + end - 1)];
                 const uint4 nr = __ldg(reinterpret_cast<const uint4 *>(T.dom_list + (uint64_t)nd * 8));
@@ -1554,6 +1560,24 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
 }
 
 // ---------------------------------------------------------------------------
+// batch_out_kernel (dfa_match_batch): input j's final state is entry 0 of its
+// reporting map over {q0} (absolute: its last sub-chunk ends in states); empty
+// inputs (kidx < 0) end in q0.
+// ---------------------------------------------------------------------------
+__global__ void batch_out_kernel(DevTables T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,
+                                 uint32_t count, uint16_t *dev_final, uint8_t *dev_accept, DevStatus *status) {
+    pdl_wait();
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+        const int32_t k = kidx[j];
+        uint32_t q = k < 0 ? T.q0 : rep_rows[(uint64_t)k * rs];
+        if (q >= T.nq || is_rank(q)) { atomicMax(&status->err, 8u); q = T.q0; }
+        if (q == T.poison) atomicMax(&status->err, 5u);
+        dev_final[j] = (uint16_t)q;
+        dev_accept[j] = (uint8_t)test_bit(T.accept_bits, q);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // fold_segments_kernel: the top of the multi-GPU merge (the
 // master step of Fig.Merge): segment g's map is a row over the
 // user's I_sigma of lookahead byte lookahead[g] (segment 0: over {q0});
@@ -1866,6 +1890,13 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,
+                             uint32_t count, uint16_t *dev_final, uint8_t *dev_accept, DevStatus *st, cudaStream_t s) {
+    const uint32_t grid = std::min<uint32_t>((count + 255) / 256, 1024);
+    return launch_pdl(batch_out_kernel, dim3(std::max<uint32_t>(grid, 1)), dim3(256), 0, s, T, rep_rows, rs, kidx,
+                      count, dev_final, dev_accept, st);
 }
 
 cudaError_t launch_leaf_fold(const uint16_t *in_rows, const uint16_t *in_dom, uint32_t L0, uint32_t L, uint32_t P,

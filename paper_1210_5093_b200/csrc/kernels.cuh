@@ -60,6 +60,7 @@ struct Plan {
     const uint64_t *bounds;  // device [P+1]
     uint32_t first_dom;      // domain of sub-chunk 0: start_dom ({q0}) or a lookahead class
     uint64_t in_addr;        // device address of the input (split alignment)
+    uint32_t indep;          // batch: every chunk is an independent input matched from q0
 };
 
 struct DevStatus {
@@ -154,6 +155,8 @@ const void *tree_fn();
 cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row0, const uint16_t *rows,
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s);
 cudaError_t setup_kernel_attributes(const DevTables &T);
+cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,
+                             uint32_t count, uint16_t *dev_final, uint8_t *dev_accept, DevStatus *st, cudaStream_t s);
 cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
                                  DevStatus *st, uint16_t *dev_final, cudaStream_t s);
 int probe_dynamic_smem_base(uint32_t *dev_scratch);

@@ -560,3 +560,41 @@ def test_match_host_early_exit_stops():
         assert D.dfa_get_stats(d.h)["host_bytes"] < y.size
     finally:
         d.close()
+
+
+# ------------------------------------------------------------------ dfa_match_batch (N4 multi-input batching)
+def check_batch(c: Case, lengths, seed=0):
+    rng = np.random.default_rng(seed)
+    ns = c.a.table.shape[1]
+    offs = np.concatenate([[0], np.cumsum(lengths)]).astype(np.uint64)
+    data = rng.integers(0, ns, int(offs[-1]) + 1).astype(np.uint8)
+    d = c.handle()
+    try:
+        dd = torch.from_numpy(data).to(DEV)
+        fin = torch.empty(len(lengths), dtype=torch.int16, device=DEV)
+        acc = torch.empty(len(lengths), dtype=torch.uint8, device=DEV)
+        D.dfa_match_batch(d.h, dd, offs, fin, acc)
+        torch.cuda.synchronize()
+        assert D.dfa_get_last_device_error(d.h) == 0
+        gf, ga = u16(fin), acc.cpu().numpy()
+        for j in range(len(lengths)):
+            x = data[int(offs[j]):int(offs[j + 1])]
+            of = c.od.run(x)
+            assert gf[j] == of and ga[j] == int(c.a.accepting[of]), f"input {j} (len {x.size})"
+    finally:
+        d.close()
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_match_batch_many_small(name):
+    w = W.get(name)
+    rng = np.random.default_rng(5)
+    lengths = rng.integers(0, 700, 5000)
+    lengths[rng.random(5000) < 0.05] = 0
+    check_batch(Case(w.automaton, np.zeros(1, np.uint8), name), lengths)
+
+
+@pytest.mark.parametrize("name", ["random", "protein", "worst"])
+def test_match_batch_few_large(name):
+    w = W.get(name)
+    check_batch(Case(w.automaton, np.zeros(1, np.uint8), name), [300000, 0, 1, 123457, 65536], seed=2)
