@@ -292,7 +292,7 @@ def main():
     if world == 1 and not args.no_batch:
         rec = 1024
         cnt = min(n // rec, 1 << 18)
-        offs = np.arange(cnt + 1, dtype=np.uint64) * rec
+        offs = torch.arange(cnt + 1, dtype=torch.int64, device=dev) * rec
         bfin = torch.empty(cnt, dtype=torch.int16, device=dev)
         bacc = torch.empty(cnt, dtype=torch.uint8, device=dev)
         for _ in range(3):

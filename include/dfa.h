@@ -183,18 +183,22 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
 /*
  * dfa_match_batch: many independent inputs in one pass (multi-input
  * batching; the paper packs inputs and automata into one SBase/IBase layout,
- * P:1430-1440).  Input j is dev_data[host_offsets[j] .. host_offsets[j+1])
- * (device bytes; host_offsets is a HOST array of count+1 non-decreasing
- * offsets), each matched from q0 as its own membership test (Alg.seqmatch).
- * Writes dev_final[j] (uint16 final state) and dev_accept[j] (uint8 0/1),
- * device arrays of count entries.  Empty inputs give (q0, F[q0]).  Inside,
- * the non-empty inputs are the reporting chunks of one partition whose
- * chunks all start from {q0} (no speculation across inputs, no fold).
- * Asynchronous on `stream`; a byte >= |Sigma| is reported by
- * dfa_get_last_device_error.  DFA_ERR_ARG for decreasing offsets.
+ * P:1430-1440).  Input j is dev_data[dev_offsets[j] .. dev_offsets[j+1])
+ * (device bytes, data_len of them; dev_offsets: DEVICE array of count+1
+ * non-decreasing offsets <= data_len), each matched from q0 as its own
+ * membership test (Alg.seqmatch).  Writes dev_final[j] (uint16 final state)
+ * and dev_accept[j] (uint8 0/1), device arrays of count entries; empty inputs
+ * give (q0, F[q0]).  Inside, the inputs are the reporting chunks of one
+ * partition whose chunks all start from {q0} (no speculation across inputs,
+ * no fold).  count >= 4096: fully asynchronous, one sub-chunk per input, bad
+ * offsets are clamped and reported as DFA_ERR_ARG by
+ * dfa_get_last_device_error; count < 4096: the offsets are read back (the
+ * call synchronises `stream` once), validated (DFA_ERR_ARG) and each input is
+ * split for parallelism.  A byte >= |Sigma| is reported by
+ * dfa_get_last_device_error.
  */
-dfa_status dfa_match_batch(dfa_handle_t h, const uint8_t *dev_data, const uint64_t *host_offsets, uint32_t count,
-                           void *stream, uint16_t *dev_final, uint8_t *dev_accept);
+dfa_status dfa_match_batch(dfa_handle_t h, const uint8_t *dev_data, uint64_t data_len, const uint64_t *dev_offsets,
+                           uint32_t count, void *stream, uint16_t *dev_final, uint8_t *dev_accept);
 
 /*
  * dfa_lookahead_maps: multiple reverse lookahead symbols (PAPER.md Sec.

@@ -97,7 +97,7 @@ def lib():
             "dfa_segment_map": [V, V, u64, ctypes.c_int32, V, V],
             "dfa_fold_segments": [V, V, V, u32, V, V],
             "dfa_lookahead_maps": [V, V, u64, u32, V, V, u32, V, V, V, V],
-            "dfa_match_batch": [V, V, V, u32, V, V, V],
+            "dfa_match_batch": [V, V, u64, V, u32, V, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -242,11 +242,12 @@ def dfa_lookahead_maps(h, dev_input, P: int, dev_bounds, dev_maps, r: int, dev_d
         "dfa_lookahead_maps")
 
 
-def dfa_match_batch(h, dev_data, offsets, dev_final, dev_accept, stream=None):
-    """Independent inputs dev_data[offsets[j]:offsets[j+1]] (offsets: host uint64 array of
+def dfa_match_batch(h, dev_data, dev_offsets, dev_final, dev_accept, data_len: Optional[int] = None, stream=None):
+    """Independent inputs dev_data[off[j]:off[j+1]] (dev_offsets: device uint64/int64 tensor of
     count+1 entries) matched from q0; finals -> dev_final (uint16), accept -> dev_accept (uint8)."""
-    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
-    _ck(lib().dfa_match_batch(h, _ptr(dev_data), off.ctypes.data, int(off.size - 1), _stream(stream),
+    n = dev_data.numel() if data_len is None else int(data_len)
+    count = dev_offsets.numel() - 1
+    _ck(lib().dfa_match_batch(h, _ptr(dev_data), n, _ptr(dev_offsets), int(count), _stream(stream),
                               _ptr(dev_final), _ptr(dev_accept)), "dfa_match_batch")
 
 

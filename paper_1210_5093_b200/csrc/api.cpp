@@ -363,9 +363,10 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         if (h->convergence && h->T.imax > (uint32_t)kLanes && lanes_occupancy(h->T, 512) < 2)
             target = target * 5 / 8;
     }
-    const uint64_t len0 = hb[1] - hb[0];
+    // (explicit partitions need no host bounds: one sub-chunk per chunk)
+    const uint64_t len0 = explicit_bounds ? 0 : hb[1] - hb[0];
     uint64_t minlen = len0, avg = len0;
-    if (P > 1) {
+    if (P > 1 && !explicit_bounds) {
         minlen = UINT64_MAX;
         for (uint32_t k = 1; k < P; k++) minlen = std::min(minlen, hb[k + 1] - hb[k]);
         avg = (n - len0) / (P - 1);
@@ -1060,53 +1061,70 @@ dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t 
     return run(h, dev_input, len, P, dev_bounds_in, sp, s, o);
 }
 
-dfa_status dfa_match_batch(dfa_handle_t h, const uint8_t *dev_data, const uint64_t *host_offsets, uint32_t count,
-                           void *stream, uint16_t *dev_final, uint8_t *dev_accept) {
+dfa_status dfa_match_batch(dfa_handle_t h, const uint8_t *dev_data, uint64_t data_len, const uint64_t *dev_offsets,
+                           uint32_t count, void *stream, uint16_t *dev_final, uint8_t *dev_accept) {
     dfa_status st = check_ready(h);
     if (st != DFA_OK) return st;
     if (count == 0) return DFA_OK;
-    if (!host_offsets || !dev_final || !dev_accept) return DFA_ERR_ARG;
-    for (uint32_t j = 0; j < count; j++)
-        if (host_offsets[j + 1] < host_offsets[j]) return DFA_ERR_ARG;
-    const uint64_t base = host_offsets[0], n = host_offsets[count] - base;
-    if (n && !dev_data) return DFA_ERR_ARG;
+    if (!dev_offsets || !dev_final || !dev_accept || (data_len && !dev_data)) return DFA_ERR_ARG;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    // the non-empty inputs are the reporting chunks of one partition of [base, base + n)
+    h->last_stream = s;
+    const uint32_t P = count;
+    Outputs o;
+    o.indep = true;
+    if (count >= 4096) {
+        // many inputs: the batch is the parallelism -- one sub-chunk per input, the
+        // caller's offsets are the partition as they are (empty inputs included), no
+        // host round trip; the kernels clamp offsets to data_len and flag bad ones
+        const Split sp = plan_split(h, data_len, P, nullptr, true);
+        st = run(h, dev_data, data_len, P, dev_offsets, sp, s, o);
+        if (st != DFA_OK) return st;
+        CK(launch_batch_out(h->T, h->rep_rows, h->rep_rs, nullptr, dev_offsets, data_len, count, dev_final,
+                            dev_accept, h->status.as<DevStatus>(), s));
+        h->stats.num_kernels++;
+        return DFA_OK;
+    }
+    // few inputs: read the offsets, drop empty inputs, split each input for parallelism
     if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
-    CK(h->h_batch.ensure((size_t)(count + 1) * 8 + (size_t)count * 4 + 64));
-    CK(cudaStreamSynchronize(s));  // the pinned staging of a previous call may still be in flight
-    uint64_t *hb = h->h_batch.as<uint64_t>();
+    CK(h->h_batch.ensure((size_t)(count + 1) * 8 * 2 + (size_t)count * 4 + 64));
+    uint64_t *ho = h->h_batch.as<uint64_t>();
+    uint64_t *hb = ho + count + 1;
     int32_t *hk = reinterpret_cast<int32_t *>(hb + count + 1);
-    uint32_t P = 0;
+    CK(cudaMemcpyAsync(ho, dev_offsets, (size_t)(count + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t j = 0; j < count; j++)
+        if (ho[j + 1] < ho[j]) return DFA_ERR_ARG;
+    if (ho[count] > data_len) return DFA_ERR_ARG;
+    const uint64_t base = ho[0], n = ho[count] - base;
+    uint32_t Pn = 0;
     hb[0] = 0;
     for (uint32_t j = 0; j < count; j++) {
-        if (host_offsets[j + 1] > host_offsets[j]) {
-            hk[j] = (int32_t)P++;
-            hb[P] = host_offsets[j + 1] - base;
+        if (ho[j + 1] > ho[j]) {
+            hk[j] = (int32_t)Pn++;
+            hb[Pn] = ho[j + 1] - base;
         } else {
             hk[j] = -1;
         }
     }
     CK(h->batch_kidx.ensure((size_t)count * 4));
     CK(cudaMemcpyAsync(h->batch_kidx.p, hk, (size_t)count * 4, cudaMemcpyHostToDevice, s));
-    h->last_stream = s;
-    if (P == 0) {
+    if (Pn == 0) {
         CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
-        CK(launch_batch_out(h->T, nullptr, 8, h->batch_kidx.as<int32_t>(), count, dev_final, dev_accept,
-                            h->status.as<DevStatus>(), s));
-        return DFA_OK;
+        CK(launch_batch_out(h->T, nullptr, 8, h->batch_kidx.as<int32_t>(), nullptr, 0, count, dev_final,
+                            dev_accept, h->status.as<DevStatus>(), s));
+    } else {
+        CK(h->batch_bounds.ensure((size_t)(Pn + 1) * 8));
+        CK(cudaMemcpyAsync(h->batch_bounds.p, hb, (size_t)(Pn + 1) * 8, cudaMemcpyHostToDevice, s));
+        const Split sp = plan_split(h, n, Pn, hb, false);
+        st = run(h, dev_data + base, n, Pn, h->batch_bounds.as<uint64_t>(), sp, s, o);
+        if (st != DFA_OK) return st;
+        CK(launch_batch_out(h->T, h->rep_rows, h->rep_rs, h->batch_kidx.as<int32_t>(), nullptr, 0, count,
+                            dev_final, dev_accept, h->status.as<DevStatus>(), s));
+        h->stats.num_kernels++;
     }
-    CK(h->batch_bounds.ensure((size_t)(P + 1) * 8));
-    CK(cudaMemcpyAsync(h->batch_bounds.p, hb, (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
-    // many inputs: one sub-chunk each (the batch itself is the parallelism); few: split them
-    const Split sp = plan_split(h, n, P, hb, P >= 4096);
-    Outputs o;
-    o.indep = true;
-    st = run(h, dev_data + base, n, P, h->batch_bounds.as<uint64_t>(), sp, s, o);
-    if (st != DFA_OK) return st;
-    CK(launch_batch_out(h->T, h->rep_rows, h->rep_rs, h->batch_kidx.as<int32_t>(), count, dev_final, dev_accept,
-                        h->status.as<DevStatus>(), s));
-    h->stats.num_kernels++;
+    // the pinned staging must outlive the async copies above
+    CK(cudaEventRecord(h->staging_done, s));
+    h->staging_pending = true;
     return DFA_OK;
 }
 

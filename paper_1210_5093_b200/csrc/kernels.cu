@@ -76,7 +76,12 @@ __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s
     uint64_t k, j, mk;
     if (i < p.m0) { k = 0; j = i; mk = p.m0; }
     else { uint64_t t = i - p.m0; k = 1 + t / p.m; j = t % p.m; mk = p.m; }
-    uint64_t b0 = p.bounds[k], b1 = p.bounds[k + 1], len = b1 - b0;
+    uint64_t b0 = p.bounds[k], b1 = p.bounds[k + 1];
+    if (p.indep) {  // caller-given batch offsets: clamp (batch_out_kernel flags bad ones)
+        b0 = min(b0, p.n);
+        b1 = min(max(b1, b0), p.n);
+    }
+    const uint64_t len = b1 - b0;
     s = split_point(p, b0, len, j, mk);
     e = split_point(p, b0, len, j + 1, mk);
 }
@@ -1565,10 +1570,13 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
 // inputs (kidx < 0) end in q0.
 // ---------------------------------------------------------------------------
 __global__ void batch_out_kernel(DevTables T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,
-                                 uint32_t count, uint16_t *dev_final, uint8_t *dev_accept, DevStatus *status) {
+                                 const uint64_t *offsets, uint64_t data_len, uint32_t count, uint16_t *dev_final,
+                                 uint8_t *dev_accept, DevStatus *status) {
     pdl_wait();
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
-        const int32_t k = kidx[j];
+        if (offsets && (offsets[j + 1] < offsets[j] || offsets[j + 1] > data_len))
+            atomicMax(&status->err, 1u);  // DFA_ERR_ARG: decreasing offsets or past data_len
+        const int32_t k = kidx ? kidx[j] : (int32_t)j;
         uint32_t q = k < 0 ? T.q0 : rep_rows[(uint64_t)k * rs];
         if (q >= T.nq || is_rank(q)) { atomicMax(&status->err, 8u); q = T.q0; }
         if (q == T.poison) atomicMax(&status->err, 5u);
@@ -1893,10 +1901,11 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 }
 
 cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,
-                             uint32_t count, uint16_t *dev_final, uint8_t *dev_accept, DevStatus *st, cudaStream_t s) {
+                             const uint64_t *offsets, uint64_t data_len, uint32_t count, uint16_t *dev_final,
+                             uint8_t *dev_accept, DevStatus *st, cudaStream_t s) {
     const uint32_t grid = std::min<uint32_t>((count + 255) / 256, 1024);
     return launch_pdl(batch_out_kernel, dim3(std::max<uint32_t>(grid, 1)), dim3(256), 0, s, T, rep_rows, rs, kidx,
-                      count, dev_final, dev_accept, st);
+                      offsets, data_len, count, dev_final, dev_accept, st);
 }
 
 cudaError_t launch_leaf_fold(const uint16_t *in_rows, const uint16_t *in_dom, uint32_t L0, uint32_t L, uint32_t P,

@@ -156,7 +156,8 @@ cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row
                           const uint16_t *dom, uint16_t *starts, DevStatus *st, cudaStream_t s);
 cudaError_t setup_kernel_attributes(const DevTables &T);
 cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,
-                             uint32_t count, uint16_t *dev_final, uint8_t *dev_accept, DevStatus *st, cudaStream_t s);
+                             const uint64_t *offsets, uint64_t data_len, uint32_t count, uint16_t *dev_final,
+                             uint8_t *dev_accept, DevStatus *st, cudaStream_t s);
 cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
                                  DevStatus *st, uint16_t *dev_final, cudaStream_t s);
 int probe_dynamic_smem_base(uint32_t *dev_scratch);

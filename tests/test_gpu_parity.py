@@ -573,7 +573,7 @@ def check_batch(c: Case, lengths, seed=0):
         dd = torch.from_numpy(data).to(DEV)
         fin = torch.empty(len(lengths), dtype=torch.int16, device=DEV)
         acc = torch.empty(len(lengths), dtype=torch.uint8, device=DEV)
-        D.dfa_match_batch(d.h, dd, offs, fin, acc)
+        D.dfa_match_batch(d.h, dd, torch.from_numpy(offs.astype(np.int64)).to(DEV), fin, acc)
         torch.cuda.synchronize()
         assert D.dfa_get_last_device_error(d.h) == 0
         gf, ga = u16(fin), acc.cpu().numpy()
@@ -598,3 +598,24 @@ def test_match_batch_many_small(name):
 def test_match_batch_few_large(name):
     w = W.get(name)
     check_batch(Case(w.automaton, np.zeros(1, np.uint8), name), [300000, 0, 1, 123457, 65536], seed=2)
+
+
+def test_match_batch_bad_offsets():
+    w = W.get("random")
+    d = Case(w.automaton, np.zeros(1, np.uint8), "random").handle()
+    try:
+        dd = torch.zeros(1000, dtype=torch.uint8, device=DEV)
+        fin = torch.empty(5000, dtype=torch.int16, device=DEV)
+        acc = torch.empty(5000, dtype=torch.uint8, device=DEV)
+        off = torch.arange(5001, dtype=torch.int64, device=DEV) % 1200  # decreasing and past the data
+        D.dfa_match_batch(d.h, dd, off, fin, acc)
+        torch.cuda.synchronize()
+        assert D.dfa_get_last_device_error(d.h) == D.DFA_ERR_ARG
+        bad = torch.tensor([0, 10, 5, 20], dtype=torch.int64, device=DEV)
+        with pytest.raises(D.DfaError):
+            D.dfa_match_batch(d.h, dd, bad, fin, acc)  # few inputs: validated on the host
+        past = torch.tensor([0, 10, 2000], dtype=torch.int64, device=DEV)
+        with pytest.raises(D.DfaError):
+            D.dfa_match_batch(d.h, dd, past, fin, acc)
+    finally:
+        d.close()
