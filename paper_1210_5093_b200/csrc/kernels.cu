@@ -681,7 +681,7 @@ __device__ __forceinline__ uint32_t scratch_u16(const DevTables &T) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) ? 1 : 2) converge_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                        uint16_t *__restrict__ surv, uint8_t *__restrict__ surv_n,
                                                        uint64_t *__restrict__ surv_pos,
                                                        uint16_t *__restrict__ amap, uint32_t cap) {
@@ -737,13 +737,19 @@ __global__ void __launch_bounds__(512) converge_kernel(DevTables T, Plan p, cons
                     const uint32_t e = base + lane + 32 * l;
                     s[l] = tab.enc(e < np ? pool_s[e] : 0);
                 }
-                for (uint32_t k = k0; k < k1; k++) {
-                    const uint32_t wsel = k >> 2;
-                    const uint32_t word = wsel == 0 ? v.x : wsel == 1 ? v.y : wsel == 2 ? v.z : v.w;
-                    const uint32_t b = (word >> (8 * (k & 3))) & 0xFFu;
-                    const typename Tab<MODE>::Pre pb = tab.bpre(b);
+                if (k0 == 0 && k1 == 16) {
+                    // a full aligned window: the match kernel's 16-byte step (static byte
+                    // selection, per-word column preparation)
+                    block16<kConvergeLA, MODE>(tab, v, s);
+                } else {
+                    for (uint32_t k = k0; k < k1; k++) {
+                        const uint32_t wsel = k >> 2;
+                        const uint32_t word = wsel == 0 ? v.x : wsel == 1 ? v.y : wsel == 2 ? v.z : v.w;
+                        const uint32_t b = (word >> (8 * (k & 3))) & 0xFFu;
+                        const typename Tab<MODE>::Pre pb = tab.bpre(b);
 #pragma unroll
-                    for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_pre(s[l], pb);
+                        for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_pre(s[l], pb);
+                    }
                 }
 #pragma unroll
                 for (int l = 0; l < kConvergeLA; l++) {
