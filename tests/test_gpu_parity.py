@@ -619,3 +619,50 @@ def test_match_batch_bad_offsets():
             D.dfa_match_batch(d.h, dd, past, fin, acc)
     finally:
         d.close()
+
+
+def _nccl_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    from paper_1210_5093_b200 import multi_gpu
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        res = []
+        for name in ("random", "protein", "keyword"):
+            w = W.get(name)
+            x = w.input(1 << 20, segment=rank)
+            dx = torch.from_numpy(x).cuda()
+            d = D.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accept_bitmap)
+            smap, fold = multi_gpu.gpu_ops(d, dx)
+            m = multi_gpu.SegmentMatcher(rank, world, dist, dx[-1:], smap, fold)
+            out = m.step()
+            torch.cuda.synchronize()
+            res.append((name, out.cpu().numpy().view(np.uint16).tolist(), D.dfa_get_last_device_error(d.h)))
+            d.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_path_nccl_world1():
+    """The N > 1 bench path (segment map -> NCCL all-gather -> fold) end to end over
+    NCCL on this GPU with world size 1 (one process per GPU; the box has one)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(0, 1, port, q))
+    p.start()
+    rank, res = q.get(timeout=300)
+    p.join(60)
+    for name, fin, err in res:
+        w = W.get(name)
+        od = oracle.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accepting)
+        f = od.run(w.input(1 << 20))
+        assert err == 0 and fin == [f, int(w.automaton.accepting[f])], name
