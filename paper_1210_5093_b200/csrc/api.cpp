@@ -745,18 +745,20 @@ dfa_status dfa_create_ex(const uint16_t *table, uint32_t num_states, uint32_t al
     if (!out) return DFA_ERR_ARG;
     std::unique_ptr<dfa_handle> h(new (std::nothrow) dfa_handle());
     if (!h) return DFA_ERR_OOM;
-    uint32_t budget = 200 * 1024;
+    uint32_t budget = 200 * 1024, rep_budget = 223 * 1024;
     uint32_t u8_limit = 256 - 4;  // dynamic smem starts at shared address 0x400 on sm_100
     if (!(flags & DFA_CREATE_HOST_ONLY)) {
         int dev = 0, optin = 0;
         if (cudaGetDevice(&dev) != cudaSuccess) return DFA_ERR_CUDA;
-        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0)
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0) {
             budget = (uint32_t)optin - 24 * 1024;
+            rep_budget = (uint32_t)optin - 4 * 1024;  // lanes kernel only: table + bitmaps
+        }
         dfa_status ps = probe(h.get(), u8_limit);
         if (ps != DFA_OK) return ps;
     }
     int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, u8_limit, h->prep,
-                     (flags & DFA_CREATE_FULL_DOMAIN) != 0);
+                     (flags & DFA_CREATE_FULL_DOMAIN) != 0, rep_budget);
     if (st != 0) return (dfa_status)st;
     if (!(flags & DFA_CREATE_HOST_ONLY)) {
         dfa_status ds = upload(h.get());
@@ -813,7 +815,7 @@ dfa_status dfa_get_info(dfa_handle_t h, dfa_info *out) {
     i.dead_state = p.first_dead_user;
     i.num_absorbing = p.num_absorbing_user;
     i.table_mode = (uint32_t)p.mode;
-    i.table_bytes = p.mode == kGlobalU16 ? 0 : (uint32_t)(p.image.size() * 4);
+    i.table_bytes = p.mode == kGlobalU16 ? 0 : (uint32_t)(p.image.size() * 4) << rep_log_of(p.mode);
     i.c_num = h->c_num;
     i.c_den = h->c_den;
     i.device_ready = h->device_ready ? 1 : 0;

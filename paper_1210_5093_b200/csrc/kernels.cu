@@ -104,6 +104,22 @@ __device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const Plan &p
 // modes map 4 bytes to 4 columns with two SIMD ops); bprep: per byte, shared
 // by all lanes of a thread; look: per lane, one shared-memory load.
 // ---------------------------------------------------------------------------
+// prmt.b32 with sign-replicate selector nibbles (0xC -> 0x00 for a byte < 0x80);
+// __byte_perm keeps only the low three bits of each nibble.
+__device__ __forceinline__ uint32_t prmt_s(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+
+template <int MODE>
+__host__ __device__ constexpr bool is_rep() { return rep_log_of(MODE) != 0; }
+
+// Words of the table image as laid out in shared memory (R copies for the
+// replicated modes).
+template <int MODE>
+__device__ __forceinline__ uint32_t smem_words(const DevTables &T) { return T.image_words << rep_log_of(MODE); }
+
 template <int MODE>
 struct Tab {
     const uint8_t *t8;
@@ -120,6 +136,14 @@ struct Tab {
     // current input symbol"), with no base add.  Other modes: bias = 0 and
     // one IMAD per lane (state * row bytes + per-byte column address).
     uint32_t bias;
+    // Replicated modes (R = 2^LR copies): the copy of lane l is g = l % R, and
+    // the shared address of entry (s, b) in it is
+    //   (s_enc << (8 + LR)) + K(b),  K(b) = (b & (2^M - 1)) | g << M | (b >> M) << 7,
+    // M = 7 - LR: each 128-byte bank row holds R slices of 2^M bytes, slice g
+    // in banks g*32/R .. (g+1)*32/R - 1.  G = g << M in every byte.
+    static constexpr uint32_t LR = rep_log_of(MODE);
+    static constexpr uint32_t M = 7u - LR;
+    uint32_t G;
 
     struct Pre { uint32_t a, sh; };
 
@@ -134,7 +158,8 @@ struct Tab {
         base4 = T.win_base * 0x01010101u;
         w4 = T.win_w * 0x01010101u;
         tb = (uint32_t)__cvta_generic_to_shared(table_smem);
-        bias = MODE == kIdentU8 ? (tb >> 8) : 0u;
+        bias = MODE == kIdentU8 ? (tb >> 8) : is_rep<MODE>() ? (tb >> (8 + LR)) : 0u;
+        G = is_rep<MODE>() ? (((threadIdx.x & 31u) & ((1u << LR) - 1u)) << M) * 0x01010101u : 0u;
         rowb = MODE == kIdentU16 ? 512u : MODE == kWindowU8 ? T.stride : MODE == kWindowU16 ? 2u * T.stride
              : MODE == kPacked9 ? 4u * T.stride : 0u;
     }
@@ -155,12 +180,26 @@ struct Tab {
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
         return r;
     }
-    __device__ __forceinline__ uint32_t wprep(uint32_t x) const {
+    // replicated modes: K(b) of a raw byte
+    __device__ __forceinline__ uint32_t rep_k(uint32_t b) const {
+        return (b & ((1u << M) - 1u)) | (G & 0xFFu) | ((b >> M) << 7);
+    }
+    __device__ __forceinline__ auto wprep(uint32_t x) const {
         if constexpr (MODE == kWindowU8 || MODE == kWindowU16) return __vminu4(__vsub4(x, base4), w4);
-        else return x;
+        else if constexpr (is_rep<MODE>()) {
+            // per byte: y = low M bits | g << M | bit M << 7, z = b >> (M + 1)
+            constexpr uint32_t lo = ((1u << M) - 1u) * 0x01010101u, bm = (1u << M) * 0x01010101u;
+            constexpr uint32_t zm = ((1u << (7u - M)) - 1u) * 0x01010101u;
+            return make_uint2((x & lo) | ((x & bm) << (7u - M)) | G, (x >> (M + 1u)) & zm);
+        } else return x;
     }
     // per input byte, shared by all lanes of the thread: the column's address
-    __device__ __forceinline__ Pre bprep(uint32_t x, int k) const {
+    template <class X>
+    __device__ __forceinline__ Pre bprep(X xw, int k) const {
+        if constexpr (is_rep<MODE>()) {
+            return {prmt_s(xw.x, xw.y, 0xCC00u | ((4u + k) << 4) | (uint32_t)k), 0u};
+        } else {
+        const uint32_t x = xw;
         const uint32_t c = (x >> (8 * k)) & 0xFFu;
         if constexpr (MODE == kIdentU16) return {tb + 2u * c, 0u};
         else if constexpr (MODE == kWindowU8) return {tb + c, 0u};
@@ -169,9 +208,12 @@ struct Tab {
             const uint32_t wc = (c * 171u) >> 9;  // c / 3 for c < 256
             return {tb + 4u * wc, (c - 3u * wc) * 9u};
         } else return {c, 0u};
+        }
     }
-    __device__ __forceinline__ uint32_t look(uint32_t s, uint32_t x, int k, Pre p) const {
-        if constexpr (MODE == kIdentU8) return lds_u8(__byte_perm(x, s, 0x6540 + k));
+    template <class X>
+    __device__ __forceinline__ uint32_t look(uint32_t s, X x, int k, Pre p) const {
+        if constexpr (is_rep<MODE>()) return lds_u8((s << (8 + LR)) + p.a);
+        else if constexpr (MODE == kIdentU8) return lds_u8(__byte_perm(x, s, 0x6540 + k));
         else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
         else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
         else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
@@ -179,7 +221,8 @@ struct Tab {
     }
     // per raw byte b, shared by all lanes stepping on it (scalar paths)
     __device__ __forceinline__ Pre bpre(uint32_t b) const {
-        if constexpr (MODE == kIdentU8 || MODE == kGlobalU16) return {b, 0u};
+        if constexpr (is_rep<MODE>()) return {rep_k(b), 0u};
+        else if constexpr (MODE == kIdentU8 || MODE == kGlobalU16) return {b, 0u};
         else if constexpr (MODE == kIdentU16) return {tb + 2u * b, 0u};
         else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
             const uint32_t c = min((b - base) & 0xFFu, w);
@@ -190,7 +233,8 @@ struct Tab {
         }
     }
     __device__ __forceinline__ uint32_t look_pre(uint32_t s, Pre p) const {
-        if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | p.a);
+        if constexpr (is_rep<MODE>()) return lds_u8((s << (8 + LR)) + p.a);
+        else if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | p.a);
         else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
         else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
         else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
@@ -198,7 +242,8 @@ struct Tab {
     }
     // scalar step on an encoded state and a raw byte
     __device__ __forceinline__ uint32_t look_byte(uint32_t s, uint32_t b) const {
-        if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | b);
+        if constexpr (is_rep<MODE>()) return lds_u8((s << (8 + LR)) + rep_k(b));
+        else if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | b);
         else if constexpr (MODE == kIdentU16) return t16[(s << 8) | b];
         else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
             uint32_t c = min((b - base) & 0xFFu, w);
@@ -215,20 +260,32 @@ struct Tab {
 // IdentU8 entries are stored biased by the table's shared address >> 8.
 template <int MODE>
 __device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem, uint32_t bits_words_n) {
+    constexpr uint32_t LR = rep_log_of(MODE);
+    constexpr uint32_t AL = 256u << LR;  // table alignment: (s_enc << (8 + LR)) is a row address
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
-    uint8_t *tab = reinterpret_cast<uint8_t *>(smem) + (((sb + 255u) & ~255u) - sb);
-    const uint32_t bias4 = MODE == kIdentU8 ? (((sb + 255u) & ~255u) >> 8) * 0x01010101u : 0u;
+    const uint32_t tb = (sb + AL - 1u) & ~(AL - 1u);
+    uint8_t *tab = reinterpret_cast<uint8_t *>(smem) + (tb - sb);
+    const uint32_t bias4 = (MODE == kIdentU8 || LR) ? (tb >> (8 + LR)) * 0x01010101u : 0u;
     const uint4 *src = reinterpret_cast<const uint4 *>(T.image);
     uint4 *dst = reinterpret_cast<uint4 *>(tab);
     for (uint32_t i = threadIdx.x; i < T.image_words / 4; i += blockDim.x) {
         uint4 v = __ldg(src + i);
-        if (MODE == kIdentU8) {
+        if (MODE == kIdentU8 || LR) {
             v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4);
             v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
         }
-        dst[i] = v;
+        if constexpr (LR != 0) {
+            // bytes 16j..16j+15 of row s -> R copies at (s << (8+LR)) + K(16j)
+            constexpr uint32_t M = 7u - LR;
+            const uint32_t s = i >> 4, j = i & 15u;
+            const uint32_t off = (s << (8 + LR)) | ((16u * j) & ((1u << M) - 1u)) | (((16u * j) >> M) << 7);
+#pragma unroll
+            for (uint32_t g = 0; g < (1u << LR); g++) dst[(off | (g << M)) >> 4] = v;
+        } else {
+            dst[i] = v;
+        }
     }
-    uint32_t *w = reinterpret_cast<uint32_t *>(tab) + T.image_words;
+    uint32_t *w = reinterpret_cast<uint32_t *>(tab) + smem_words<MODE>(T);
     for (uint32_t i = threadIdx.x; i < bits_words_n; i += blockDim.x) w[i] = __ldg(T.absorb_bits + i);
     return tab;
 }
@@ -238,17 +295,23 @@ __device__ __forceinline__ uint32_t bits_words(uint32_t nq) { return ((nq + 31) 
 // ---------------------------------------------------------------------------
 // lanes_kernel: one thread per execution sub-chunk, <= kLanes lanes in registers.
 // ---------------------------------------------------------------------------
+// Lanes l >= nlive of a thread do not load: a warp gather in which only some
+// threads still carry a second lane costs wavefronts for those threads only.
 template <int B, int MODE>
-__device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t (&st)[kLanes]) {
+__device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t (&st)[kLanes], uint32_t nlive) {
     const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
+    bool act[B];
+#pragma unroll
+    for (int l = 0; l < B; l++) act[l] = l == 0 || (uint32_t)l < nlive;
 #pragma unroll
     for (int wi = 0; wi < 4; wi++) {
-        uint32_t x = tab.wprep(wds[wi]);
+        const auto x = tab.wprep(wds[wi]);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const typename Tab<MODE>::Pre c = tab.bprep(x, k);
 #pragma unroll
-            for (int l = 0; l < B; l++) st[l] = tab.look(st[l], x, k, c);
+            for (int l = 0; l < B; l++)
+                if (act[l]) st[l] = tab.look(st[l], x, k, c);
         }
     }
 }
@@ -359,7 +422,7 @@ __device__ __forceinline__ bool block_step(const Tab<MODE> &tab, uint4 v, const 
                                            uint32_t (&fin)[kLanes], int convergence, bool tick,
                                            const uint32_t *sticky, bool suspend, uint32_t &pend, uint32_t &pend_off,
                                            uint32_t cur_off) {
-    block16<B, MODE>(tab, v, st);
+    block16<B, MODE>(tab, v, st, nlive);
     if (!convergence) return false;
     if (B > 1 && nlive > 1) {
         checkpoint<B>(absorb, has_absorb, tab.bias, st, own, nlive, fin, sticky, suspend, pend, pend_off, cur_off);
@@ -527,7 +590,7 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
     uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
     // sticky and error-state bitmaps after the absorbing one (sticky variant only)
     const uint32_t bw = bits_words(T.nq);
-    uint32_t *sticky_s = reinterpret_cast<uint32_t *>(tsm) + T.image_words + bw;
+    uint32_t *sticky_s = reinterpret_cast<uint32_t *>(tsm) + smem_words<MODE>(T) + bw;
     uint32_t *dead_s = sticky_s + bw;
     if (STICKY) {
         for (uint32_t i = threadIdx.x; i < bw; i += blockDim.x) {
@@ -541,7 +604,7 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
 #endif
     Tab<MODE> tab;
     tab.init(T, tsm);
-    const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + T.image_words;
+    const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
 
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -740,7 +803,8 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
                 if (k0 == 0 && k1 == 16) {
                     // a full aligned window: the match kernel's 16-byte step (static byte
                     // selection, per-word column preparation)
-                    block16<kConvergeLA, MODE>(tab, v, s);
+                    const uint32_t nact = np > base + lane ? min((uint32_t)kConvergeLA, (np - base - lane + 31u) / 32u) : 0u;
+                    block16<kConvergeLA, MODE>(tab, v, s, nact);
                 } else {
                     for (uint32_t k = k0; k < k1; k++) {
                         const uint32_t wsel = k >> 2;
@@ -1740,6 +1804,8 @@ void *lanes_fn(const DevTables &T) {
     const bool st = T.has_sticky != 0;
     switch (T.mode) {
     case kIdentU8: return lanes_ptr<kIdentU8>(st);
+    case kRepU8x8: return lanes_ptr<kRepU8x8>(st);
+    case kRepU8x4: return lanes_ptr<kRepU8x4>(st);
     case kIdentU16: return lanes_ptr<kIdentU16>(st);
     case kWindowU8: return lanes_ptr<kWindowU8>(st);
     case kWindowU16: return lanes_ptr<kWindowU16>(st);
@@ -1747,9 +1813,13 @@ void *lanes_fn(const DevTables &T) {
     default: return lanes_ptr<kGlobalU16>(st);
     }
 }
+// The converge kernel steps all lanes of one sub-chunk on the same byte (a
+// warp per sub-chunk): it reads the single IdentU8 copy of the same image.
 void *converge_fn(int mode) {
     switch (mode) {
-    case kIdentU8: return converge_ptr<kIdentU8>();
+    case kIdentU8:
+    case kRepU8x8:
+    case kRepU8x4: return converge_ptr<kIdentU8>();
     case kIdentU16: return converge_ptr<kIdentU16>();
     case kWindowU8: return converge_ptr<kWindowU8>();
     case kWindowU16: return converge_ptr<kWindowU16>();
@@ -1777,12 +1847,13 @@ int probe_dynamic_smem_base(uint32_t *dev_scratch) {
 }
 
 int lanes_smem_bytes(const DevTables &T) {
-    return (int)(256 + T.image_words * 4 + (T.has_sticky ? 3 : 1) * bits_words_host(T.nq) * 4);
+    const uint32_t lr = rep_log_of(T.mode);
+    return (int)((256u << lr) + (T.image_words << lr) * 4 + (T.has_sticky ? 3 : 1) * bits_words_host(T.nq) * 4);
 }
 
 int converge_smem_bytes(const DevTables &T, int warps_per_cta) {
     const uint32_t scr = (4 * T.imax + T.nq + 7) & ~7u;
-    return lanes_smem_bytes(T) + warps_per_cta * (int)scr * 2;
+    return (int)(256 + T.image_words * 4 + bits_words_host(T.nq) * 4) + warps_per_cta * (int)scr * 2;
 }
 
 uint32_t tree_lrs(const DevTables &T) {

@@ -42,7 +42,7 @@ uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uin
 
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
             const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &p,
-            bool full_domain) {
+            bool full_domain, uint32_t rep_budget) {
     if (!table || !accept_bitmap) return ST_ARG;
     if (ns == 0 || ns > 256) return ST_ALPHABET;
     if (nq == 0 || nq > kMaxStates || q0 >= nq) return ST_STATES;
@@ -173,6 +173,17 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
     } else if (fm == kPacked9 && p.nq <= 512) {
         p.mode = kPacked9;
         p.stride = 87;
+    } else if (fm == kRepU8x4 && p.nq <= u8_state_limit && (size_t)p.nq * 1024 + 1024 <= rep_budget) {
+        p.mode = kRepU8x4;
+        p.stride = 256;
+    } else if ((fm == kRepU8x8 || (fm == 0 && p.nq >= 32)) && p.nq <= u8_state_limit &&
+               (size_t)p.nq * 2048 + 2048 <= rep_budget) {
+        // eight bank-group copies: ~2.96 instead of ~3.53 shared-memory
+        // wavefronts per warp gather (tools/lds_gather_bench.cu, profiles/).
+        // Below 32 states the 8x table copy costs more than it saves (Tiny is
+        // launch/latency bound).
+        p.mode = kRepU8x8;
+        p.stride = 256;
     } else if (p.nq <= u8_state_limit) {
         p.mode = kIdentU8;
         p.stride = 256;
@@ -196,6 +207,8 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
         return col < W ? base + col : p.class_rep[defc];
     };
     switch (p.mode) {
+    case kRepU8x8:
+    case kRepU8x4:
     case kIdentU8: {
         p.image.assign((size_t)p.nq * 256 / 4, 0);
         uint8_t *img = reinterpret_cast<uint8_t *>(p.image.data());

@@ -21,8 +21,20 @@ enum TableMode : int {
     kWindowU8 = 3,  // smem, row = W window columns + 1 default column, uint8
     kWindowU16 = 4, // same, uint16
     kPacked9 = 5,   // smem, 256 columns of 9-bit states, 3 per 32-bit word
-    kGlobalU16 = 6  // global memory [nq][256] uint16 through the read-only path
+    kGlobalU16 = 6, // global memory [nq][256] uint16 through the read-only path
+    // IdentU8 replicated in shared memory: copy g (of R) confined to banks
+    // g*32/R .. (g+1)*32/R - 1, lane l of a warp reads copy l % R, so a warp's
+    // gather conflicts only within groups of 32/R lanes.
+    // The host image is the IdentU8 image; the lanes kernel expands it.
+    kRepU8x8 = 7,   // R = 8 (|Q| <= ~110: |Q| * 2 KB)
+    kRepU8x4 = 8    // R = 4 (|Q| * 1 KB)
 };
+#ifdef __CUDACC__
+#define DFA_HD __host__ __device__
+#else
+#define DFA_HD
+#endif
+DFA_HD constexpr uint32_t rep_log_of(int mode) { return mode == kRepU8x8 ? 3u : mode == kRepU8x4 ? 2u : 0u; }
 
 struct Prep {
     // user view
@@ -70,7 +82,7 @@ struct Prep {
 // shared-address bias of the table, see Tab<kIdentU8> in kernels.cu).
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
             const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &out,
-            bool full_domain = false);
+            bool full_domain = false, uint32_t rep_budget = 0);
 
 // Exact c-form partition (header dfa.h), 128-bit integer arithmetic.
 uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uint32_t k);

@@ -517,6 +517,39 @@ def test_max_lanes(name, cap):
     check_chunk_maps(c, 129, opts={D.DFA_OPT_MAX_LANES: cap})
 
 
+# ------------------------------------------------------------------ shared-memory table layouts
+@pytest.mark.parametrize("mode", [1, 7, 8])
+def test_table_layouts(mode, monkeypatch):
+    """IdentU8 and its bank-group replicas (R = 8, 4 copies)
+    give identical results: the five-config DFAs that fit, a small-alphabet DFA
+    with a sink (poison state), a sticky-parking DFA and misaligned input."""
+    monkeypatch.setenv("DFA_TABLE_MODE", str(mode))
+    cases = []
+    for name in ("tiny", "random", "keyword"):
+        w = W.get(name)
+        cases.append((Case(w.automaton, w.input(min(w.small_n, 1 << 19)), name), 129))
+    rng = np.random.default_rng(7)
+    a = automata.random_dfa_with_sink(40, 20, 7, 0.3)
+    cases.append((Case(a, rng.integers(0, 20, 300001).astype(np.uint8), "sink"), 77))
+    s = sticky_dfa(30, 3)
+    xs = rng.integers(0, 250, 1 << 18).astype(np.uint8)
+    xs[rng.choice(xs.size, 2000, replace=False)] = 10
+    xs[rng.choice(xs.size, 9, replace=False)] = 255
+    cases.append((Case(s, xs, "sticky"), 333))
+    for c, P in cases:
+        info = check_chunk_maps(c, P)
+        nq = c.a.table.shape[0] + (1 if c.a.table.shape[1] < 256 else 0)
+        want = {1: "ident_u8", 7: "rep8_u8" if nq * 2048 + 2048 <= 223 * 1024 else "ident_u8",
+                8: "rep4_u8" if nq * 1024 + 1024 <= 223 * 1024 else "ident_u8"}[mode]
+        assert info["table_mode_name"] == want, (c.name, info["table_mode_name"])
+        check_match(c)
+    # misaligned device input
+    w = W.get("random")
+    x = w.input(1 << 20)
+    buf = torch.from_numpy(np.concatenate([np.zeros(5, np.uint8), x])).to(DEV)
+    check_chunk_maps(Case(w.automaton, x, "random+5"), 300, dev=buf[5:])
+
+
 # ------------------------------------------------------------------ dfa_match_host pipeline + early exit (N4)
 @pytest.mark.parametrize("name", ["random", "keyword", "protein", "tiny"])
 @pytest.mark.parametrize("early", [0, 1])
