@@ -38,7 +38,7 @@ DFA_OPT_MAX_LANES = 9
 DFA_OPT_HOST_PIECE = 10
 DFA_OPT_EARLY_EXIT = 11
 TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16",
-               7: "rep8_u8", 8: "rep4_u8"}
+               7: "rep8_u8", 8: "rep4_u8", 9: "ident_u8_pad"}
 
 
 class DfaInfo(ctypes.Structure):

@@ -267,7 +267,8 @@ dfa_status probe(dfa_handle *h, uint32_t &u8_limit) {
     CK(h->status.ensure(sizeof(DevStatus)));
     int base = probe_dynamic_smem_base(h->status.as<uint32_t>());
     if (base < 0) return cuda_fail(cudaGetLastError(), "probe_dynamic_smem_base", __LINE__);
-    const uint32_t bias = (((uint32_t)base + 255u) & ~255u) >> 8;
+    const uint32_t bias = std::max((((uint32_t)base + 255u) & ~255u) >> 8,  // IdentU8
+                                   ((uint32_t)base + kPadStride - 1) / kPadStride);  // IdentU8P
     u8_limit = bias >= 256 ? 0 : 256 - bias;
     return DFA_OK;
 }
@@ -815,7 +816,9 @@ dfa_status dfa_get_info(dfa_handle_t h, dfa_info *out) {
     i.dead_state = p.first_dead_user;
     i.num_absorbing = p.num_absorbing_user;
     i.table_mode = (uint32_t)p.mode;
-    i.table_bytes = p.mode == kGlobalU16 ? 0 : (uint32_t)(p.image.size() * 4) << rep_log_of(p.mode);
+    i.table_bytes = p.mode == kGlobalU16 ? 0
+                  : p.mode == kIdentU8P ? p.nq * kPadStride
+                  : (uint32_t)(p.image.size() * 4) << rep_log_of(p.mode);
     i.c_num = h->c_num;
     i.c_den = h->c_den;
     i.device_ready = h->device_ready ? 1 : 0;

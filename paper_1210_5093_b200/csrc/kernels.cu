@@ -118,7 +118,10 @@ __host__ __device__ constexpr bool is_rep() { return rep_log_of(MODE) != 0; }
 // Words of the table image as laid out in shared memory (R copies for the
 // replicated modes).
 template <int MODE>
-__device__ __forceinline__ uint32_t smem_words(const DevTables &T) { return T.image_words << rep_log_of(MODE); }
+__device__ __forceinline__ uint32_t smem_words(const DevTables &T) {
+    if constexpr (MODE == kIdentU8P) return T.image_words / 64u * (kPadStride / 4u);
+    else return T.image_words << rep_log_of(MODE);
+}
 
 template <int MODE>
 struct Tab {
@@ -158,7 +161,7 @@ struct Tab {
         base4 = T.win_base * 0x01010101u;
         w4 = T.win_w * 0x01010101u;
         tb = (uint32_t)__cvta_generic_to_shared(table_smem);
-        bias = MODE == kIdentU8 ? (tb >> 8) : is_rep<MODE>() ? (tb >> (8 + LR)) : 0u;
+        bias = MODE == kIdentU8 ? (tb >> 8) : is_rep<MODE>() ? (tb >> (8 + LR)) : MODE == kIdentU8P ? tb / kPadStride : 0u;
         G = is_rep<MODE>() ? (((threadIdx.x & 31u) & ((1u << LR) - 1u)) << M) * 0x01010101u : 0u;
         rowb = MODE == kIdentU16 ? 512u : MODE == kWindowU8 ? T.stride : MODE == kWindowU16 ? 2u * T.stride
              : MODE == kPacked9 ? 4u * T.stride : 0u;
@@ -213,6 +216,7 @@ struct Tab {
     template <class X>
     __device__ __forceinline__ uint32_t look(uint32_t s, X x, int k, Pre p) const {
         if constexpr (is_rep<MODE>()) return lds_u8((s << (8 + LR)) + p.a);
+        else if constexpr (MODE == kIdentU8P) return lds_u8(s * kPadStride + p.a);
         else if constexpr (MODE == kIdentU8) return lds_u8(__byte_perm(x, s, 0x6540 + k));
         else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
         else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
@@ -222,7 +226,7 @@ struct Tab {
     // per raw byte b, shared by all lanes stepping on it (scalar paths)
     __device__ __forceinline__ Pre bpre(uint32_t b) const {
         if constexpr (is_rep<MODE>()) return {rep_k(b), 0u};
-        else if constexpr (MODE == kIdentU8 || MODE == kGlobalU16) return {b, 0u};
+        else if constexpr (MODE == kIdentU8 || MODE == kIdentU8P || MODE == kGlobalU16) return {b, 0u};
         else if constexpr (MODE == kIdentU16) return {tb + 2u * b, 0u};
         else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
             const uint32_t c = min((b - base) & 0xFFu, w);
@@ -234,6 +238,7 @@ struct Tab {
     }
     __device__ __forceinline__ uint32_t look_pre(uint32_t s, Pre p) const {
         if constexpr (is_rep<MODE>()) return lds_u8((s << (8 + LR)) + p.a);
+        else if constexpr (MODE == kIdentU8P) return lds_u8(s * kPadStride + p.a);
         else if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | p.a);
         else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
         else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
@@ -243,6 +248,7 @@ struct Tab {
     // scalar step on an encoded state and a raw byte
     __device__ __forceinline__ uint32_t look_byte(uint32_t s, uint32_t b) const {
         if constexpr (is_rep<MODE>()) return lds_u8((s << (8 + LR)) + rep_k(b));
+        else if constexpr (MODE == kIdentU8P) return lds_u8(s * kPadStride + b);
         else if constexpr (MODE == kIdentU8) return lds_u8((s << 8) | b);
         else if constexpr (MODE == kIdentU16) return t16[(s << 8) | b];
         else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
@@ -262,19 +268,26 @@ template <int MODE>
 __device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem, uint32_t bits_words_n) {
     constexpr uint32_t LR = rep_log_of(MODE);
     constexpr uint32_t AL = 256u << LR;  // table alignment: (s_enc << (8 + LR)) is a row address
+    constexpr bool PAD = MODE == kIdentU8P;
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t tb = (sb + AL - 1u) & ~(AL - 1u);
+    // IdentU8P: s_enc * 260 is a row address, so the table starts at a multiple of 260
+    const uint32_t tb = PAD ? (sb + kPadStride - 1u) / kPadStride * kPadStride : (sb + AL - 1u) & ~(AL - 1u);
     uint8_t *tab = reinterpret_cast<uint8_t *>(smem) + (tb - sb);
-    const uint32_t bias4 = (MODE == kIdentU8 || LR) ? (tb >> (8 + LR)) * 0x01010101u : 0u;
+    const uint32_t bias4 = PAD ? (tb / kPadStride) * 0x01010101u
+                         : (MODE == kIdentU8 || LR) ? (tb >> (8 + LR)) * 0x01010101u : 0u;
     const uint4 *src = reinterpret_cast<const uint4 *>(T.image);
     uint4 *dst = reinterpret_cast<uint4 *>(tab);
     for (uint32_t i = threadIdx.x; i < T.image_words / 4; i += blockDim.x) {
         uint4 v = __ldg(src + i);
-        if (MODE == kIdentU8 || LR) {
+        if (MODE == kIdentU8 || LR || PAD) {
             v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4);
             v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
         }
-        if constexpr (LR != 0) {
+        if constexpr (PAD) {
+            // bytes 16j..16j+15 of row s -> s*260 + 16j (4-byte aligned)
+            uint32_t *d32 = reinterpret_cast<uint32_t *>(tab) + (i >> 4) * (kPadStride / 4u) + (i & 15u) * 4u;
+            d32[0] = v.x; d32[1] = v.y; d32[2] = v.z; d32[3] = v.w;
+        } else if constexpr (LR != 0) {
             // bytes 16j..16j+15 of row s -> R copies at (s << (8+LR)) + K(16j)
             constexpr uint32_t M = 7u - LR;
             const uint32_t s = i >> 4, j = i & 15u;
@@ -753,9 +766,9 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
     uint8_t *tsm = load_tables<MODE>(T, smem4, bw);
     Tab<MODE> tab;
     tab.init(T, tsm);
-    const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + T.image_words;
+    const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint16_t *scr = reinterpret_cast<uint16_t *>(reinterpret_cast<uint32_t *>(tsm) + T.image_words + bw) +
+    uint16_t *scr = reinterpret_cast<uint16_t *>(reinterpret_cast<uint32_t *>(tsm) + smem_words<MODE>(T) + bw) +
                     (size_t)warp * scratch_u16(T);
     uint16_t *pool_s = scr, *pool_id = scr + T.imax, *parent = scr + 2 * T.imax, *res = scr + 3 * T.imax;
     uint16_t *first = scr + 4 * T.imax;
@@ -1806,6 +1819,7 @@ void *lanes_fn(const DevTables &T) {
     case kIdentU8: return lanes_ptr<kIdentU8>(st);
     case kRepU8x8: return lanes_ptr<kRepU8x8>(st);
     case kRepU8x4: return lanes_ptr<kRepU8x4>(st);
+    case kIdentU8P: return lanes_ptr<kIdentU8P>(st);
     case kIdentU16: return lanes_ptr<kIdentU16>(st);
     case kWindowU8: return lanes_ptr<kWindowU8>(st);
     case kWindowU16: return lanes_ptr<kWindowU16>(st);
@@ -1814,12 +1828,14 @@ void *lanes_fn(const DevTables &T) {
     }
 }
 // The converge kernel steps all lanes of one sub-chunk on the same byte (a
-// warp per sub-chunk): it reads the single IdentU8 copy of the same image.
+// warp per sub-chunk): with 256-byte rows they would all read one bank, so
+// every byte-table mode converges on the padded single copy of the same image.
 void *converge_fn(int mode) {
     switch (mode) {
     case kIdentU8:
+    case kIdentU8P:
     case kRepU8x8:
-    case kRepU8x4: return converge_ptr<kIdentU8>();
+    case kRepU8x4: return converge_ptr<kIdentU8P>();
     case kIdentU16: return converge_ptr<kIdentU16>();
     case kWindowU8: return converge_ptr<kWindowU8>();
     case kWindowU16: return converge_ptr<kWindowU16>();
@@ -1846,14 +1862,22 @@ int probe_dynamic_smem_base(uint32_t *dev_scratch) {
     return (int)v;
 }
 
+// shared-memory bytes of the table as a kernel lays it out (plus alignment pad)
+static int table_smem_bytes(const DevTables &T, int mode) {
+    if (mode == kIdentU8P) return (int)(kPadStride + T.image_words / 64 * kPadStride);
+    const uint32_t lr = rep_log_of(mode);
+    return (int)((256u << lr) + (T.image_words << lr) * 4);
+}
+static bool is_u8_mode(int mode) { return mode == kIdentU8 || mode == kIdentU8P || mode == kRepU8x8 || mode == kRepU8x4; }
+
 int lanes_smem_bytes(const DevTables &T) {
-    const uint32_t lr = rep_log_of(T.mode);
-    return (int)((256u << lr) + (T.image_words << lr) * 4 + (T.has_sticky ? 3 : 1) * bits_words_host(T.nq) * 4);
+    return table_smem_bytes(T, T.mode) + (T.has_sticky ? 3 : 1) * bits_words_host(T.nq) * 4;
 }
 
 int converge_smem_bytes(const DevTables &T, int warps_per_cta) {
     const uint32_t scr = (4 * T.imax + T.nq + 7) & ~7u;
-    return (int)(256 + T.image_words * 4 + bits_words_host(T.nq) * 4) + warps_per_cta * (int)scr * 2;
+    return table_smem_bytes(T, is_u8_mode(T.mode) ? kIdentU8P : T.mode) + bits_words_host(T.nq) * 4 +
+           warps_per_cta * (int)scr * 2;
 }
 
 uint32_t tree_lrs(const DevTables &T) {

@@ -185,7 +185,7 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
         p.mode = kRepU8x8;
         p.stride = 256;
     } else if (p.nq <= u8_state_limit) {
-        p.mode = kIdentU8;
+        p.mode = fm == kIdentU8 ? kIdentU8 : kIdentU8P;
         p.stride = 256;
     } else if (W && (size_t)p.nq * window_words_u16(W + 1) * 4 <= smem_budget) {
         p.mode = kWindowU16;
@@ -209,6 +209,7 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
     switch (p.mode) {
     case kRepU8x8:
     case kRepU8x4:
+    case kIdentU8P:
     case kIdentU8: {
         p.image.assign((size_t)p.nq * 256 / 4, 0);
         uint8_t *img = reinterpret_cast<uint8_t *>(p.image.data());

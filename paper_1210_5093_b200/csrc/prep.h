@@ -27,8 +27,14 @@ enum TableMode : int {
     // gather conflicts only within groups of 32/R lanes.
     // The host image is the IdentU8 image; the lanes kernel expands it.
     kRepU8x8 = 7,   // R = 8 (|Q| <= ~110: |Q| * 2 KB)
-    kRepU8x4 = 8    // R = 4 (|Q| * 1 KB)
+    kRepU8x4 = 8,   // R = 4 (|Q| * 1 KB)
+    // IdentU8 with rows padded to kPadStride = 260 bytes: entry (s, b) in bank
+    // (s_enc + b/4) mod 32, so lanes in different states that read the same
+    // byte (Zipf text; the converge kernel's lanes, which all step one byte)
+    // fall into different banks.  Address s_enc * 260 + b: one IMAD.
+    kIdentU8P = 9
 };
+constexpr uint32_t kPadStride = 260;
 #ifdef __CUDACC__
 #define DFA_HD __host__ __device__
 #else

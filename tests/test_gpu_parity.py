@@ -518,10 +518,10 @@ def test_max_lanes(name, cap):
 
 
 # ------------------------------------------------------------------ shared-memory table layouts
-@pytest.mark.parametrize("mode", [1, 7, 8])
+@pytest.mark.parametrize("mode", [1, 7, 8, 9])
 def test_table_layouts(mode, monkeypatch):
-    """IdentU8 and its bank-group replicas (R = 8, 4 copies)
-    give identical results: the five-config DFAs that fit, a small-alphabet DFA
+    """IdentU8, its bank-group replicas (R = 8, 4 copies) and its padded-row form
+     give identical results: the five-config DFAs that fit, a small-alphabet DFA
     with a sink (poison state), a sticky-parking DFA and misaligned input."""
     monkeypatch.setenv("DFA_TABLE_MODE", str(mode))
     cases = []
@@ -539,8 +539,8 @@ def test_table_layouts(mode, monkeypatch):
     for c, P in cases:
         info = check_chunk_maps(c, P)
         nq = c.a.table.shape[0] + (1 if c.a.table.shape[1] < 256 else 0)
-        want = {1: "ident_u8", 7: "rep8_u8" if nq * 2048 + 2048 <= 223 * 1024 else "ident_u8",
-                8: "rep4_u8" if nq * 1024 + 1024 <= 223 * 1024 else "ident_u8"}[mode]
+        want = {1: "ident_u8", 7: "rep8_u8" if nq * 2048 + 2048 <= 223 * 1024 else "ident_u8_pad",
+                8: "rep4_u8" if nq * 1024 + 1024 <= 223 * 1024 else "ident_u8_pad", 9: "ident_u8_pad"}[mode]
         assert info["table_mode_name"] == want, (c.name, info["table_mode_name"])
         check_match(c)
     # misaligned device input

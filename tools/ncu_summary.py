@@ -11,6 +11,9 @@ KEYS = [
     ("dram__bytes_read.sum", "DRAM bytes read (MB)"),
     ("dram__bytes_write.sum", "DRAM bytes written (MB)"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/TEX throughput (% of peak)"),
+    ("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed", "L1 data-pipe (LSU) wavefronts (% of peak)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "  of which shared memory (% of peak)"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "shared-load bank conflicts"),
     ("sass__inst_executed_shared_loads", "shared-load instructions (warp)"),
@@ -18,6 +21,11 @@ KEYS = [
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global-load sectors"),
     ("smsp__inst_executed.sum", "instructions executed (warp)"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy (%)"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+     "warps stalled on short scoreboard (shared-memory results) per issue"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+     "warps stalled on long scoreboard (global loads) per issue"),
+    ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "warps stalled on MIO throttle per issue"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy (%)"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),

@@ -9,7 +9,9 @@ python bench.py > $O/bench_random.json 2> $O/bench_random.err
 for c in tiny keyword protein; do python bench.py --config $c --steps 50 --e2e-steps 3 --no-cpu-baseline > $O/bench_$c.json 2>&1; done
 python bench.py --config worst --steps 5 --e2e-steps 1 --no-cpu-baseline > $O/bench_worst.json 2>&1
 for c in random keyword protein; do python bench.py --config $c --steps 20 --e2e-steps 1 --no-cpu-baseline --no-lookahead --alg2 > $O/bench_alg2_$c.json 2>&1; done
+for c in random keyword; do python bench.py --config $c --steps 20 --e2e-steps 1 --no-cpu-baseline --no-lookahead --no-batch --convergence 0 > $O/bench_noconv_$c.json 2>&1; done
 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/ldsb tools/lds_gather_bench.cu && /tmp/ldsb 1024 > $O/lds_gather.jsonl 2>&1
 B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --quiet-json --no-lookahead"
 $B > $O/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -s 30 -c 12 --csv --log-file $O/launches_random.csv $B > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"lanes_kernel|compose8" -s 6 -c 2 -o $O/random $B > /dev/null 2>&1
