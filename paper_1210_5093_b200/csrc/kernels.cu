@@ -130,6 +130,7 @@ struct Tab {
     const uint32_t *t32;
     const uint16_t *g;
     uint32_t stride, base4, w4, base, w;
+    uint32_t lo4, hi4;  // window modes: column bits / window-tag bits of every byte
     uint32_t tb;      // shared-space address of the table
     uint32_t rowb;    // bytes per table row
     // IdentU8: the table sits at a 256-aligned shared address A = bias*256 and
@@ -162,9 +163,14 @@ struct Tab {
         w4 = T.win_w * 0x01010101u;
         tb = (uint32_t)__cvta_generic_to_shared(table_smem);
         bias = MODE == kIdentU8 ? (tb >> 8) : is_rep<MODE>() ? (tb >> (8 + LR)) : MODE == kIdentU8P ? tb / kPadStride : 0u;
+        lo4 = (T.win_w - 1u) * 0x01010101u;
+        hi4 = (~(T.win_w - 1u) & 0xFFu) * 0x01010101u;
         G = is_rep<MODE>() ? (((threadIdx.x & 31u) & ((1u << LR) - 1u)) << M) * 0x01010101u : 0u;
         rowb = MODE == kIdentU16 ? 512u : MODE == kWindowU8 ? T.stride : MODE == kWindowU16 ? 2u * T.stride
              : MODE == kPacked9 ? 4u * T.stride : 0u;
+        // WindowU16: the table starts at a multiple of the row size and holds
+        // s + bias, so s_enc * rowb is the row's shared address (no base add)
+        if (MODE == kWindowU16) bias = tb / rowb;
     }
     __device__ __forceinline__ uint32_t enc(uint32_t s) const { return s + bias; }
     __device__ __forceinline__ uint32_t dec(uint32_t s) const { return s - bias; }
@@ -206,7 +212,7 @@ struct Tab {
         const uint32_t c = (x >> (8 * k)) & 0xFFu;
         if constexpr (MODE == kIdentU16) return {tb + 2u * c, 0u};
         else if constexpr (MODE == kWindowU8) return {tb + c, 0u};
-        else if constexpr (MODE == kWindowU16) return {tb + 2u * c, 0u};
+        else if constexpr (MODE == kWindowU16) return {2u * c, 0u};
         else if constexpr (MODE == kPacked9) {
             const uint32_t wc = (c * 171u) >> 9;  // c / 3 for c < 256
             return {tb + 4u * wc, (c - 3u * wc) * 9u};
@@ -230,7 +236,7 @@ struct Tab {
         else if constexpr (MODE == kIdentU16) return {tb + 2u * b, 0u};
         else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
             const uint32_t c = min((b - base) & 0xFFu, w);
-            return {tb + (MODE == kWindowU16 ? 2u : 1u) * c, 0u};
+            return {MODE == kWindowU16 ? 2u * c : tb + c, 0u};
         } else {
             const uint32_t wc = (b * 171u) >> 9;
             return {tb + 4u * wc, (b - 3u * wc) * 9u};
@@ -254,7 +260,7 @@ struct Tab {
         else if constexpr (MODE == kWindowU8 || MODE == kWindowU16) {
             uint32_t c = min((b - base) & 0xFFu, w);
             if constexpr (MODE == kWindowU8) return t8[s * stride + c];
-            else return t16[s * stride + c];
+            else return lds_u16(s * rowb + 2u * c);
         } else if constexpr (MODE == kPacked9) {
             return (t32[s * stride + b / 3u] >> ((b % 3u) * 9u)) & 511u;
         } else return __ldg(g + (s << 8) + b);
@@ -271,8 +277,12 @@ __device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem,
     constexpr bool PAD = MODE == kIdentU8P;
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
     // IdentU8P: s_enc * 260 is a row address, so the table starts at a multiple of 260
-    const uint32_t tb = PAD ? (sb + kPadStride - 1u) / kPadStride * kPadStride : (sb + AL - 1u) & ~(AL - 1u);
+    constexpr bool WIN16 = MODE == kWindowU16;
+    const uint32_t rowb = 2u * T.stride;  // WindowU16 row bytes (4-byte multiple: odd word count)
+    const uint32_t tb = PAD ? (sb + kPadStride - 1u) / kPadStride * kPadStride
+                      : WIN16 ? (sb + rowb - 1u) / rowb * rowb : (sb + AL - 1u) & ~(AL - 1u);
     uint8_t *tab = reinterpret_cast<uint8_t *>(smem) + (tb - sb);
+    const uint32_t bias2 = WIN16 ? (tb / rowb) * 0x00010001u : 0u;
     const uint32_t bias4 = PAD ? (tb / kPadStride) * 0x01010101u
                          : (MODE == kIdentU8 || LR) ? (tb >> (8 + LR)) * 0x01010101u : 0u;
     const uint4 *src = reinterpret_cast<const uint4 *>(T.image);
@@ -283,7 +293,12 @@ __device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem,
             v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4);
             v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
         }
-        if constexpr (PAD) {
+        if constexpr (WIN16) {
+            // u16 entries + bias; rows are 4-byte multiples, the image 16-byte chunks
+            // are not row aligned: store as words
+            uint32_t *d32 = reinterpret_cast<uint32_t *>(tab) + 4u * i;
+            d32[0] = v.x + bias2; d32[1] = v.y + bias2; d32[2] = v.z + bias2; d32[3] = v.w + bias2;
+        } else if constexpr (PAD) {
             // bytes 16j..16j+15 of row s -> s*260 + 16j (4-byte aligned)
             uint32_t *d32 = reinterpret_cast<uint32_t *>(tab) + (i >> 4) * (kPadStride / 4u) + (i & 15u) * 4u;
             d32[0] = v.x; d32[1] = v.y; d32[2] = v.z; d32[3] = v.w;
@@ -316,6 +331,26 @@ __device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t 
     bool act[B];
 #pragma unroll
     for (int l = 0; l < B; l++) act[l] = l == 0 || (uint32_t)l < nlive;
+    if constexpr (MODE == kWindowU16) {
+        // All 16 bytes inside the aligned window [base, base + W): the column is
+        // the byte's low bits, no clamp (residue text: always).  u16 entries and
+        // W <= 128, so 2 * column fits the byte lane.
+        const uint32_t out = ((v.x ^ tab.base4) | (v.y ^ tab.base4) | (v.z ^ tab.base4) | (v.w ^ tab.base4)) & tab.hi4;
+        if (out == 0) {
+#pragma unroll
+            for (int wi = 0; wi < 4; wi++) {
+                const uint32_t xd = (wds[wi] & tab.lo4) << 1;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t a = (xd >> (8 * k)) & 0xFFu;
+#pragma unroll
+                    for (int l = 0; l < B; l++)
+                        if (act[l]) st[l] = Tab<MODE>::lds_u16(st[l] * tab.rowb + a);
+                }
+            }
+            return;
+        }
+    }
 #pragma unroll
     for (int wi = 0; wi < 4; wi++) {
         const auto x = tab.wprep(wds[wi]);

@@ -550,6 +550,27 @@ def test_table_layouts(mode, monkeypatch):
     check_chunk_maps(Case(w.automaton, x, "random+5"), 300, dev=buf[5:])
 
 
+def test_window_fast_and_slow_paths():
+    """WindowU16 (|Q| > 252, the non-default bytes inside one aligned window): 16-byte
+    blocks entirely inside the window take the low-bits column step, blocks with an
+    outside byte the clamped one; mixed per warp, same results."""
+    rng = np.random.default_rng(11)
+    nq = 300
+    t = rng.integers(0, nq, size=(nq, 256)).astype(np.uint16)
+    t[:, :64] = t[:, [200]]          # every byte outside [64, 128) behaves like byte 200
+    t[:, 128:] = t[:, [200]]
+    a = automata.Automaton(t, 0, rng.random(nq) < 0.3, "window")
+    n = 1 << 19
+    x = rng.integers(64, 128, n).astype(np.uint8)
+    out = rng.random(n) < 0.02
+    x[out] = rng.integers(0, 256, int(out.sum()))
+    c = Case(a, x, "window")
+    for P in (1, 97, 1000):
+        info = check_chunk_maps(c, P)
+        assert info["table_mode_name"] == "window_u16", info["table_mode_name"]
+    check_match(c)
+
+
 # ------------------------------------------------------------------ dfa_match_host pipeline + early exit (N4)
 @pytest.mark.parametrize("name", ["random", "keyword", "protein", "tiny"])
 @pytest.mark.parametrize("early", [0, 1])
