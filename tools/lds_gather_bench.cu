@@ -124,6 +124,84 @@ __global__ void __launch_bounds__(1024, 1) gather(const uint8_t *img, uint32_t i
     out[tid] = ILP == 1 ? s[0] - bias : r;
 }
 
+
+// Input staged by per-thread 1-D bulk copies (cp.async.bulk, the TMA engine)
+// into a shared-memory ring instead of register loads: S stages of CH bytes per
+// thread, slot pitch CH + 16 (conflict-free LDS.128 read-back), one mbarrier per
+// thread and stage.  L = 0 (ident_u8) or 1 (rep8_u8) table layout.
+template <int L, int CH, int S>
+__global__ void __launch_bounds__(1024, 1) gather_tma(const uint8_t *img, uint32_t img_bytes, uint32_t align,
+                                                      const uint8_t *in, uint64_t per_thread, uint32_t *out) {
+    extern __shared__ uint4 sm[];
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t base = (sb + align - 1) & ~(align - 1);
+    uint8_t *tab = reinterpret_cast<uint8_t *>(sm) + (base - sb);
+    const int shift = L == 0 ? 8 : 11;
+    const uint32_t bias = base >> shift, bias4 = bias * 0x01010101u;
+    for (uint32_t i = threadIdx.x; i < img_bytes / 16; i += blockDim.x) {
+        uint4 v = reinterpret_cast<const uint4 *>(img)[i];
+        v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4); v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
+        reinterpret_cast<uint4 *>(tab)[i] = v;
+    }
+    constexpr uint32_t PITCH = CH + 16;
+    uint8_t *ring = tab + ((img_bytes + 127) & ~127u);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ring + (size_t)blockDim.x * S * PITCH);
+    const uint32_t t = threadIdx.x;
+    const uint32_t my_slot0 = (uint32_t)__cvta_generic_to_shared(ring) + t * S * PITCH;
+    const uint32_t my_bar0 = (uint32_t)__cvta_generic_to_shared(bars) + t * S * 8;
+#pragma unroll
+    for (int k = 0; k < S; k++) asm volatile("mbarrier.init.shared.b64 [%0], 1;" :: "r"(my_bar0 + 8 * k));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint8_t *p = in + (uint64_t)tid * per_thread;
+    const uint32_t lane = t & 31;
+    uint32_t s = L == 0 ? (base >> 8) : (base >> 11);
+    const uint32_t g4 = L == 1 ? ((lane & 7) << 4) * 0x01010101u : 0u;
+    auto issue = [&](uint64_t off, int k) {
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" :: "r"(my_bar0 + 8 * k), "r"((uint32_t)CH) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"(my_slot0 + k * PITCH), "l"(p + off), "r"((uint32_t)CH), "r"(my_bar0 + 8 * k) : "memory");
+    };
+    const uint64_t nblk = per_thread / CH;
+#pragma unroll
+    for (int k = 0; k < S; k++) if ((uint64_t)k < nblk) issue((uint64_t)k * CH, k);
+    uint32_t phase = 0;
+    for (uint64_t bi = 0; bi < nblk; bi++) {
+        const int k = (int)(bi % S);
+        const uint32_t bar = my_bar0 + 8 * k;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                         : "=r"(done) : "r"(bar), "r"((phase >> k) & 1u) : "memory");
+        phase ^= 1u << k;
+        uint4 q[CH / 16];
+#pragma unroll
+        for (int j = 0; j < CH / 16; j++)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q[j].x), "=r"(q[j].y), "=r"(q[j].z), "=r"(q[j].w)
+                         : "r"(my_slot0 + k * PITCH + 16 * j));
+        if (bi + S < nblk) issue((bi + S) * CH, k);  // the slot is in registers now
+#pragma unroll
+        for (int j = 0; j < CH / 16; j++) {
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+            for (int wq = 0; wq < 4; wq++) {
+                const uint32_t x = w4[wq];
+                if (L == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) s = lds_u8(__byte_perm(x, s, 0x6540 + kk));
+                } else {
+                    const uint32_t y = (x & 0x0F0F0F0Fu) | ((x & 0x10101010u) << 3) | g4;
+                    const uint32_t z = (x >> 5) & 0x07070707u;
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) s = lds_u8((s << 11) + prmt(y, z, 0xCC00 | ((4 + kk) << 4) | kk));
+                }
+            }
+        }
+    }
+    out[tid] = s - bias;
+}
+
 static uint64_t rng = 88172645463325252ull;
 static uint32_t nxt() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return (uint32_t)rng; }
 
@@ -208,6 +286,55 @@ int main(int argc, char **argv) {
                "\"lookups_per_clk_per_sm_at_1965\": %.2f, \"check\": \"%s\"}\n",
                L, ILP, L == 0 ? "ident_u8" : L == 1 ? "rep8_u8" : L == 2 ? "rep16_p6" : L == 3 ? "rep16_u8" : L == 4 ? "load_only" : L == 5 ? "ident_u8_L2pf256" : L == 6 ? "ident_u8_L1noalloc" : "load_only_L1noalloc", nq, bytes, ms,
                bytes_done / ms / 1e6, bytes_done / (ms * 1e-3) / sms / 1.965e9, bad ? "FAIL" : "ok");
+        CK(cudaFree(dimg));
+    }
+    // TMA-staged input (layouts 0 and 1, CH bytes per stage, S stages)
+    for (int L = 0; L < 2; L++) {
+        const int nq = 64;
+        std::vector<uint8_t> delta(nq * 256);
+        for (auto &d : delta) d = nxt() % nq;
+        uint32_t bytes, align;
+        std::vector<uint8_t> img;
+        if (L == 0) { bytes = nq * 256; align = 256; img.assign(bytes, 0);
+            for (int s = 0; s < nq; s++) for (int b = 0; b < 256; b++) img[s * 256 + b] = delta[s * 256 + b]; }
+        else { bytes = nq * 2048; align = 2048; img.assign(bytes, 0);
+            for (int g = 0; g < 8; g++) for (int s = 0; s < nq; s++) for (int b = 0; b < 256; b++)
+                img[(s << 11) | (((b >> 5) & 7) << 8) | (((b >> 4) & 1) << 7) | (g << 4) | (b & 15)] = delta[s * 256 + b]; }
+        uint8_t *dimg; CK(cudaMalloc(&dimg, bytes + 16));
+        CK(cudaMemcpy(dimg, img.data(), bytes, cudaMemcpyHostToDevice));
+        for (int variant = 0; variant < 3; variant++) {
+            const int CHv = variant == 0 ? 32 : variant == 1 ? 64 : 32, Sv = variant == 2 ? 3 : 2;
+            void (*f)(const uint8_t *, uint32_t, uint32_t, const uint8_t *, uint64_t, uint32_t *) =
+                L == 0 ? (variant == 0 ? gather_tma<0, 32, 2> : variant == 1 ? gather_tma<0, 64, 2> : gather_tma<0, 32, 3>)
+                       : (variant == 0 ? gather_tma<1, 32, 2> : variant == 1 ? gather_tma<1, 64, 2> : gather_tma<1, 32, 3>);
+            const int threads = 1024, grid = sms;
+            const size_t smem = align + ((bytes + 127) & ~127u) + (size_t)threads * Sv * (CHv + 16) + threads * Sv * 8 + 64;
+            if (smem > 232448) { printf("{\"tma\": 1, \"layout\": %d, \"skip\": \"smem %zu\"}\n", L, smem); continue; }
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            const uint64_t per = (n / ((uint64_t)grid * threads)) & ~(uint64_t)(CHv - 1);
+            f<<<grid, threads, smem>>>(dimg, bytes, align, din, per, dout);
+            CK(cudaDeviceSynchronize());
+            std::vector<uint32_t> got(grid * threads);
+            CK(cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost));
+            int bad = 0;
+            for (uint32_t t : {0u, 777u, (uint32_t)(grid * threads - 1)}) {
+                uint32_t hs = 0;
+                for (uint64_t i = 0; i < per; i++) hs = delta[hs * 256 + hin[t * per + i]];
+                bad += got[t] != hs;
+            }
+            cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+            cudaEventRecord(a);
+            for (int r = 0; r < 20; r++) f<<<grid, threads, smem>>>(dimg, bytes, align, din, per, dout);
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            ms /= 20;
+            const double bytes_done = (double)per * grid * threads;
+            printf("{\"tma\": 1, \"layout\": %d, \"name\": \"%s_tma\", \"stage_bytes\": %d, \"stages\": %d, \"ms\": %.4f, "
+                   "\"GBps\": %.1f, \"lookups_per_clk_per_sm_at_1965\": %.2f, \"check\": \"%s\"}\n",
+                   L, L == 0 ? "ident_u8" : "rep8_u8", CHv, Sv, ms, bytes_done / ms / 1e6,
+                   bytes_done / (ms * 1e-3) / sms / 1.965e9, bad ? "FAIL" : "ok");
+        }
         CK(cudaFree(dimg));
     }
     return 0;
