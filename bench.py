@@ -354,7 +354,9 @@ def main():
         "config": {"workload": BASELINE_WORKLOAD.get(args.config, args.config), "name": args.config,
                    "input_bytes_per_gpu": n, "chunks": P, "states": a.nq, "alphabet": a.ns,
                    "i_max": imax, "gamma": f"{d.info['gamma_num']}/{d.info['gamma_den']}",
-                   "table_mode": d.info["table_mode_name"], "chunk_ratio_c": f"{d.info['c_num']}/{d.info['c_den']}",
+                   "classes": d.info["num_classes"], "table_mode": d.info["table_mode_name"],
+                   "table_smem_bytes": d.info["table_bytes"], "table_sha256": W.sha256(a.table)[:16],
+                   "chunk_ratio_c": f"{d.info['c_num']}/{d.info['c_den']}",
                    "convergence": bool(args.convergence),
                    "domains": "Q minus Z for every sub-chunk (Alg.2 ablation)" if args.alg2 else "I_sigma (Alg.3)",
                    "l2": "input 256 MiB+ > 126 MB L2, no flush",
