@@ -659,6 +659,10 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
         uint64_t start, end;
         sub_range(p, i, start, end);
         const uint32_t dom = sub_domain(T, p, in, i, start);
+        // the next sub-chunk's domain (its sigma = this sub-chunk's last byte), loaded now
+        // beside this one's so that the epilogue's rank conversion waits for one load only
+        const bool to_rank = g_log != kNoGroup && i + 1 < p.NS && !(p.indep && chunk_first_sub(p, i + 1));
+        const uint32_t nd_pre = to_rank ? (uint32_t)T.byte_class[__ldg(in + end - 1)] : 0u;
         dom_of[i] = (uint16_t)dom;
         uint32_t u;
         uint64_t pos;
@@ -671,10 +675,9 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
             // rank space: final states as ranks in the next sub-chunk's domain
             // I_sigma, sigma = this sub-chunk's last byte (absolute for error
             // states and for the input's last sub-chunk)
-            if (i + 1 < p.NS && !(p.indep && chunk_first_sub(p, i + 1))) {
+            if (to_rank) {
                 // rank = position in the next domain's row (<= 8 entries, one 16-byte load)
-                const uint32_t nd = T.byte_class[__ldg(in + end - 1)];
-                const uint4 nr = __ldg(reinterpret_cast<const uint4 *>(T.dom_list + (uint64_t)nd * 8));
+                const uint4 nr = __ldg(reinterpret_cast<const uint4 *>(T.dom_list + (uint64_t)nd_pre * 8));
                 const uint32_t w[4] = {nr.x, nr.y, nr.z, nr.w};
 #pragma unroll
                 for (int l = 0; l < kLanes; l++) {
