@@ -129,3 +129,25 @@ def test_host_only_handle_refuses_compute():
         assert e.value.status == D.DFA_ERR_ARG
     finally:
         D.dfa_destroy(h)
+
+
+@pytest.mark.parametrize("name,make,mode", [
+    ("tiny", lambda: W.get("tiny").automaton, "ident_u8_pad"),          # < 32 states: one padded copy
+    ("random", lambda: W.get("random").automaton, "rep8_u8"),           # 64 states: 8 bank-group copies
+    ("keyword", lambda: W.get("keyword").automaton, "ident_u8_pad"),    # 217 states: too big for 8 copies
+    ("protein", lambda: W.get("protein").automaton, "window_u16"),      # 342 states, residue window
+    ("worst", lambda: W.get("worst").automaton, "packed9"),             # 512 states x 256 columns
+    ("sink256", lambda: automata.random_dfa_with_sink(40, 256, 2, 0.6), "rep8_u8"),
+    ("poison", lambda: automata.random_dfa(109, 20, 3), "rep8_u8"),     # 109 + poison = 110 states
+    ("poison111", lambda: automata.random_dfa(110, 20, 3), "ident_u8_pad"),
+])
+def test_table_layout_choice(name, make, mode):
+    """Host-side layout selection: replicated copies while
+    8 x |Q'| x 256 bytes fit the 223 KiB lanes-kernel budget and |Q'| >= 32, else
+    padded rows up to 252 states, then the window / packed / global layouts."""
+    h = host_handle(make())
+    try:
+        info = D.dfa_get_info(h)
+        assert D.TABLE_MODES[info["table_mode"]] == mode, (name, D.TABLE_MODES[info["table_mode"]])
+    finally:
+        D.dfa_destroy(h)
