@@ -61,6 +61,7 @@ def parse():
                     help="N2 ablation: match every sub-chunk from all of Q minus Z (Alg.2, P:753-790)")
     ap.add_argument("--no-batch", action="store_true", help="skip the multi-input batch (N4) report")
     ap.add_argument("--no-lookahead", action="store_true", help="skip the r-symbol lookahead (N1) report")
+    ap.add_argument("--no-ceiling", action="store_true", help="skip the table layout's gather ceiling (roofline.lds_ceiling)")
     ap.add_argument("--quiet-json", action="store_true", help="print a one-line summary instead of JSON")
     return ap.parse_args()
 
@@ -315,6 +316,29 @@ def main():
         dist.barrier() if dist else None
         return 0
 
+    # practical ceiling of the table layout on this input: the lanes kernel's match step
+    # alone (dfa_gather_ceiling: one lane per thread from q0, no method bookkeeping)
+    ceiling = None
+    if not args.no_ceiling:
+        nt, per = D.dfa_gather_ceiling(d.h, dx, None, stream=stream)
+        if per > 0:
+            cout = torch.empty(nt, dtype=torch.int16, device=dev)
+            for _ in range(3):
+                D.dfa_gather_ceiling(d.h, dx, cout, stream=stream)
+            torch.cuda.synchronize(dev)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            csteps = 20
+            c0.record(stream)
+            for _ in range(csteps):
+                D.dfa_gather_ceiling(d.h, dx, cout, stream=stream)
+            c1.record(stream)
+            torch.cuda.synchronize(dev)
+            cms = c0.elapsed_time(c1) / csteps
+            ceiling = {"kernel": "ceiling_kernel (dfa_gather_ceiling)", "threads": nt, "bytes_per_thread": per,
+                       "bytes_per_launch": nt * per, "ms": cms, "GBps": nt * per / (cms * 1e-3) / 1e9,
+                       "note": "the match step alone with this table layout: one lane per thread from q0, "
+                               "no I_sigma lanes, convergence checks, maps or composition"}
+
     # roofline of the dominant kernel (the lanes kernel) and of the whole step
     hbm_peak, sm_max, peak_src = peaks()
     km = stats.get("kernel_ms", {})
@@ -346,6 +370,8 @@ def main():
     f_clk = (clocks["sm_mhz"] or sm_max) * 1e6
     lds_peak = 148 * 32 * f_clk
     achieved = n / (lanes_ms * 1e-3) / 1e9 if lanes_ms else None
+    if ceiling and achieved:
+        ceiling["lanes_kernel_frac"] = achieved / ceiling["GBps"]
     t_star = max(n / (hbm_peak * 1e9), L_alg / (148 * 32 * 1965e6))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -368,6 +394,7 @@ def main():
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
                      "traffic_source": traffic_src,
                      "kernel": "lanes_kernel", "algorithmic_bytes_per_launch": n, "kernel_ms": lanes_ms,
+                     "lds_ceiling": ceiling,
                      "peak_source": peak_src,
                      "step_frac_of_hbm": (n / (ms * 1e-3) / 1e9) / hbm_peak,
                      "lookup": {"L_alg": L_alg, "lookups_per_s": L_alg / (ms * 1e-3),

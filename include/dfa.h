@@ -239,6 +239,23 @@ dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t le
 dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uint8_t *dev_lookahead,
                              uint32_t G, void *stream, uint16_t *dev_final);
 
+/*
+ * Measurement aid (not part of the method): the match kernel's step alone.
+ * T = *out_threads threads each run ONE lane from q0 over their own
+ * *out_per_thread consecutive bytes of dev_input (a multiple of 32; the first
+ * T * per bytes are used) with the handle's table layout, load pattern and
+ * 16-byte block step, and none of the method's bookkeeping (domains I_sigma,
+ * convergence checks, maps, composition).  Its throughput is the practical
+ * ceiling of the layout on this input, reported beside the lanes kernel's
+ * (bench.py roofline.lds_ceiling).  dev_out[t] (device, caller-owned, >= T
+ * entries; query T first by passing dev_out = NULL) = delta-hat(q0, bytes of
+ * thread t) (Alg.seqmatch over that range, checkable against the oracle).
+ * dev_input must be 32-byte aligned and len >= 32 * T, else DFA_ERR_ARG.
+ * Bad symbols are not detected.  Asynchronous.
+ */
+dfa_status dfa_gather_ceiling(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, void *stream,
+                              uint16_t *dev_out, uint64_t *out_per_thread, uint32_t *out_threads);
+
 /* After a stream sync: DFA_ERR_SYMBOL / DFA_ERR_INTERNAL raised by the last
  * asynchronous call's kernels, else DFA_OK.  Clears the flag. */
 dfa_status dfa_get_last_device_error(dfa_handle_t h);

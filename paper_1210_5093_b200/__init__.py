@@ -22,7 +22,7 @@ __all__ = [
     "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
     "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
     "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
-    "dfa_lookahead_maps", "dfa_match_batch", "Dfa", "lib", "EXPORTED",
+    "dfa_lookahead_maps", "dfa_match_batch", "dfa_gather_ceiling", "Dfa", "lib", "EXPORTED",
 ]
 
 DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
@@ -66,7 +66,7 @@ EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_d
             "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
             "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
             "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
-            "dfa_lookahead_maps", "dfa_match_batch"]
+            "dfa_lookahead_maps", "dfa_match_batch", "dfa_gather_ceiling"]
 
 _lib = None
 
@@ -99,6 +99,7 @@ def lib():
             "dfa_fold_segments": [V, V, V, u32, V, V],
             "dfa_lookahead_maps": [V, V, u64, u32, V, V, u32, V, V, V, V],
             "dfa_match_batch": [V, V, u64, V, u32, V, V, V],
+            "dfa_gather_ceiling": [V, V, u64, V, V, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -257,6 +258,18 @@ def dfa_segment_map(h, dev_input, lookahead: int, dev_row, n: Optional[int] = No
     n = dev_input.numel() if n is None else int(n)
     _ck(lib().dfa_segment_map(h, _ptr(dev_input), n, int(lookahead), _stream(stream), _ptr(dev_row)),
         "dfa_segment_map")
+
+
+def dfa_gather_ceiling(h, dev_input=None, dev_out=None, stream=None, length=None):
+    """Measurement aid (include/dfa.h): run the match step alone, one lane per thread
+    from q0.  Returns (threads, bytes_per_thread); with dev_out None only queries them."""
+    per = ctypes.c_uint64(0)
+    nt = ctypes.c_uint32(0)
+    n = int(length if length is not None else (dev_input.numel() if dev_input is not None else 0))
+    _ck(lib().dfa_gather_ceiling(h, _ptr(dev_input) if dev_input is not None else None, n, _stream(stream),
+                                 _ptr(dev_out) if dev_out is not None else None, ctypes.byref(per),
+                                 ctypes.byref(nt)), "dfa_gather_ceiling")
+    return int(nt.value), int(per.value)
 
 
 def dfa_fold_segments(h, dev_rows, dev_lookahead, G: int, dev_final, stream=None):

@@ -1192,6 +1192,23 @@ dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uin
     return DFA_OK;
 }
 
+dfa_status dfa_gather_ceiling(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, void *stream,
+                              uint16_t *dev_out, uint64_t *out_per_thread, uint32_t *out_threads) {
+    dfa_status st = check_ready(h);
+    if (st != DFA_OK) return st;
+    if (!out_per_thread || !out_threads) return DFA_ERR_ARG;
+    const int threads = lanes_threads(h);
+    const int grid = h->sms * std::max(1, ceiling_occupancy(h->T, threads));
+    const uint64_t T = (uint64_t)grid * threads;
+    const uint64_t per = (len / T) & ~31ull;
+    *out_threads = (uint32_t)T;
+    *out_per_thread = per;
+    if (!dev_out) return DFA_OK;  // query
+    if (!dev_input || per == 0 || (reinterpret_cast<uintptr_t>(dev_input) & 31u)) return DFA_ERR_ARG;
+    CK(launch_ceiling(h->T, dev_input, per, dev_out, threads, grid, reinterpret_cast<cudaStream_t>(stream)));
+    return DFA_OK;
+}
+
 dfa_status dfa_get_last_device_error(dfa_handle_t h) {
     dfa_status st = check_ready(h);
     if (st != DFA_OK) return st;

@@ -784,6 +784,40 @@ __global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, con
 }
 
 // ---------------------------------------------------------------------------
+// ceiling_kernel (dfa_gather_ceiling, a measurement aid): the lanes kernel's
+// match step alone -- one lane per thread from q0 over `per` bytes, the same
+// table layout, 32-byte loads and 16-byte block step, no domains, convergence
+// checkpoints, maps or composition.  Its rate is the practical ceiling of the
+// layout on this input; out[t] = delta-hat(q0, in[t*per .. (t+1)*per)).
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) ceiling_kernel(DevTables T, const uint8_t *__restrict__ in, uint64_t per,
+                                                          uint16_t *__restrict__ out) {
+    extern __shared__ uint4 smem4[];
+    uint8_t *tsm = load_tables<MODE>(T, smem4, bits_words(T.nq));
+    __syncthreads();
+    Tab<MODE> tab;
+    tab.init(T, tsm);
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint8_t *p = in + tid * per;
+    uint32_t st[kLanes];
+#pragma unroll
+    for (int l = 0; l < kLanes; l++) st[l] = tab.enc(l == 0 ? T.q0 : 0u);
+    const uint64_t nblk = per >> 5;
+    if (nblk) {
+        U8x32 cur = ldg32(p);
+        for (uint64_t bi = 0; bi < nblk; bi++) {
+            U8x32 nxt = cur;
+            if (bi + 1 < nblk) nxt = ldg32(p + 32 * (bi + 1));
+            block16<1, MODE>(tab, cur.lo, st, 1u);
+            block16<1, MODE>(tab, cur.hi, st, 1u);
+            cur = nxt;
+        }
+    }
+    out[tid] = (uint16_t)(st[0] - tab.bias);
+}
+
+// ---------------------------------------------------------------------------
 // converge_kernel: one warp per sub-chunk, all |I_sigma| lanes in lock-step
 // (the lanes of Alg.MatchingInitialStates line 17 for one chunk), merging
 // lanes that reach equal states every kSubWindow bytes until <= kLanes remain.
@@ -1851,6 +1885,20 @@ void *lanes_ptr(bool sticky) { return sticky ? (void *)lanes_kernel<MODE, true> 
 template <int MODE>
 void *converge_ptr() { return (void *)converge_kernel<MODE>; }
 
+void *ceiling_fn(int mode) {
+    switch (mode) {
+    case kIdentU8: return (void *)ceiling_kernel<kIdentU8>;
+    case kRepU8x8: return (void *)ceiling_kernel<kRepU8x8>;
+    case kRepU8x4: return (void *)ceiling_kernel<kRepU8x4>;
+    case kIdentU8P: return (void *)ceiling_kernel<kIdentU8P>;
+    case kIdentU16: return (void *)ceiling_kernel<kIdentU16>;
+    case kWindowU8: return (void *)ceiling_kernel<kWindowU8>;
+    case kWindowU16: return (void *)ceiling_kernel<kWindowU16>;
+    case kPacked9: return (void *)ceiling_kernel<kPacked9>;
+    default: return (void *)ceiling_kernel<kGlobalU16>;
+    }
+}
+
 void *lanes_fn(const DevTables &T) {
     const bool st = T.has_sticky != 0;
     switch (T.mode) {
@@ -1942,6 +1990,8 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(ceiling_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)fold_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((void *)lookahead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192);
@@ -1986,6 +2036,18 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
 }
 
 const void *tree_fn() { return (const void *)tree_kernel; }
+
+int ceiling_occupancy(const DevTables &T, int threads) {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, ceiling_fn(T.mode), threads, lanes_smem_bytes(T));
+    return blocks;
+}
+
+cudaError_t launch_ceiling(const DevTables &T, const uint8_t *in, uint64_t per, uint16_t *out, int threads, int grid,
+                           cudaStream_t s) {
+    void *args[] = {(void *)&T, (void *)&in, (void *)&per, (void *)&out};
+    return cudaLaunchKernel(ceiling_fn(T.mode), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
+}
 
 #ifdef DFA_TREE_TIMING
 extern "C" int dfa_debug_tree_timing(unsigned long long *out, int reset) {

@@ -161,5 +161,8 @@ cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint3
 cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
                                  DevStatus *st, uint16_t *dev_final, cudaStream_t s);
 int probe_dynamic_smem_base(uint32_t *dev_scratch);
+int ceiling_occupancy(const DevTables &T, int threads);
+cudaError_t launch_ceiling(const DevTables &T, const uint8_t *in, uint64_t per, uint16_t *out, int threads, int grid,
+                           cudaStream_t s);
 
 } // namespace dfa

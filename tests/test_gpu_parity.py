@@ -571,6 +571,33 @@ def test_window_fast_and_slow_paths():
     check_match(c)
 
 
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_gather_ceiling_kernel(name):
+    """dfa_gather_ceiling (measurement aid): thread t's output is delta-hat(q0, its bytes)."""
+    w = W.get(name)
+    x = w.input(min(w.small_n, 1 << 22))
+    dx = torch.from_numpy(x).to(DEV)
+    d = D.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accept_bitmap)
+    try:
+        nt, per = D.dfa_gather_ceiling(d.h, dx, None)
+        if per == 0:
+            x = np.tile(x, 32 * nt // x.size + 1)[:32 * nt * 2]
+            dx = torch.from_numpy(x).to(DEV)
+            nt, per = D.dfa_gather_ceiling(d.h, dx, None)
+        assert per > 0 and per % 32 == 0
+        out = torch.empty(nt, dtype=torch.int16, device=DEV)
+        D.dfa_gather_ceiling(d.h, dx, out)
+        torch.cuda.synchronize()
+        got = u16(out)
+        od = oracle.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accepting)
+        for t in (0, 1, nt // 2, nt - 1):
+            assert got[t] == od.run(x[t * per:(t + 1) * per]), t
+        with pytest.raises(D.DfaError):
+            D.dfa_gather_ceiling(d.h, dx[1:], out, length=x.size - 1)  # misaligned
+    finally:
+        d.close()
+
+
 # ------------------------------------------------------------------ dfa_match_host pipeline + early exit (N4)
 @pytest.mark.parametrize("name", ["random", "keyword", "protein", "tiny"])
 @pytest.mark.parametrize("early", [0, 1])
