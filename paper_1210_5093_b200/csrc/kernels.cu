@@ -1376,15 +1376,6 @@ struct LMap {
     uint32_t v, dom, ok;
 };
 
-__device__ __forceinline__ LMap lmap_load(const uint16_t *rows, const uint16_t *doms, uint64_t r, bool ok) {
-    LMap m;
-    const uint32_t j = threadIdx.x & 7;
-    m.ok = ok;
-    m.v = ok ? __ldcg(rows + r * 8 + j) : (uint32_t)kNone;
-    m.dom = ok ? __ldcg(doms + r) : 0u;
-    return m;
-}
-
 // Tree step over the 4 maps of a warp: group g (g % 2gs == 0) <- group g+gs o g.
 __device__ __forceinline__ void lmap_merge(LMap &m, uint32_t gs) {
     const uint32_t lane = threadIdx.x & 31, g = lane >> 3;
@@ -1397,49 +1388,6 @@ __device__ __forceinline__ void lmap_merge(LMap &m, uint32_t gs) {
     const uint32_t nv = __shfl_sync(0xffffffffu, m.v, sb + (m.ok ? (rr & 7u) : (lane & 7u)));
     if (take) m.v = nv;
     if (lead && !m.ok) { m.dom = bdom; m.ok = 1; }
-}
-
-// acc (group 0) <- b (group 0) o acc
-__device__ __forceinline__ void lmap_then(LMap &acc, const LMap &b) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t bdom = __shfl_sync(0xffffffffu, b.dom, 0);
-    const uint32_t bok = __shfl_sync(0xffffffffu, b.ok, 0) && lane < 8;
-    const uint32_t rr = acc.v - kRank;
-    const bool take = bok && (!acc.ok || rr < (uint32_t)kLanes);
-    const uint32_t nv = __shfl_sync(0xffffffffu, b.v, acc.ok ? (rr & 7u) : (lane & 7u));
-    if (take) acc.v = nv;
-    if (bok && !acc.ok) { acc.dom = bdom; acc.ok = 1; }
-}
-
-// acc (group 0) <- maps [a, b) of (rows, doms) o acc, in order; the loads of
-// 16 maps are issued before their compositions.
-template <bool GLOBAL>
-__device__ __forceinline__ void warp_fold_range(const uint16_t *rows, const uint16_t *doms, uint32_t a, uint32_t b,
-                                                LMap &acc) {
-    const uint32_t g = (threadIdx.x & 31) >> 3, j = threadIdx.x & 7;
-#pragma unroll 1
-    for (uint32_t base = a; base < b; base += 16) {
-        LMap m[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const uint32_t r = base + 4 * q + g;
-            if (GLOBAL) m[q] = lmap_load(rows, doms, r, r < b);
-            else {
-                m[q].ok = r < b;
-                m[q].v = m[q].ok ? rows[r * 8 + j] : (uint32_t)kNone;
-                m[q].dom = m[q].ok ? doms[r] : 0u;
-            }
-        }
-        // the 4 batches side by side: within-batch tree, then pairs, then acc
-#pragma unroll
-        for (int q = 0; q < 4; q++) lmap_merge(m[q], 1);
-#pragma unroll
-        for (int q = 0; q < 4; q++) lmap_merge(m[q], 2);
-        lmap_then(m[0], m[1]);
-        lmap_then(m[2], m[3]);
-        lmap_then(m[0], m[2]);
-        lmap_then(acc, m[0]);
-    }
 }
 
 // Tree fold of the n >= 1 maps (rows, doms) in shared memory: each level,
