@@ -338,8 +338,9 @@ struct Outputs {
 };
 
 int lanes_threads(const dfa_handle *h) {
+    if (h->threads_auto && lanes_max_threads(h->T.mode) < 1024) return lanes_max_threads(h->T.mode);
     if (h->threads_auto && lanes_occupancy(h->T, 512) < 2) return 1024;
-    return h->threads;
+    return std::min(h->threads, lanes_max_threads(h->T.mode));
 }
 
 // Execution split of the P reporting chunks (chunk 0 into m0 sub-chunks, the
@@ -418,7 +419,7 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
     }
     // threads per CTA: spread the sub-chunks evenly over all SMs (one wave when possible)
     const uint64_t NS = (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m;
-    const int maxt = bps >= 2 ? 512 : 1024;
+    const int maxt = std::min(bps >= 2 ? 512 : 1024, lanes_max_threads(h->T.mode));
     uint64_t t = (NS + (uint64_t)h->sms * bps - 1) / ((uint64_t)h->sms * bps);
     t = (t + 31) / 32 * 32;
     sp.threads = h->threads_auto ? (int)std::min<uint64_t>(std::max<uint64_t>(t, 128), (uint64_t)maxt) : base_threads;

@@ -621,7 +621,7 @@ __device__ __forceinline__ void warp_compose(uint32_t mask, uint32_t g_log, uint
 }
 
 template <int MODE, bool STICKY>
-__global__ void __launch_bounds__(1024, 1) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                     const uint16_t *__restrict__ surv,
                                                     const uint8_t *__restrict__ surv_n,
                                                     const uint64_t *__restrict__ surv_pos,
