@@ -1198,7 +1198,9 @@ dfa_status dfa_gather_ceiling(dfa_handle_t h, const uint8_t *dev_input, uint64_t
     dfa_status st = check_ready(h);
     if (st != DFA_OK) return st;
     if (!out_per_thread || !out_threads) return DFA_ERR_ARG;
-    const int threads = lanes_threads(h);
+    // the step alone has one dependent chain per thread: it wants every warp slot (1024
+    // threads per CTA), whatever CTA size the lanes kernel picks for its own trade-offs
+    const int threads = 1024;
     const int grid = h->sms * std::max(1, ceiling_occupancy(h->T, threads));
     const uint64_t T = (uint64_t)grid * threads;
     const uint64_t per = (len / T) & ~31ull;
