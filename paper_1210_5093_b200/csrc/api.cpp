@@ -363,7 +363,7 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         // by a large table is pipe-bound at ~16 warps per SM (Worst, measured: 95k
         // sub-chunks 1499 GB/s, 151k 1388 GB/s): fewer, longer sub-chunks there
         if (h->convergence && h->T.imax > (uint32_t)kLanes && lanes_occupancy(h->T, 512) < 2)
-            target = target * 5 / 8;
+            target = std::min<uint64_t>(target, (uint64_t)h->sms * 1024 * 5 / 8);
         // converge_kernel work per sub-chunk is ~|I_sigma| lanes over the first few hundred
         // bytes whatever the sub-chunk length: keep sub-chunks >= 4 KiB on average so that
         // short inputs (dfa_match_host pieces, segments) are not all convergence

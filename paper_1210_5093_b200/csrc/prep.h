@@ -45,8 +45,10 @@ DFA_HD constexpr uint32_t rep_log_of(int mode) { return mode == kRepU8x8 ? 3u : 
 // lanes_kernel CTA size bound per layout.  rep8_u8 (one 131+ KB CTA per SM) runs
 // 640 threads: 102 registers (no spills) and longer sub-chunks, so fewer initial
 // I_sigma lane-steps; measured on Random 1868 GB/s vs 1746 at 1024 threads (sweep
-// 512..1024 in DESIGN.md section 4).  Every other layout: 1024 (64 registers).
-DFA_HD constexpr int lanes_max_threads(int mode) { return mode == kRepU8x8 ? 640 : 1024; }
+// 512..1024 in DESIGN.md section 4).  packed9 (176 KB, Worst) is bounded at 704
+// threads for 88 registers with its sub-chunk count unchanged (6.80 vs 6.99 ms).
+// Every other layout: 1024 (64 registers).
+DFA_HD constexpr int lanes_max_threads(int mode) { return mode == kRepU8x8 ? 640 : mode == kPacked9 ? 704 : 1024; }
 
 struct Prep {
     // user view
