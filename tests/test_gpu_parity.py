@@ -666,6 +666,28 @@ def check_batch(c: Case, lengths, seed=0):
         d.close()
 
 
+@pytest.mark.parametrize("nq,ns", [(40, 256), (80, 256), (109, 20)])
+def test_rep8_with_converge_stage(nq, ns):
+    """rep8_u8 (640-thread lanes kernel) on DFAs whose I_max > 8, so the converge kernel
+    (padded single copy) hands survivors to the replicated-table lanes kernel: chunk maps,
+    host-input pipeline and batches against the oracle."""
+    a = automata.random_dfa(nq, ns, 1000 + nq)
+    rng = np.random.default_rng(nq)
+    x = rng.integers(0, ns, 700001).astype(np.uint8)
+    c = Case(a, x, f"rep8conv{nq}")
+    d = c.handle()
+    try:
+        assert d.info["table_mode_name"] == "rep8_u8" and d.info["i_max"] > 8, d.info
+        D.dfa_set_option(d.h, D.DFA_OPT_HOST_PIECE, 1 << 20)  # several pipelined pieces
+        fin, acc = D.dfa_match_host(d.h, x)
+        assert fin == c.od.run(x)
+    finally:
+        d.close()
+    for P in (1, 33, 4000):
+        check_chunk_maps(c, P)
+    check_batch(c, [0, 1, 31, 32, 33, 1000, 4097] * 50, seed=nq)
+
+
 @pytest.mark.parametrize("name", list(W.CONFIGS))
 def test_match_batch_many_small(name):
     w = W.get(name)
