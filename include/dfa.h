@@ -90,7 +90,12 @@ enum {
     DFA_TABLE_WINDOW_U8 = 3,  /* smem, columns = byte window + default column  */
     DFA_TABLE_WINDOW_U16 = 4,
     DFA_TABLE_PACKED9 = 5,    /* smem, 9-bit states packed 3 per 32-bit word    */
-    DFA_TABLE_GLOBAL_U16 = 6  /* global memory through L1/__ldg                 */
+    DFA_TABLE_GLOBAL_U16 = 6, /* global memory through L1/__ldg                 */
+    DFA_TABLE_REP8_U8 = 7,    /* smem, IDENT_U8 image x 8 copies, copy g in banks
+                                 4g..4g+3, read by lanes l = g mod 8 (32..110 states) */
+    DFA_TABLE_REP4_U8 = 8,    /* same with 4 copies (only when forced)          */
+    DFA_TABLE_IDENT_U8_PAD = 9 /* smem, uint8 states, rows of 260 bytes: entry
+                                 (s, b) in bank (s + b/4) mod 32 (<= 252 states) */
 };
 
 /* dfa_create_ex flags */
