@@ -386,6 +386,12 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         const uint64_t Ls = std::max<uint64_t>(32, (n + target - 1) / target);
         sp.m0 = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (len0 + Ls / 2) / Ls), std::min<uint64_t>(len0, 1u << 30));
         sp.m = P > 1 ? (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (avg + Ls / 2) / Ls), minlen) : 1;
+        // rounding to the nearest split can exceed the resident threads, and the excess
+        // sub-chunks would run as a second wave (Protein P = 32768: 163,840 sub-chunks for
+        // 151,552 threads, 1694 GB/s; 2072 after rounding down)
+        const uint64_t slots = (uint64_t)h->sms * bps * std::min(bps >= 2 ? 512 : 1024, lanes_max_threads(h->T.mode));
+        while (sp.m > 1 && (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m > slots) sp.m--;
+        while (sp.m0 > 1 && (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m > slots) sp.m0--;
     } else {
         // sub-chunks of >= 32 bytes; m a multiple of the largest power-of-two group
         // g <= 32 that keeps >= 95% of the estimated split (whole groups per warp)
