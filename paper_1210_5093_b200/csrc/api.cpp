@@ -338,8 +338,7 @@ struct Outputs {
 };
 
 int lanes_threads(const dfa_handle *h) {
-    if (h->threads_auto && lanes_max_threads(h->T.mode) < 1024) return lanes_max_threads(h->T.mode);
-    if (h->threads_auto && lanes_occupancy(h->T, 512) < 2) return 1024;
+    if (h->threads_auto) return lanes_max_threads(h->T.mode);
     return std::min(h->threads, lanes_max_threads(h->T.mode));
 }
 
@@ -355,7 +354,9 @@ struct Split {
 Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb, bool explicit_bounds) {
     Split sp;
     const int base_threads = lanes_threads(h);
-    const int bps = std::max(1, std::min(2, lanes_occupancy(h->T, 512)));
+    // one CTA per SM of up to 1024 threads (lanes_max_threads) rather than two of 512 where
+    // the table would allow two: same warps, measured +0.5% (Protein) / +0.8% (Keyword)
+    const int bps = 1;
     uint64_t target = h->subchunk_target;
     if (target <= 0) {
         target = (uint64_t)h->sms * std::max(1, lanes_occupancy(h->T, base_threads)) * base_threads;
@@ -425,8 +426,11 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
     }
     // threads per CTA: spread the sub-chunks evenly over all SMs (one wave when possible)
     const uint64_t NS = (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m;
-    const int maxt = std::min(bps >= 2 ? 512 : 1024, lanes_max_threads(h->T.mode));
-    uint64_t t = (NS + (uint64_t)h->sms * bps - 1) / ((uint64_t)h->sms * bps);
+    // small splits (Tiny) keep two CTAs per SM where the table allows: shorter CTAs start sooner
+    const int bpt = NS * 2 >= (uint64_t)h->sms * lanes_max_threads(h->T.mode)
+                        ? bps : std::max(1, std::min(2, lanes_occupancy(h->T, 512)));
+    const int maxt = std::min(bpt >= 2 ? 512 : 1024, lanes_max_threads(h->T.mode));
+    uint64_t t = (NS + (uint64_t)h->sms * bpt - 1) / ((uint64_t)h->sms * bpt);
     t = (t + 31) / 32 * 32;
     sp.threads = h->threads_auto ? (int)std::min<uint64_t>(std::max<uint64_t>(t, 128), (uint64_t)maxt) : base_threads;
     return sp;
