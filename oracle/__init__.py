@@ -112,8 +112,9 @@ class Dfa:
                "oracle_run")
         return int(out[0])
 
+    # Alg.seqmatch lines 4-6: accept iff the final state is in F
     def accepts(self, x: np.ndarray) -> bool:
-        return bool(self.accepting[self.run(x)])
+        return bool(lib().oracle_accepts(_p(self.accept_bitmap), self.run(x)))
 
     def run_record(self, x: np.ndarray, positions: np.ndarray):
         x = np.ascontiguousarray(x, dtype=np.uint8)

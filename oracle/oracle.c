@@ -371,7 +371,9 @@ int oracle_fold(const uint16_t *delta, uint32_t nq, uint32_t ns,
 }
 
 /* Binary combining operation of Eq.MapReduction on dense maps
- * over Q: Lij[q] = Lj[Li[q]].  Used by the tests to check associativity. */
+ * over Q: Lij[q] = Lj[Li[q]].  Pinned by the hand-derived dense maps of
+ * Fig.motivDFA (L_{0,1,2}[q0] = q1, tests/golden/fig_motiv_dfa.json) and by
+ * compose(M(u), M(v)) == M(uv) against Alg.seqmatch runs. */
 void oracle_compose_dense(const uint16_t *Li, const uint16_t *Lj, uint32_t nq,
                           uint16_t *Lij) {
     for (uint32_t q = 0; q < nq; q++) Lij[q] = Lj[Li[q]];

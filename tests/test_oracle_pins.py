@@ -280,16 +280,41 @@ def test_p1_equals_sequential():
     assert maps.shape[0] == 0 and e0 == d.run(x)
 
 
-def test_compose_associative_dense():
+def test_compose_dense_paper_example(golden_dir):
+    """Eq.MapReduction on Fig.motivDFA's dense chunk maps, derived by
+    hand from the figure: L_{0,1,2}[q0] = q1 (accepted final P:243).
+    The reversed operand order (L_i[L_j[q]]) gives qE and fails here."""
+    g = load(golden_dir, "fig_motiv_dfa.json")
+    L0, L1, L2 = (np.array(g[k], np.uint16) for k in ("L0_dense", "L1_dense", "L2_dense"))
+    assert oracle.compose_dense(L0, L1).tolist() == g["L01_dense"]
+    assert oracle.compose_dense(L1, L2).tolist() == g["L12_dense"]
+    L012 = oracle.compose_dense(oracle.compose_dense(L0, L1), L2)
+    assert L012.tolist() == g["L012_dense"]
+    assert int(L012[g["q0"]]) == g["expected_final"]
+    # the printed part of L2 (P:723-731)
+    assert L2[[0, 1]].tolist() == g["L2_over_q0_q1"]
+
+
+def test_compose_dense_is_concatenation():
+    """Eq.MapReduction is the map of the concatenated chunk: with M(w)[q] =
+    delta-hat(q, w) (Alg.seqmatch from every start state, pinned separately),
+    compose_dense(M(u), M(v)) == M(uv) for random DFAs and strings.  A swapped
+    operand order or an index slip fails on non-commuting maps."""
     rng = np.random.default_rng(4)
-    for _ in range(50):
-        nq = int(rng.integers(1, 30))
+    for _ in range(40):
+        nq, ns = int(rng.integers(2, 30)), int(rng.integers(1, 6))
+        table = rng.integers(0, nq, (nq, ns)).astype(np.uint16)
+
+        def M(w):
+            return np.array([Dfa(table, q, []).run(w) for q in range(nq)], np.uint16)
+
+        u = rng.integers(0, ns, int(rng.integers(0, 12))).astype(np.uint8)
+        v = rng.integers(0, ns, int(rng.integers(0, 12))).astype(np.uint8)
+        assert oracle.compose_dense(M(u), M(v)).tolist() == M(np.concatenate([u, v])).tolist()
+        # associativity (a property the paper relies on for the binary reduction, P:812-818)
         A, B, C = (rng.integers(0, nq, nq).astype(np.uint16) for _ in range(3))
-        lhs = oracle.compose_dense(oracle.compose_dense(A, B), C)
-        rhs = oracle.compose_dense(A, oracle.compose_dense(B, C))
-        assert lhs.tolist() == rhs.tolist()
-        # Eq.MapReduction semantics: L_ij[q] = L_j[L_i[q]]
-        assert lhs.tolist() == [int(C[B[A[q]]]) for q in range(nq)]
+        assert (oracle.compose_dense(oracle.compose_dense(A, B), C).tolist()
+                == oracle.compose_dense(A, oracle.compose_dense(B, C)).tolist())
 
 
 def test_lemma1_containment():
