@@ -10,6 +10,12 @@
 #include "kernels.cuh"
 #include "prep.h"
 
+// Translation units: kernels.cu (DFA_TU_MAIN: composition kernels, launchers) and
+// kernels_m<MODE>.cu (DFA_TU_MODE = MODE: the match kernels of one table layout).
+#if !defined(DFA_TU_MODE)
+#define DFA_TU_MAIN 1
+#endif
+
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <utility>
@@ -961,6 +967,7 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
     }
 }
 
+#ifdef DFA_TU_MAIN  // composition, batch, lookahead, starts kernels: main translation unit only
 // ---------------------------------------------------------------------------
 // tree_kernel: the composition tree of Tree (kernels.cuh) in one launch.  Warps
 // take level-1 nodes; a warp that finishes a node bumps its parent's arrival
@@ -1828,37 +1835,70 @@ __global__ void __launch_bounds__(512) starts_kernel(DevTables T, Plan p, const 
     }
 }
 
-template <int MODE>
-void *lanes_ptr(bool sticky) { return sticky ? (void *)lanes_kernel<MODE, true> : (void *)lanes_kernel<MODE, false>; }
-template <int MODE>
-void *converge_ptr() { return (void *)converge_kernel<MODE>; }
+#endif  // DFA_TU_MAIN
+
+} // namespace
+
+// Per-layout kernel entry points, defined in the translation unit of that
+// layout (kernels_m<MODE>.cu): the template kernels of every layout compile in
+// parallel, and the main unit dispatches through these.
+#ifdef DFA_TU_MODE
+template <int M>
+void *converge_or_null() {
+    // the converge kernel runs the byte-table modes on the padded copy (converge_fn)
+    if constexpr (M == kIdentU8 || M == kRepU8x8 || M == kRepU8x4) return nullptr;
+    else return (void *)converge_kernel<M>;
+}
+#define DFA_DEFINE_MODE_ENTRIES(M)                                                                      \
+    template <> void *lanes_entry<M>(bool sticky) {                                                     \
+        return sticky ? (void *)lanes_kernel<M, true> : (void *)lanes_kernel<M, false>;                 \
+    }                                                                                                   \
+    template <> void *ceiling_entry<M>() { return (void *)ceiling_kernel<M>; }                          \
+    template <> void *converge_entry<M>() { return converge_or_null<M>(); }
+#if DFA_TU_MODE == 0
+DFA_DEFINE_MODE_ENTRIES(kIdentU8)
+DFA_DEFINE_MODE_ENTRIES(kIdentU16)
+DFA_DEFINE_MODE_ENTRIES(kWindowU8)
+DFA_DEFINE_MODE_ENTRIES(kWindowU16)
+DFA_DEFINE_MODE_ENTRIES(kPacked9)
+DFA_DEFINE_MODE_ENTRIES(kGlobalU16)
+DFA_DEFINE_MODE_ENTRIES(kRepU8x8)
+DFA_DEFINE_MODE_ENTRIES(kRepU8x4)
+DFA_DEFINE_MODE_ENTRIES(kIdentU8P)
+#else
+DFA_DEFINE_MODE_ENTRIES(DFA_TU_MODE)
+#endif
+#endif  // DFA_TU_MODE
+
+#ifdef DFA_TU_MAIN
+namespace {
 
 void *ceiling_fn(int mode) {
     switch (mode) {
-    case kIdentU8: return (void *)ceiling_kernel<kIdentU8>;
-    case kRepU8x8: return (void *)ceiling_kernel<kRepU8x8>;
-    case kRepU8x4: return (void *)ceiling_kernel<kRepU8x4>;
-    case kIdentU8P: return (void *)ceiling_kernel<kIdentU8P>;
-    case kIdentU16: return (void *)ceiling_kernel<kIdentU16>;
-    case kWindowU8: return (void *)ceiling_kernel<kWindowU8>;
-    case kWindowU16: return (void *)ceiling_kernel<kWindowU16>;
-    case kPacked9: return (void *)ceiling_kernel<kPacked9>;
-    default: return (void *)ceiling_kernel<kGlobalU16>;
+    case kIdentU8: return ceiling_entry<kIdentU8>();
+    case kRepU8x8: return ceiling_entry<kRepU8x8>();
+    case kRepU8x4: return ceiling_entry<kRepU8x4>();
+    case kIdentU8P: return ceiling_entry<kIdentU8P>();
+    case kIdentU16: return ceiling_entry<kIdentU16>();
+    case kWindowU8: return ceiling_entry<kWindowU8>();
+    case kWindowU16: return ceiling_entry<kWindowU16>();
+    case kPacked9: return ceiling_entry<kPacked9>();
+    default: return ceiling_entry<kGlobalU16>();
     }
 }
 
 void *lanes_fn(const DevTables &T) {
     const bool st = T.has_sticky != 0;
     switch (T.mode) {
-    case kIdentU8: return lanes_ptr<kIdentU8>(st);
-    case kRepU8x8: return lanes_ptr<kRepU8x8>(st);
-    case kRepU8x4: return lanes_ptr<kRepU8x4>(st);
-    case kIdentU8P: return lanes_ptr<kIdentU8P>(st);
-    case kIdentU16: return lanes_ptr<kIdentU16>(st);
-    case kWindowU8: return lanes_ptr<kWindowU8>(st);
-    case kWindowU16: return lanes_ptr<kWindowU16>(st);
-    case kPacked9: return lanes_ptr<kPacked9>(st);
-    default: return lanes_ptr<kGlobalU16>(st);
+    case kIdentU8: return lanes_entry<kIdentU8>(st);
+    case kRepU8x8: return lanes_entry<kRepU8x8>(st);
+    case kRepU8x4: return lanes_entry<kRepU8x4>(st);
+    case kIdentU8P: return lanes_entry<kIdentU8P>(st);
+    case kIdentU16: return lanes_entry<kIdentU16>(st);
+    case kWindowU8: return lanes_entry<kWindowU8>(st);
+    case kWindowU16: return lanes_entry<kWindowU16>(st);
+    case kPacked9: return lanes_entry<kPacked9>(st);
+    default: return lanes_entry<kGlobalU16>(st);
     }
 }
 // The converge kernel steps all lanes of one sub-chunk on the same byte (a
@@ -1869,12 +1909,12 @@ void *converge_fn(int mode) {
     case kIdentU8:
     case kIdentU8P:
     case kRepU8x8:
-    case kRepU8x4: return converge_ptr<kIdentU8P>();
-    case kIdentU16: return converge_ptr<kIdentU16>();
-    case kWindowU8: return converge_ptr<kWindowU8>();
-    case kWindowU16: return converge_ptr<kWindowU16>();
-    case kPacked9: return converge_ptr<kPacked9>();
-    default: return converge_ptr<kGlobalU16>();
+    case kRepU8x4: return converge_entry<kIdentU8P>();
+    case kIdentU16: return converge_entry<kIdentU16>();
+    case kWindowU8: return converge_entry<kWindowU8>();
+    case kWindowU16: return converge_entry<kWindowU16>();
+    case kPacked9: return converge_entry<kPacked9>();
+    default: return converge_entry<kGlobalU16>();
     }
 }
 
@@ -2115,5 +2155,7 @@ cudaError_t launch_starts(const DevTables &T, const Plan &p, const uint16_t *row
     const size_t smem = rb + (size_t)blk * T.rs * 2 + (size_t)blk * 2 + 16;
     return launch_pdl(starts_kernel, dim3(1), dim3(512), smem, s, T, p, row0, rows, dom, starts, st, mode, blk);
 }
+
+#endif  // DFA_TU_MAIN
 
 } // namespace dfa

@@ -161,6 +161,20 @@ cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint3
 cudaError_t launch_fold_segments(const DevTables &T, const uint16_t *rows, const uint8_t *lookahead, uint32_t G,
                                  DevStatus *st, uint16_t *dev_final, cudaStream_t s);
 int probe_dynamic_smem_base(uint32_t *dev_scratch);
+
+// Match kernels of one table layout (MODE = TableMode), one translation unit
+// each (kernels_m<MODE>.cu); nullptr where a layout has no such kernel.
+template <int MODE> void *lanes_entry(bool sticky);
+template <int MODE> void *ceiling_entry();
+template <int MODE> void *converge_entry();
+#define DFA_DECLARE_MODE_ENTRIES(M)                  \
+    template <> void *lanes_entry<M>(bool sticky);   \
+    template <> void *ceiling_entry<M>();            \
+    template <> void *converge_entry<M>();
+DFA_DECLARE_MODE_ENTRIES(1) DFA_DECLARE_MODE_ENTRIES(2) DFA_DECLARE_MODE_ENTRIES(3)
+DFA_DECLARE_MODE_ENTRIES(4) DFA_DECLARE_MODE_ENTRIES(5) DFA_DECLARE_MODE_ENTRIES(6)
+DFA_DECLARE_MODE_ENTRIES(7) DFA_DECLARE_MODE_ENTRIES(8) DFA_DECLARE_MODE_ENTRIES(9)
+#undef DFA_DECLARE_MODE_ENTRIES
 int ceiling_occupancy(const DevTables &T, int threads);
 cudaError_t launch_ceiling(const DevTables &T, const uint8_t *in, uint64_t per, uint16_t *out, int threads, int grid,
                            cudaStream_t s);
