@@ -105,6 +105,11 @@ enum {
                                   Q \ Z instead of I_sigma; results identical, i_max unchanged
                                   (API rows stay over I_sigma), speed shows the I_sigma win */
 };
+/* Force a shared-memory table layout (a DFA_TABLE_* value) instead of the
+ * default choice: flags |= DFA_CREATE_TABLE_MODE(m).  Used by the layout parity
+ * tests and the layout experiments; a layout that cannot hold the DFA falls back
+ * to the default choice (dfa_get_info reports the layout taken). */
+#define DFA_CREATE_TABLE_MODE(m) (((uint32_t)(m) & 0xFu) << 8)
 
 /*
  * dfa_create: validate and analyse a DFA, upload device tables.
@@ -284,7 +289,10 @@ enum {
                                     runs until at most this many lanes survive; larger domains without
                                     the converge stage take several passes */
     DFA_OPT_HOST_PIECE = 10,     /* dfa_match_host piece size in bytes (>= 1 MiB, default 32 MiB) */
-    DFA_OPT_EARLY_EXIT = 11      /* 1 (default): dfa_match_host stops at an absorbing running state */
+    DFA_OPT_EARLY_EXIT = 11,     /* 1 (default): dfa_match_host stops at an absorbing running state */
+    DFA_OPT_STICKY_PARKING = 12, /* 1 (default): park lanes in sticky states; 0 = off */
+    DFA_OPT_COUNT_WORK = 13      /* 1: the match kernels count the lane-steps (table lookups) they execute,
+                                    summed into dfa_stats.work_* until dfa_get_stats reads them; 0 (default) */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 
@@ -302,6 +310,11 @@ typedef struct {
     float kernel_ms[8];        /* summed section durations (DFA_OPT_PROFILE) */
     char kernel_name[8][32];
     uint64_t host_bytes;       /* bytes dfa_match_host copied to the device in its last call */
+    /* DFA_OPT_COUNT_WORK: executed lane-steps (one table lookup each) since the
+     * previous dfa_get_stats: [0] converge_kernel, [1] lanes_kernel (including
+     * the re-read of parked sticky lanes).  0 when the option is off. */
+    uint64_t work_lookups[2];
+    uint32_t work_calls;       /* calls summed in work_lookups */
 } dfa_stats;
 dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out);
 

@@ -37,6 +37,14 @@ DFA_OPT_GRAPHS = 8
 DFA_OPT_MAX_LANES = 9
 DFA_OPT_HOST_PIECE = 10
 DFA_OPT_EARLY_EXIT = 11
+DFA_OPT_STICKY_PARKING = 12
+DFA_OPT_COUNT_WORK = 13
+
+
+def DFA_CREATE_TABLE_MODE(m: int) -> int:
+    """dfa_create_ex flag forcing table layout m (a TABLE_MODES key), include/dfa.h."""
+    return (int(m) & 0xF) << 8
+
 TABLE_MODES = {1: "ident_u8", 2: "ident_u16", 3: "window_u8", 4: "window_u16", 5: "packed9", 6: "global_u16",
                7: "rep8_u8", 8: "rep4_u8", 9: "ident_u8_pad"}
 
@@ -51,7 +59,8 @@ class DfaStats(ctypes.Structure):
     _fields_ = [("input_bytes", ctypes.c_uint64), ("num_subchunks", ctypes.c_uint64),
                 ("num_kernels", ctypes.c_uint32),
                 ("profiled", ctypes.c_uint32), ("kernel_ms", ctypes.c_float * 8),
-                ("kernel_name", (ctypes.c_char * 32) * 8), ("host_bytes", ctypes.c_uint64)]
+                ("kernel_name", (ctypes.c_char * 32) * 8), ("host_bytes", ctypes.c_uint64),
+                ("work_lookups", ctypes.c_uint64 * 2), ("work_calls", ctypes.c_uint32)]
 
 
 class DfaError(RuntimeError):
@@ -295,6 +304,8 @@ def dfa_get_stats(h) -> dict:
     if s.profiled:
         d["kernel_ms"] = {bytes(s.kernel_name[i]).split(b"\0")[0].decode(): s.kernel_ms[i]
                           for i in range(8) if s.kernel_name[i][0]}
+    if s.work_calls:
+        d["work"] = {"converge": int(s.work_lookups[0]), "lanes": int(s.work_lookups[1]), "calls": int(s.work_calls)}
     return d
 
 

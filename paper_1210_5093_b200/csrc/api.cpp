@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -19,11 +20,17 @@ using namespace dfa;
 
 namespace {
 
+// Bumped whenever a scratch buffer is (re)allocated or a composition tree's
+// arrival counters are reset: a captured CUDA graph holds raw scratch pointers
+// and counter residues, so its replay key includes this generation.
+std::atomic<uint64_t> g_scratch_gen{0};
+
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap && p) return cudaSuccess;
+        g_scratch_gen++;
         if (p) { cudaFree(p); p = nullptr; cap = 0; }
         size_t want = std::max<size_t>(bytes, 256);
         cudaError_t e = cudaMalloc(&p, want);
@@ -78,6 +85,12 @@ struct dfa_handle {
     struct { uint32_t m0, m, g_log; int threads; } plan_split_c{};
     int fold_in_tree = 0;
     int max_lanes = kLanes;       // lanes per thread (DFA_OPT_MAX_LANES, 1..8)
+    uint32_t sticky_avail = 0;    // the DFA has sticky states (upload)
+    int sticky_parking = 1;       // DFA_OPT_STICKY_PARKING
+    int count_work = 0;           // DFA_OPT_COUNT_WORK
+    DevBuf work;                  // [2] u64 lane-step counters (converge, lanes)
+    bool work_pending = false;
+    uint32_t work_calls = 0;
     std::vector<uint64_t> tree_sig;
     HostPinned h_status, h_bounds;
     cudaEvent_t staging_done = nullptr;
@@ -233,7 +246,8 @@ dfa_status upload(dfa_handle *h) {
     T.sticky_bits = reinterpret_cast<const uint32_t *>(at(14));
     T.has_sticky = 0;
     for (uint32_t w : sticky) T.has_sticky |= w != 0;
-    if (getenv("DFA_NO_STICKY")) T.has_sticky = 0;  // experiments only
+    h->sticky_avail = T.has_sticky;
+    T.has_sticky = h->sticky_avail && h->sticky_parking;
     T.nq_user = p.nq_user;
     T.ns = p.ns;
     T.nq = nq;
@@ -317,7 +331,6 @@ uint32_t tree_fanin(const dfa_handle *h, int &rank_smem, int &smem_bytes) {
     // stage the uint8 rank table in shared memory when it leaves room for F >= 8
     rank_smem = 0;
     if (T.rank8 && (uint64_t)tree_fixed_bytes(T, 1) + (uint64_t)tree_slice_bytes(T, 8) * 8 <= cap) rank_smem = 1;
-    if (getenv("DFA_TREE_DBG") && (atoi(getenv("DFA_TREE_DBG")) & 4)) rank_smem = 0;
     const uint64_t fixed = (uint64_t)tree_fixed_bytes(T, rank_smem);
     const uint64_t budget = cap - fixed;
     uint32_t F = h->tree_fanin_cap;
@@ -379,7 +392,8 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         for (uint32_t k = 1; k < P; k++) minlen = std::min(minlen, hb[k + 1] - hb[k]);
         avg = (n - len0) / (P - 1);
     }
-    const bool warp_mode = h->T.rs == 8 && h->warp_compose && !h->fold_in_tree;
+    // compose8's last CTA folds <= 1024 CTA maps of <= 1024 chunks: P > 2^20 takes the tree path
+    const bool warp_mode = h->T.rs == 8 && h->warp_compose && !h->fold_in_tree && P <= (1u << 20);
     if (explicit_bounds) {
         sp.m0 = sp.m = 1;
         if (warp_mode) sp.g_log = 0;
@@ -444,8 +458,17 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     h->stats.input_bytes = 0;
     h->last_stream = s;
     CK(cudaMemsetAsync(h->status.p, 0, sizeof(DevStatus), s));
+    unsigned long long *work = nullptr;
+    if (h->count_work) {
+        CK(h->work.ensure(16));
+        if (!h->work_pending) CK(cudaMemsetAsync(h->work.p, 0, 16, s));
+        h->work_pending = true;
+        h->work_calls++;
+        work = h->work.as<unsigned long long>();
+    }
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
-              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in, o.indep ? 1u : 0u};
+              o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in, o.indep ? 1u : 0u,
+              work};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;
@@ -503,7 +526,6 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         // rank-space leaves (maps of <= 8 entries): leaf_fold passes while the
         // chunks hold more than 64 leaves, then compose8_kernel
         uint32_t L0 = m0 >> sp.g_log, Lm = P > 1 ? (m >> sp.g_log) : 1;
-        if (P > (1u << 20)) return DFA_ERR_INTERNAL;
         CK(h->lvlA.ensure((uint64_t)P * T.rs * 2));
         CK(h->domA.ensure((uint64_t)P * 2));
         uint16_t *lrows = h->leaf_rows.as<uint16_t>(), *ldom = h->leaf_dom.as<uint16_t>();
@@ -553,7 +575,6 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     int tree_smem = 0;
     const uint32_t F = tree_fanin(h, tr.rank_smem, tree_smem);
     tr.F = F;
-    tr.dbg = getenv("DFA_TREE_DBG") ? atoi(getenv("DFA_TREE_DBG")) : 0;
     {
         uint32_t L = 0;
         uint64_t total = 0;
@@ -595,6 +616,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         // the child counts), zeroed when the tree changes
         std::vector<uint64_t> sig = {total, F, L, (uint64_t)m0, (uint64_t)m, (uint64_t)P, (uint64_t)gl};
         if (sig != h->tree_sig || h->counters.cap < total * 4) {
+            g_scratch_gen++;
             CK(h->counters.ensure(total * 4));
             CK(cudaMemsetAsync(h->counters.p, 0, total * 4, s));
             h->tree_sig = sig;
@@ -691,7 +713,7 @@ dfa_status fetch_status(dfa_handle *h, cudaStream_t s, DevStatus &out) {
 // the caller's stream.  Later calls: cudaGraphLaunch only.
 template <class Body>
 dfa_status run_graphed(dfa_handle *h, const std::vector<uint64_t> &gkey, cudaStream_t s, Body body) {
-    if (!h->use_graphs) return body(s);
+    if (!h->use_graphs || h->count_work) return body(s);  // counters: eager (memset + call count per call)
     if (h->graph_exec && gkey == h->graph_key) {
         CK(cudaGraphLaunch(h->graph_exec, s));
         h->recs = h->graph_recs;
@@ -705,6 +727,7 @@ dfa_status run_graphed(dfa_handle *h, const std::vector<uint64_t> &gkey, cudaStr
     }
     if (h->graph_exec) { cudaGraphExecDestroy(h->graph_exec); h->graph_exec = nullptr; }
     if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    const uint64_t gen0 = g_scratch_gen.load();
     h->recs.clear();
     h->ev_used = 0;
     CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed));
@@ -716,7 +739,8 @@ dfa_status run_graphed(dfa_handle *h, const std::vector<uint64_t> &gkey, cudaStr
     e = cudaGraphInstantiate(&h->graph_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(e, "cudaGraphInstantiate", __LINE__); }
-    h->graph_key = gkey;
+    // scratch reallocated while capturing: the graph would hold stale pointers
+    h->graph_key = g_scratch_gen.load() == gen0 ? gkey : std::vector<uint64_t>{};
     // the graph owns the events it records: take them out of the pool
     for (auto &gr : h->graph_recs) { cudaEventDestroy(gr.a); cudaEventDestroy(gr.b); }
     h->graph_recs = h->recs;
@@ -774,8 +798,10 @@ dfa_status dfa_create_ex(const uint16_t *table, uint32_t num_states, uint32_t al
         dfa_status ps = probe(h.get(), u8_limit);
         if (ps != DFA_OK) return ps;
     }
+    if (flags & ~(uint32_t)(DFA_CREATE_HOST_ONLY | DFA_CREATE_FULL_DOMAIN | DFA_CREATE_TABLE_MODE(0xF)))
+        return DFA_ERR_ARG;
     int st = prepare(table, num_states, alphabet_size, q0, accept_bitmap, budget, u8_limit, h->prep,
-                     (flags & DFA_CREATE_FULL_DOMAIN) != 0, rep_budget);
+                     (flags & DFA_CREATE_FULL_DOMAIN) != 0, rep_budget, (int)((flags >> 8) & 0xFu));
     if (st != 0) return (dfa_status)st;
     if (!(flags & DFA_CREATE_HOST_ONLY)) {
         dfa_status ds = upload(h.get());
@@ -807,7 +833,8 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         for (auto &e : h->ev_pool) if (e) cudaEventDestroy(e);
         if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
         for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
-        for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx})
+        for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx,
+                          &h->work})
             b->release();
         h->h_hm.release();
         h->h_batch.release();
@@ -985,9 +1012,9 @@ dfa_status dfa_match_host(dfa_handle_t h, const uint8_t *host_input, uint64_t le
         o.user_row0 = rows + (size_t)g * imu;
         st = run(h, h->input.as<uint8_t>() + off, sz, 1, h->hm_bounds.as<uint64_t>() + 2 * g, sp, s, o);
         if (st != DFA_OK) return st;
-        CK(cudaMemcpyAsync(hst + g, h->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(launch_fold_segments(h->T, rows, h->hm_la.as<uint8_t>(), g + 1, h->status.as<DevStatus>(),
                                 h->hm_final.as<uint16_t>() + 2 * g, s));
+        CK(cudaMemcpyAsync(hst + g, h->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(hfin + 2 * g, h->hm_final.as<uint16_t>() + 2 * g, 4, cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(h->hm_ev[2 * g + 1], s));
         issued = g + 1;
@@ -1018,8 +1045,10 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     // the partition and its execution split depend on (n, P, c, options) only:
     // computed once, kept on the device, copied device-to-device per call
+    // (every input plan_split reads besides the device and the table layout, fixed per handle)
     const std::vector<uint64_t> key = {len, P, h->c_num, h->c_den, (uint64_t)h->subchunk_target,
-                                       (uint64_t)h->threads, (uint64_t)h->threads_auto, (uint64_t)h->warp_compose};
+                                       (uint64_t)h->threads, (uint64_t)h->threads_auto, (uint64_t)h->warp_compose,
+                                       (uint64_t)h->convergence, (uint64_t)h->fold_in_tree};
     if (key != h->plan_key) {
         st = stage_bounds(h, len, P);
         if (st != DFA_OK) return st;
@@ -1053,7 +1082,8 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
                        (uint64_t)(uintptr_t)dev_chunk_start, (uint64_t)(uintptr_t)dev_final, (uint64_t)h->profile,
                        (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
                        (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
-                       (uint64_t)h->threads})
+                       (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work,
+                       (uint64_t)g_scratch_gen.load()})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
 }
@@ -1259,6 +1289,13 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
     case DFA_OPT_FOLD_IN_TREE:
         h->fold_in_tree = value ? 1 : 0;
         return DFA_OK;
+    case DFA_OPT_STICKY_PARKING:
+        h->sticky_parking = value ? 1 : 0;
+        h->T.has_sticky = h->sticky_avail && h->sticky_parking;
+        return DFA_OK;
+    case DFA_OPT_COUNT_WORK:
+        h->count_work = value ? 1 : 0;
+        return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         h->threads_auto = value == 0;
         if (value == 0) value = 512;
@@ -1287,6 +1324,18 @@ dfa_status dfa_get_stats(dfa_handle_t h, dfa_stats *out) {
         s.profiled = calls;
         h->recs.clear();
         h->ev_used = 0;
+    }
+    s.work_lookups[0] = s.work_lookups[1] = 0;
+    s.work_calls = 0;
+    if (h->device_ready && h->work_pending) {
+        unsigned long long w[2] = {0, 0};
+        if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
+        CK(cudaMemcpy(w, h->work.p, 16, cudaMemcpyDeviceToHost));
+        s.work_lookups[0] = w[0];
+        s.work_lookups[1] = w[1];
+        s.work_calls = h->work_calls;
+        h->work_pending = false;
+        h->work_calls = 0;
     }
     *out = s;
     return DFA_OK;

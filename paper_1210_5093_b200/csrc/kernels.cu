@@ -326,6 +326,14 @@ __device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem,
 
 __device__ __forceinline__ uint32_t bits_words(uint32_t nq) { return ((nq + 31) / 32 + 3) & ~3u; }
 
+// DFA_OPT_COUNT_WORK: a warp's executed lane-steps into one 64-bit counter
+// (called by every thread of the warp at kernel end).
+__device__ __forceinline__ void add_work(unsigned long long *ctr, uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o /= 2) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(ctr, (unsigned long long)v);
+}
+
 // ---------------------------------------------------------------------------
 // lanes_kernel: one thread per execution sub-chunk, <= kLanes lanes in registers.
 // ---------------------------------------------------------------------------
@@ -517,7 +525,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
                                           const uint32_t *sticky, const uint32_t *deadb,
                                           const uint8_t *in, uint64_t pos,
                           uint64_t end, uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t nl,
-                          int convergence, uint32_t (&fin)[kLanes]) {
+                          int convergence, uint32_t (&fin)[kLanes], uint32_t &wk) {
     uint32_t nlive = nl;
     const uint8_t *s0 = in + pos;
     const uint8_t *ptr = s0;
@@ -525,7 +533,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
     uint32_t pend = kNoPend, pend_off = 0;
     const bool susp = STICKY && convergence;
     // head: up to 31 bytes until 32-byte alignment
-    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) step_scalar(tab, *ptr++, st, nlive);
+    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) { wk += nlive; step_scalar(tab, *ptr++, st, nlive); }
     for (;;) {
         bool restart = false;
         const uint32_t nblk = (uint32_t)((uint64_t)(endp - ptr) >> 5);  // sub-chunks < 128 GiB
@@ -542,6 +550,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
                     const bool tick = half && (bi & 1);
                     const bool sp = susp && half;
                     const uint32_t co = (uint32_t)(nptr - s0);
+                    wk += 16u * max(nlive, 1u);  // block16: lane 0 always steps (DFA_OPT_COUNT_WORK)
                     bool done;
                     switch (__reduce_max_sync(__activemask(), nlive)) {
                     case 0:
@@ -565,7 +574,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
             if (!restart) ptr += (uint64_t)nblk * 32;
         }
         if (!restart) {
-            while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
+            while (ptr < endp) { wk += nlive; step_scalar(tab, *ptr++, st, nlive); }
             if (pend == kNoPend) break;
             bool alive = false;  // a live, non-error lane witnesses that no kill byte came
 #pragma unroll
@@ -659,6 +668,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     Tab<MODE> tab;
     tab.init(T, tsm);
     const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
+    uint64_t work = 0;  // executed lane-steps of this thread (DFA_OPT_COUNT_WORK)
 
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -738,8 +748,10 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
                 }
                 fin[l] = kNone;
             }
+            uint32_t wk = 0;
             if (nl) run_lanes<MODE, STICKY>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
-                                            convergence, fin);
+                                            convergence, fin, wk);
+            work += wk;
 #ifdef DFA_TREE_TIMING
             if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[27], gtimer());
 #endif
@@ -787,6 +799,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
 #ifdef DFA_TREE_TIMING
     if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[29], gtimer());
 #endif
+    if (p.work) add_work(p.work + 1, work);
 }
 
 // ---------------------------------------------------------------------------
@@ -854,6 +867,7 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
     __syncthreads();
 
     const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint64_t work = 0;  // lane-steps of this warp (counted on lane 0; DFA_OPT_COUNT_WORK)
     for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; i < p.NS; i += warps_total) {
         uint64_t start, end;
         sub_range(p, i, start, end);
@@ -893,9 +907,20 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
                 }
                 if (k0 == 0 && k1 == 16) {
                     // a full aligned window: the match kernel's 16-byte step (static byte
-                    // selection, per-word column preparation)
+                    // selection, per-word column preparation) on B = ceil(lanes left / 32)
+                    // lanes per thread -- the pool shrinks fast (Worst: 240 lanes, ~30
+                    // after the first window), so later windows step 1-2 lanes, not 8
                     const uint32_t nact = np > base + lane ? min((uint32_t)kConvergeLA, (np - base - lane + 31u) / 32u) : 0u;
-                    block16<kConvergeLA, MODE>(tab, v, s, nact);
+                    switch (min((uint32_t)kConvergeLA, (np - base + 31u) / 32u)) {
+                    case 1: block16<1, MODE>(tab, v, s, nact); break;
+                    case 2: block16<2, MODE>(tab, v, s, nact); break;
+                    case 3: block16<3, MODE>(tab, v, s, nact); break;
+                    case 4: block16<4, MODE>(tab, v, s, nact); break;
+                    case 5: block16<5, MODE>(tab, v, s, nact); break;
+                    case 6: block16<6, MODE>(tab, v, s, nact); break;
+                    case 7: block16<7, MODE>(tab, v, s, nact); break;
+                    default: block16<kConvergeLA, MODE>(tab, v, s, nact); break;
+                    }
                 } else {
                     for (uint32_t k = k0; k < k1; k++) {
                         const uint32_t wsel = k >> 2;
@@ -913,6 +938,7 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
                 }
             }
             pos = abase + k1;
+            if (lane == 0) work += (uint64_t)(k1 - k0) * np;
             __syncwarp();
             // merge lanes with equal states (leader = first in pool order),
             // retire lanes in absorbing states, compact the pool in place.
@@ -965,6 +991,7 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
         }
         __syncwarp();
     }
+    if (p.work) add_work(p.work, work);
 }
 
 #ifdef DFA_TU_MAIN  // composition, batch, lookahead, starts kernels: main translation unit only
@@ -1112,7 +1139,7 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
             __syncwarp();
             // pairwise tree over the children in the warp: in round `step`, map a
             // (a = 0, 2step, ...) absorbs map a+step: L_a <- L_{a+step} o L_a
-            for (uint32_t step = 1; step < nc && !(tr.dbg & 1); step *= 2) {
+            for (uint32_t step = 1; step < nc; step *= 2) {
                 const uint32_t npairs = (nc - step + 2 * step - 1) / (2 * step);
                 if (lrs <= 4) {
                     // short rows: (pair, entry) tasks packed across the lanes, 4 deep
@@ -1179,8 +1206,7 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
             const uint32_t nchild = p1 - p0;
             __syncwarp();
             uint32_t prev = 0;
-            if (lane == 0 && (tr.dbg & 2)) prev = atomicAdd(tr.counters + up.off + parent, 1u);
-            else if (lane == 0) {
+            if (lane == 0) {
                 // release: this node's row (written by all lanes, ordered by the
                 // syncwarp) before the count; acquire: the siblings' rows after it.
                 // A release/acquire RMW, not fence.sc: thousands of warps do this.
@@ -1706,7 +1732,9 @@ __global__ void fold_segments_kernel(DevTables T, const uint16_t *rows, const ui
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint32_t s = rows[0];
     for (uint32_t g = 1; g < G; g++) {
-        if (s == kNone || test_bit(T.dead_bits, s)) continue;
+        // error states pass through: the internal Z (poison included) and the
+        // user's Z, whose states are absorbing over Sigma but not over bytes >= |Sigma|
+        if (s == kNone || test_bit(T.dead_bits, s) || (s < T.nq_user && test_bit(T.dead_user_bits, s))) continue;
         const uint32_t d = T.byte_class[lookahead[g]];
         const uint32_t r = T.rank[(uint64_t)d * T.nq + s];
         const uint32_t ju = r == kNone ? kNone : T.ixlat[(uint64_t)d * T.rs + r];
@@ -1974,8 +2002,14 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaError_t e = cudaFuncSetAttribute(lanes_fn(T), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    if (e != cudaSuccess) return e;
+    // both lanes kernel variants: DFA_OPT_STICKY_PARKING switches between them
+    DevTables T2 = T;
+    for (uint32_t st = 0; st < 2; st++) {
+        T2.has_sticky = st;
+        cudaError_t e = cudaFuncSetAttribute(lanes_fn(T2), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e;
     e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(ceiling_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);

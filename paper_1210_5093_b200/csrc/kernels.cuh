@@ -61,6 +61,7 @@ struct Plan {
     uint32_t first_dom;      // domain of sub-chunk 0: start_dom ({q0}) or a lookahead class
     uint64_t in_addr;        // device address of the input (split alignment)
     uint32_t indep;          // batch: every chunk is an independent input matched from q0
+    unsigned long long *work; // DFA_OPT_COUNT_WORK: [0] converge, [1] lanes lane-steps; else null
 };
 
 struct DevStatus {
@@ -98,7 +99,6 @@ struct Tree {
     uint32_t F;              // staging capacity (children per node) of a warp
     uint32_t lrs;            // log2 of the shared-memory row stride (>= T.rs)
     int rank_smem;           // uint8 rank table staged in shared memory
-    int dbg;                 // debug experiment bits (0 in production)
     int root_final;          // the top level is the root: write the final state
     TreeLevel lv[kMaxLevels + 1];
     // leaves (lanes kernel output)

@@ -42,7 +42,7 @@ uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uin
 
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
             const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &p,
-            bool full_domain, uint32_t rep_budget) {
+            bool full_domain, uint32_t rep_budget, int forced_mode) {
     if (!table || !accept_bitmap) return ST_ARG;
     if (ns == 0 || ns > 256) return ST_ALPHABET;
     if (nq == 0 || nq > kMaxStates || q0 >= nq) return ST_STATES;
@@ -165,8 +165,7 @@ int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
         if (!(w & 1)) w++;
         return w;
     };
-    const char *force = getenv("DFA_TABLE_MODE");  // experiments only
-    const int fm = force ? atoi(force) : 0;
+    const int fm = forced_mode;  // DFA_CREATE_TABLE_MODE (tests, layout experiments)
     if (fm == kIdentU16 && (size_t)p.nq * 512 <= smem_budget) {
         p.mode = kIdentU16;
         p.stride = 256;

@@ -96,7 +96,7 @@ struct Prep {
 // shared-address bias of the table, see Tab<kIdentU8> in kernels.cu).
 int prepare(const uint16_t *table, uint32_t nq, uint32_t ns, uint16_t q0,
             const uint8_t *accept_bitmap, uint32_t smem_budget, uint32_t u8_state_limit, Prep &out,
-            bool full_domain = false, uint32_t rep_budget = 0);
+            bool full_domain = false, uint32_t rep_budget = 0, int forced_mode = 0);
 
 // Exact c-form partition (header dfa.h), 128-bit integer arithmetic.
 uint64_t cform_bound(uint64_t n, uint32_t P, uint64_t c_num, uint64_t c_den, uint32_t k);

@@ -334,9 +334,32 @@ def test_segment_maps_fold(name, G):
     """Sharded path kernels on one GPU: G segment maps (dfa_segment_map) folded
     by dfa_fold_segments == the sequential run; rows == the oracle's chunk maps."""
     w = W.get(name)
-    n = 1 << 19
-    x = w.input(n)
-    c = Case(w.automaton, x, name)
+    check_segment_fold(Case(w.automaton, w.input(1 << 19), name), G)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_segment_fold_small_alphabet_sink(seed):
+    """|Sigma| < 256 with a user error state q_E: q_E is not internally absorbing (bytes
+    >= |Sigma| lead to the poison state) but the fold must pass it through
+    like any error state; the running state reaches q_E early (sink_frac 0.3)."""
+    a = automata.random_dfa_with_sink(40, 20, seed, 0.3)
+    rng = np.random.default_rng(seed)
+    c = Case(a, rng.integers(0, 20, 1 << 19).astype(np.uint8), "sink")
+    assert c.od.run(c.x) == 39  # the run ends in q_E
+    check_segment_fold(c, 2 + seed)
+    # the pipelined host path folds its pieces the same way
+    d = c.handle({D.DFA_OPT_HOST_PIECE: 1 << 20})
+    try:
+        x3 = np.tile(c.x, 5)
+        fin, acc = D.dfa_match_host(d.h, torch.from_numpy(x3).pin_memory())
+        assert (fin, acc) == (c.od.run(x3), False)
+    finally:
+        d.close()
+
+
+def check_segment_fold(c: Case, G: int):
+    x = c.x
+    n = x.size
     rng = np.random.default_rng(G)
     cuts = np.sort(rng.choice(np.arange(1, n), G - 1, replace=False))
     b = np.concatenate([[0], cuts, [n]]).astype(np.uint64)
@@ -519,11 +542,11 @@ def test_max_lanes(name, cap):
 
 # ------------------------------------------------------------------ shared-memory table layouts
 @pytest.mark.parametrize("mode", [1, 7, 8, 9])
-def test_table_layouts(mode, monkeypatch):
+def test_table_layouts(mode):
     """IdentU8, its bank-group replicas (R = 8, 4 copies) and its padded-row form
      give identical results: the five-config DFAs that fit, a small-alphabet DFA
     with a sink (poison state), a sticky-parking DFA and misaligned input."""
-    monkeypatch.setenv("DFA_TABLE_MODE", str(mode))
+    flags = D.DFA_CREATE_TABLE_MODE(mode)
     cases = []
     for name in ("tiny", "random", "keyword"):
         w = W.get(name)
@@ -537,17 +560,17 @@ def test_table_layouts(mode, monkeypatch):
     xs[rng.choice(xs.size, 9, replace=False)] = 255
     cases.append((Case(s, xs, "sticky"), 333))
     for c, P in cases:
-        info = check_chunk_maps(c, P)
+        info = check_chunk_maps(c, P, flags=flags)
         nq = c.a.table.shape[0] + (1 if c.a.table.shape[1] < 256 else 0)
         want = {1: "ident_u8", 7: "rep8_u8" if nq * 2048 + 2048 <= 223 * 1024 else "ident_u8_pad",
                 8: "rep4_u8" if nq * 1024 + 1024 <= 223 * 1024 else "ident_u8_pad", 9: "ident_u8_pad"}[mode]
         assert info["table_mode_name"] == want, (c.name, info["table_mode_name"])
-        check_match(c)
+        check_match(c, flags=flags)
     # misaligned device input
     w = W.get("random")
     x = w.input(1 << 20)
     buf = torch.from_numpy(np.concatenate([np.zeros(5, np.uint8), x])).to(DEV)
-    check_chunk_maps(Case(w.automaton, x, "random+5"), 300, dev=buf[5:])
+    check_chunk_maps(Case(w.automaton, x, "random+5"), 300, dev=buf[5:], flags=flags)
 
 
 def test_window_fast_and_slow_paths():
@@ -658,7 +681,10 @@ def check_batch(c: Case, lengths, seed=0):
         torch.cuda.synchronize()
         assert D.dfa_get_last_device_error(d.h) == 0
         gf, ga = u16(fin), acc.cpu().numpy()
-        for j in range(len(lengths)):
+        idx = range(len(lengths))
+        if len(lengths) > 20000:  # every input's result is independent: a seeded sample + both ends
+            idx = sorted(set(rng.choice(len(lengths), 20000, replace=False).tolist()) | {0, len(lengths) - 1})
+        for j in idx:
             x = data[int(offs[j]):int(offs[j + 1])]
             of = c.od.run(x)
             assert gf[j] == of and ga[j] == int(c.a.accepting[of]), f"input {j} (len {x.size})"
@@ -769,3 +795,92 @@ def test_sharded_path_nccl_world1():
         od = oracle.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accepting)
         f = od.run(w.input(1 << 20))
         assert err == 0 and fin == [f, int(w.automaton.accepting[f])], name
+
+
+# ------------------------------------------------------------------ round-2 hygiene: graph replay, limits, options
+def test_graph_replay_alternating_chunk_counts():
+    """A captured graph must never replay stale scratch: alternate P values (which
+    reallocate scratch and reshape the composition tree) with fixed output buffers."""
+    for name in ("random", "protein"):
+        w = W.get(name)
+        x = w.input(1 << 20)
+        c = Case(w.automaton, x, name)
+        d = c.handle()
+        try:
+            dx = torch.from_numpy(x).to(DEV)
+            imax = d.info["i_max"]
+            outs = {}
+            for P in (300, 65536):
+                outs[P] = (torch.empty(P + 1, dtype=torch.int64, device=DEV),
+                           torch.empty(1, dtype=torch.int16, device=DEV),
+                           torch.empty((P - 1) * imax, dtype=torch.int16, device=DEV),
+                           torch.empty(2, dtype=torch.int16, device=DEV))
+            want = {}
+            for P in outs:
+                ob = oracle.chunk_bounds_ratio(x.size, P, 1, 1)
+                want[P] = c.od.maps(x, ob, imax)
+            fin = c.od.run(x)
+            for P in (300, 300, 300, 65536, 300, 65536, 65536, 65536, 300, 300):
+                b, e0, maps, final = outs[P]
+                maps.fill_(0)
+                D.dfa_chunk_maps(d.h, dx, P, b, e0, maps, None, final)
+                torch.cuda.synchronize()
+                assert D.dfa_get_last_device_error(d.h) == 0
+                oe0, omaps = want[P]
+                assert u16(e0)[0] == oe0 and u16(final)[0] == fin, (name, P)
+                assert np.array_equal(u16(maps).reshape(omaps.shape), omaps), (name, P)
+        finally:
+            d.close()
+
+
+def test_more_than_2_20_chunks():
+    """P > 2^20 reporting chunks (compose8's limit) take the tree path; a batch of more
+    than 2^20 inputs likewise."""
+    w = W.get("random")
+    x = w.input(3 << 20)
+    c = Case(w.automaton, x, "random")
+    check_chunk_maps(c, (1 << 20) + 3)
+    check_batch(c, [2] * ((1 << 20) + 5), seed=3)
+
+
+def test_sticky_parking_option_off():
+    """DFA_OPT_STICKY_PARKING = 0 (the plain lanes kernel on a DFA with sticky states)."""
+    w = W.get("protein")
+    c = Case(w.automaton, w.input(1 << 20), "protein")
+    check_chunk_maps(c, 300, opts={D.DFA_OPT_STICKY_PARKING: 0})
+    check_chunk_maps(c, 300, opts={D.DFA_OPT_STICKY_PARKING: 1})
+
+
+@pytest.mark.parametrize("name", ["tiny", "random", "keyword"])
+def test_work_counter_is_L_alg(name):
+    """DFA_OPT_COUNT_WORK with convergence off and one execution sub-chunk per chunk
+    (dfa_chunk_maps_at): the lanes kernel's executed lane-steps are exactly L_alg =
+    len_0 + sum_k len_k |I_sigma_k| (Alg.3 runs |I_sigma| lanes over its
+    chunk; an empty I_sigma still steps one lane)."""
+    w = W.get(name)
+    x = w.input(1 << 20)
+    c = Case(w.automaton, x, name)
+    d = c.handle({D.DFA_OPT_CONVERGENCE: 0, D.DFA_OPT_COUNT_WORK: 1})
+    try:
+        P = 777
+        ob = oracle.chunk_bounds_ratio(x.size, P, 1, 1).astype(np.int64)
+        bounds = torch.from_numpy(ob).to(DEV)
+        imax = d.info["i_max"]
+        e0 = torch.empty(1, dtype=torch.int16, device=DEV)
+        maps = torch.empty((P - 1) * imax, dtype=torch.int16, device=DEV)
+        D.dfa_get_stats(d.h)
+        D.dfa_chunk_maps_at(d.h, torch.from_numpy(x).to(DEV), P, bounds, e0, maps)
+        torch.cuda.synchronize()
+        st = D.dfa_get_stats(d.h)
+        sizes = np.array([len(c.od.initial_states(int(s))) if s < w.automaton.ns else 0 for s in range(256)], np.int64)
+        lens = np.diff(ob)
+        L = int(lens[0] + (lens[1:] * np.maximum(sizes[x[ob[1:-1] - 1]], 1)).sum())
+        assert st["work"]["lanes"] == L and st["work"]["converge"] == 0 and st["work"]["calls"] == 1
+        # convergence on: executed work is below L_alg and at least n
+        D.dfa_set_option(d.h, D.DFA_OPT_CONVERGENCE, 1)
+        D.dfa_chunk_maps_at(d.h, torch.from_numpy(x).to(DEV), P, bounds, e0, maps)
+        torch.cuda.synchronize()
+        st = D.dfa_get_stats(d.h)
+        assert x.size <= st["work"]["lanes"] <= L
+    finally:
+        d.close()
