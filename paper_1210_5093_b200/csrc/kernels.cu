@@ -520,7 +520,7 @@ __device__ __forceinline__ void resume_pend(uint32_t &pend, uint32_t bias, uint3
     pend = kNoPend;
 }
 
-template <int MODE, bool STICKY>
+template <int MODE, bool STICKY, bool COUNT>
 __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *absorb, bool has_absorb,
                                           const uint32_t *sticky, const uint32_t *deadb,
                                           const uint8_t *in, uint64_t pos,
@@ -533,7 +533,10 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
     uint32_t pend = kNoPend, pend_off = 0;
     const bool susp = STICKY && convergence;
     // head: up to 31 bytes until 32-byte alignment
-    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) { wk += nlive; step_scalar(tab, *ptr++, st, nlive); }
+    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) {
+        if constexpr (COUNT) wk += nlive;
+        step_scalar(tab, *ptr++, st, nlive);
+    }
     for (;;) {
         bool restart = false;
         const uint32_t nblk = (uint32_t)((uint64_t)(endp - ptr) >> 5);  // sub-chunks < 128 GiB
@@ -550,7 +553,7 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
                     const bool tick = half && (bi & 1);
                     const bool sp = susp && half;
                     const uint32_t co = (uint32_t)(nptr - s0);
-                    wk += 16u * max(nlive, 1u);  // block16: lane 0 always steps (DFA_OPT_COUNT_WORK)
+                    if constexpr (COUNT) wk += 16u * max(nlive, 1u);  // block16: lane 0 always steps
                     bool done;
                     switch (__reduce_max_sync(__activemask(), nlive)) {
                     case 0:
@@ -574,7 +577,10 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
             if (!restart) ptr += (uint64_t)nblk * 32;
         }
         if (!restart) {
-            while (ptr < endp) { wk += nlive; step_scalar(tab, *ptr++, st, nlive); }
+            while (ptr < endp) {
+                if constexpr (COUNT) wk += nlive;
+                step_scalar(tab, *ptr++, st, nlive);
+            }
             if (pend == kNoPend) break;
             bool alive = false;  // a live, non-error lane witnesses that no kill byte came
 #pragma unroll
@@ -635,7 +641,9 @@ __device__ __forceinline__ void warp_compose(uint32_t mask, uint32_t g_log, uint
     }
 }
 
-template <int MODE, bool STICKY>
+// COUNT: the DFA_OPT_COUNT_WORK instantiation (a live counter register would make the
+// timed kernel spill, so counting is a separate instantiation)
+template <int MODE, bool STICKY, bool COUNT>
 __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                     const uint16_t *__restrict__ surv,
                                                     const uint8_t *__restrict__ surv_n,
@@ -749,7 +757,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
                 fin[l] = kNone;
             }
             uint32_t wk = 0;
-            if (nl) run_lanes<MODE, STICKY>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
+            if (nl) run_lanes<MODE, STICKY, COUNT>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
                                             convergence, fin, wk);
             work += wk;
 #ifdef DFA_TREE_TIMING
@@ -799,7 +807,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
 #ifdef DFA_TREE_TIMING
     if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[29], gtimer());
 #endif
-    if (p.work) add_work(p.work + 1, work);
+    if constexpr (COUNT) add_work(p.work + 1, work);
 }
 
 // ---------------------------------------------------------------------------
@@ -1878,8 +1886,9 @@ void *converge_or_null() {
     else return (void *)converge_kernel<M>;
 }
 #define DFA_DEFINE_MODE_ENTRIES(M)                                                                      \
-    template <> void *lanes_entry<M>(bool sticky) {                                                     \
-        return sticky ? (void *)lanes_kernel<M, true> : (void *)lanes_kernel<M, false>;                 \
+    template <> void *lanes_entry<M>(bool sticky, bool count) {                                         \
+        return count ? (sticky ? (void *)lanes_kernel<M, true, true> : (void *)lanes_kernel<M, false, true>) \
+                     : (sticky ? (void *)lanes_kernel<M, true, false> : (void *)lanes_kernel<M, false, false>); \
     }                                                                                                   \
     template <> void *ceiling_entry<M>() { return (void *)ceiling_kernel<M>; }                          \
     template <> void *converge_entry<M>() { return converge_or_null<M>(); }
@@ -1915,18 +1924,18 @@ void *ceiling_fn(int mode) {
     }
 }
 
-void *lanes_fn(const DevTables &T) {
+void *lanes_fn(const DevTables &T, bool count = false) {
     const bool st = T.has_sticky != 0;
     switch (T.mode) {
-    case kIdentU8: return lanes_entry<kIdentU8>(st);
-    case kRepU8x8: return lanes_entry<kRepU8x8>(st);
-    case kRepU8x4: return lanes_entry<kRepU8x4>(st);
-    case kIdentU8P: return lanes_entry<kIdentU8P>(st);
-    case kIdentU16: return lanes_entry<kIdentU16>(st);
-    case kWindowU8: return lanes_entry<kWindowU8>(st);
-    case kWindowU16: return lanes_entry<kWindowU16>(st);
-    case kPacked9: return lanes_entry<kPacked9>(st);
-    default: return lanes_entry<kGlobalU16>(st);
+    case kIdentU8: return lanes_entry<kIdentU8>(st, count);
+    case kRepU8x8: return lanes_entry<kRepU8x8>(st, count);
+    case kRepU8x4: return lanes_entry<kRepU8x4>(st, count);
+    case kIdentU8P: return lanes_entry<kIdentU8P>(st, count);
+    case kIdentU16: return lanes_entry<kIdentU16>(st, count);
+    case kWindowU8: return lanes_entry<kWindowU8>(st, count);
+    case kWindowU16: return lanes_entry<kWindowU16>(st, count);
+    case kPacked9: return lanes_entry<kPacked9>(st, count);
+    default: return lanes_entry<kGlobalU16>(st, count);
     }
 }
 // The converge kernel steps all lanes of one sub-chunk on the same byte (a
@@ -2004,9 +2013,9 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     // both lanes kernel variants: DFA_OPT_STICKY_PARKING switches between them
     DevTables T2 = T;
-    for (uint32_t st = 0; st < 2; st++) {
-        T2.has_sticky = st;
-        cudaError_t e = cudaFuncSetAttribute(lanes_fn(T2), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    for (uint32_t v = 0; v < 4; v++) {
+        T2.has_sticky = v & 1;
+        cudaError_t e = cudaFuncSetAttribute(lanes_fn(T2, v >= 2), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
         if (e != cudaSuccess) return e;
     }
     cudaError_t e;
@@ -2054,7 +2063,7 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
                     (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap,
                     (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status, (void *)&cap};
-    return cudaLaunchKernel(lanes_fn(T), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
+    return cudaLaunchKernel(lanes_fn(T, p.work != nullptr), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
 }
 
 const void *tree_fn() { return (const void *)tree_kernel; }

@@ -164,11 +164,11 @@ int probe_dynamic_smem_base(uint32_t *dev_scratch);
 
 // Match kernels of one table layout (MODE = TableMode), one translation unit
 // each (kernels_m<MODE>.cu); nullptr where a layout has no such kernel.
-template <int MODE> void *lanes_entry(bool sticky);
+template <int MODE> void *lanes_entry(bool sticky, bool count);
 template <int MODE> void *ceiling_entry();
 template <int MODE> void *converge_entry();
 #define DFA_DECLARE_MODE_ENTRIES(M)                  \
-    template <> void *lanes_entry<M>(bool sticky);   \
+    template <> void *lanes_entry<M>(bool sticky, bool count); \
     template <> void *ceiling_entry<M>();            \
     template <> void *converge_entry<M>();
 DFA_DECLARE_MODE_ENTRIES(1) DFA_DECLARE_MODE_ENTRIES(2) DFA_DECLARE_MODE_ENTRIES(3)

@@ -48,6 +48,13 @@ def main():
             if k in d:
                 v = d[k]
                 print(f"- {name.split(' (')[0]}: {v} {u.get(k, '')}")
+        stalls = sorted(((float(v), k) for k, v in d.items()
+                         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
+                         and v.replace(".", "", 1).isdigit()), reverse=True)
+        if stalls:
+            print("- stalls per issue: " + ", ".join(
+                f"{k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]} {v:.2f}"
+                for v, k in stalls[:6] if v >= 0.05))
         sw = d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
         sl = d.get("sass__inst_executed_shared_loads")
         try:

@@ -76,7 +76,7 @@ def protein(seed: int = 0) -> Workload:
 
 def worst(seed: int = 0) -> Workload:
     aut = automata.random_structured(512, 256, 240, 128, seed)
-    return Workload("worst", aut, 256, 10 * GiB, 1 * MiB, 16384,
+    return Workload("worst", aut, 256, 10 * GiB, 1 * MiB, 4096,
                     lambda n, out=None, sg=0: inputs.uniform_bytes(n, seed + 1000 * sg, out))
 
 
