@@ -75,6 +75,8 @@ struct dfa_handle {
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
     DevBuf cta_start, leaf_rows2, leaf_dom2;
     int warp_compose = 1;
+    int fused_tail = 1;           // DFA_OPT_FUSED_TAIL
+    DevBuf part_rows, part_doms, chunk_cnt;
     std::vector<uint64_t> plan_key;
     // CUDA graph of a repeated dfa_chunk_maps call
     int use_graphs = 1;
@@ -505,21 +507,73 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         surv_pos = h->surv_pos.as<uint64_t>();
     }
     const bool grouped = sp.g_log != kNoWarpGroup;
-    if (grouped) {
+    const int threads = sp.threads;
+    const int occ = std::max(1, lanes_occupancy(T, threads));
+    const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
+    // fused composition tail (one sub-chunk per thread, so CTAs hold contiguous leaves):
+    // the lanes kernel composes its own leaves, no leaf_fold / compose8 launches
+    const bool fused = grouped && h->fused_tail && !o.indep && NS <= grid * (uint64_t)threads && P <= (1u << 20) &&
+                       (threads >> sp.g_log) <= 1024;
+    Fuse fz{};
+    if (fused) {
+        fz.on = 1;
+        fz.rows = (o.user_maps || o.user_row0 || o.chunk0_end) ? 1u : 0u;
+        fz.L0 = m0 >> sp.g_log;
+        fz.L = P > 1 ? (m >> sp.g_log) : 1;
+        fz.P = P;
+        CK(h->lvlA.ensure((uint64_t)P * T.rs * 2));
+        CK(h->domA.ensure((uint64_t)P * 2));
+        CK(h->part_rows.ensure(((uint64_t)P + grid) * 16));
+        CK(h->part_doms.ensure(((uint64_t)P + grid) * 2));
+        if (h->chunk_cnt.cap < (uint64_t)P * 4) {
+            CK(h->chunk_cnt.ensure((uint64_t)P * 4));
+            CK(cudaMemsetAsync(h->chunk_cnt.p, 0, h->chunk_cnt.cap, s));  // then reset by the last arrivers
+        }
+        CK(h->fold_rows.ensure(grid * 16 + 256));
+        CK(h->fold_doms.ensure(grid * 2 + 256));
+        if (!h->ticket.p) {
+            CK(h->ticket.ensure(256));
+            CK(cudaMemsetAsync(h->ticket.p, 0, 256, s));
+        }
+        fz.rep_rows = h->lvlA.as<uint16_t>();
+        fz.rep_doms = h->domA.as<uint16_t>();
+        fz.user_rows = o.user_maps;
+        fz.user_row0 = o.user_row0;
+        fz.e0 = o.chunk0_end;
+        fz.part_rows = h->part_rows.as<uint16_t>();
+        fz.part_doms = h->part_doms.as<uint16_t>();
+        fz.chunk_cnt = h->chunk_cnt.as<uint32_t>();
+        fz.cta_rows = h->fold_rows.as<uint16_t>();
+        fz.cta_doms = h->fold_doms.as<uint16_t>();
+        fz.ticket = h->ticket.as<uint32_t>();
+        fz.final2 = o.final2;
+        if (o.starts) {
+            CK(h->cta_start.ensure(grid * 2 + 256));
+            fz.starts = o.starts;
+            fz.cta_code = h->cta_start.as<uint16_t>();
+        }
+    } else if (grouped) {
         CK(h->leaf_rows.ensure(((NS >> sp.g_log) + 1) * T.rs * 2));
         CK(h->leaf_dom.ensure(((NS >> sp.g_log) + 1) * 2));
     }
     {
-        const int threads = sp.threads;
-        const int occ = std::max(1, lanes_occupancy(T, threads));
-        const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
         prof_begin(h, s, 1);
         CK(launch_lanes(T, plan, in, surv, surv_n, surv_pos, h->sfin.as<uint16_t>(), sk, h->dom_of.as<uint16_t>(),
                         h->convergence, const_cast<uint16_t *>(amap), sp.g_log, h->leaf_rows.as<uint16_t>(),
                         h->leaf_dom.as<uint16_t>(), h->status.as<DevStatus>(), (uint32_t)h->max_lanes, threads,
-                        (int)grid, s));
+                        (int)grid, s, fz));
         prof_end(h, s);
         kernels++;
+    }
+    if (fused) {
+        if (o.starts) {
+            CK(launch_fused_starts(T, plan, fz, in, (uint32_t)(threads >> sp.g_log), sp.g_log, (int)grid, s));
+            kernels++;
+        }
+        h->rep_rows = h->lvlA.as<uint16_t>();
+        h->rep_rs = 8;
+        h->stats.num_kernels = kernels;
+        return DFA_OK;
     }
     // composition: sub-chunk maps -> reporting maps -> final state
     if (grouped) {
@@ -822,7 +876,8 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->last_stream) cudaStreamSynchronize(h->last_stream);
         for (DevBuf *b : {&h->tables, &h->status, &h->sfin, &h->dom_of, &h->surv, &h->surv_n, &h->surv_pos,
                           &h->amap, &h->lvlA, &h->domA, &h->counters, &h->bounds, &h->input, &h->fold_rows,
-                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds, &h->cta_start, &h->leaf_rows2, &h->leaf_dom2})
+                          &h->fold_doms, &h->ticket, &h->leaf_rows, &h->leaf_dom, &h->plan_bounds, &h->cta_start, &h->leaf_rows2, &h->leaf_dom2,
+                          &h->part_rows, &h->part_doms, &h->chunk_cnt})
             b->release();
         h->h_status.release();
         h->h_bounds.release();
@@ -1082,7 +1137,7 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
                        (uint64_t)(uintptr_t)dev_chunk_start, (uint64_t)(uintptr_t)dev_final, (uint64_t)h->profile,
                        (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
                        (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
-                       (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work,
+                       (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work, (uint64_t)h->fused_tail,
                        (uint64_t)g_scratch_gen.load()})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
@@ -1295,6 +1350,9 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
         return DFA_OK;
     case DFA_OPT_COUNT_WORK:
         h->count_work = value ? 1 : 0;
+        return DFA_OK;
+    case DFA_OPT_FUSED_TAIL:
+        h->fused_tail = value ? 1 : 0;
         return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         h->threads_auto = value == 0;

@@ -641,6 +641,209 @@ __device__ __forceinline__ void warp_compose(uint32_t mask, uint32_t g_log, uint
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused composition tail (struct Fuse in kernels.cuh).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void unpack8(uint4 v, uint32_t (&f)[kLanes]) {
+    f[0] = v.x & 0xFFFFu; f[1] = v.x >> 16; f[2] = v.y & 0xFFFFu; f[3] = v.y >> 16;
+    f[4] = v.z & 0xFFFFu; f[5] = v.z >> 16; f[6] = v.w & 0xFFFFu; f[7] = v.w >> 16;
+}
+__device__ __forceinline__ uint4 pack8(const uint32_t (&f)[kLanes]) {
+    return make_uint4((f[0] & 0xFFFFu) | (f[1] << 16), (f[2] & 0xFFFFu) | (f[3] << 16),
+                      (f[4] & 0xFFFFu) | (f[5] << 16), (f[6] & 0xFFFFu) | (f[7] << 16));
+}
+// acc <- next o acc (Eq.MapReduction on rank-space maps: a rank code of acc indexes next)
+__device__ __forceinline__ void compose_into(uint32_t (&acc)[kLanes], const uint32_t (&nx)[kLanes]) {
+#pragma unroll
+    for (int q = 0; q < kLanes; q++) {
+        const uint32_t rr = acc[q] - kRank;
+        if (rr >= (uint32_t)kLanes) continue;
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < kLanes; t++) v |= nx[t] & (0u - (uint32_t)(rr == (uint32_t)t));
+        acc[q] = v;
+    }
+}
+// One warp folds the n >= 1 maps rows[0..n) in order; lane 0 returns the composition.
+// Lane = map, butterfly over 32 maps (L_t <- L_{t+step} o L_t), batches of 32 chained.
+__device__ __forceinline__ void warp_fold(const uint4 *rows, uint32_t n, uint32_t (&acc)[kLanes], bool cg) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+        uint32_t f[kLanes];
+        const bool valid = b0 + lane < n;
+        if (valid) unpack8(cg ? __ldcg(rows + b0 + lane) : rows[b0 + lane], f);
+        else {
+#pragma unroll
+            for (int q = 0; q < kLanes; q++) f[q] = kNone;
+        }
+#pragma unroll
+        for (uint32_t step = 1; step < 32; step *= 2) {
+            uint32_t pm[kLanes];
+#pragma unroll
+            for (int q = 0; q < kLanes; q++) pm[q] = __shfl_down_sync(0xffffffffu, f[q], step);
+            const bool pv = __shfl_down_sync(0xffffffffu, valid, step);
+            if ((lane & (2 * step - 1)) == 0 && pv && lane + step < 32) compose_into(f, pm);
+        }
+        if (b0 == 0) {
+#pragma unroll
+            for (int q = 0; q < kLanes; q++) acc[q] = f[q];
+        } else {
+            compose_into(acc, f);
+        }
+    }
+}
+// Reporting chunk k's map (lane 0's acc, domain d0): rank-space row, domain, and the API
+// outputs -- the user-order row with states (rank codes decoded through the next chunk's
+// I_sigma, sigma = the byte before b_{k+1}), chunk 0's e0 / user row.  One warp.
+__device__ __forceinline__ void emit_chunk(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
+                                           uint32_t k, uint32_t d0, const uint32_t (&acc)[kLanes]) {
+    const uint32_t lane = threadIdx.x & 31, j = lane & 7;
+    uint32_t av = 0;
+#pragma unroll
+    for (int e = 0; e < kLanes; e++) {
+        const uint32_t v = __shfl_sync(0xffffffffu, acc[e], 0);
+        if (j == (uint32_t)e) av = v;
+    }
+    if (lane < 8) fz.rep_rows[(uint64_t)k * 8 + j] = (uint16_t)av;
+    if (lane == 0) fz.rep_doms[k] = (uint16_t)d0;
+    uint32_t dl = kNone;
+    if (k + 1 < fz.P && lane < 8) {
+        const uint32_t nd = T.byte_class[__ldg(in + p.bounds[k + 1] - 1)];
+        dl = __ldg(T.dom_list + (uint64_t)nd * T.rs + j);
+    }
+    const uint32_t rr = av - kRank;
+    const uint32_t dv = __shfl_sync(0xffffffffu, dl, rr & 7u);
+    const uint32_t sv = rr < (uint32_t)kLanes ? dv : av;
+    if (fz.e0 && k == 0 && lane == 0) fz.e0[0] = (uint16_t)sv;
+    uint16_t *urow = nullptr;
+    if (fz.user_rows && k > 0) urow = fz.user_rows + (uint64_t)(k - 1) * T.imax_user;
+    else if (fz.user_row0 && k == 0) urow = fz.user_row0;
+    uint32_t du, xl;
+    if (d0 < T.nclass) {
+        du = T.dom_user_size[d0];
+        xl = j < T.imax_user ? T.xlat[(uint64_t)d0 * T.imax_user + j] : 0u;
+    } else {
+        du = d0 == T.start_dom ? 1u : 0u;
+        xl = j;
+    }
+    const uint32_t v = __shfl_sync(0xffffffffu, sv, xl & 7u);
+    if (urow && lane < 8 && j < T.imax_user) urow[j] = (uint16_t)(j < du ? v : kNone);
+}
+
+// The tail proper (every thread of the CTA; the CTA's matching is done).  Shared
+// memory (the table's, no longer read): leaves [LPC] uint4, their domains, the
+// per-chunk segment maps.
+__device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
+                                        uint4 *smem, uint32_t g_log, uint4 my_leaf, uint32_t my_leaf_dom,
+                                        DevStatus *status) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t LPC = blockDim.x >> g_log;
+    const uint64_t NL = p.NS >> g_log;
+    const uint64_t l0 = (uint64_t)blockIdx.x * LPC;
+    const uint32_t nl = (uint32_t)min((uint64_t)LPC, NL > l0 ? NL - l0 : (uint64_t)0);
+    uint4 *leaves = smem;                                                  // [LPC]
+    uint4 *segs = smem + LPC;                                              // [LPC]
+    uint16_t *ldom = reinterpret_cast<uint16_t *>(smem + 2 * LPC);         // [LPC]
+    uint16_t *sdom = ldom + LPC;                                           // [LPC]
+    // (no static __shared__ in the lanes kernel: it would move the table's shared address,
+    // which the IdentU8 state bias is derived from)
+    uint32_t &s_last = *reinterpret_cast<uint32_t *>(sdom + LPC + (LPC & 1));
+    __syncthreads();  // every warp is past its match loop: the table's space is free
+    if ((threadIdx.x & ((1u << g_log) - 1)) == 0 && (threadIdx.x >> g_log) < nl) {
+        leaves[threadIdx.x >> g_log] = my_leaf;
+        ldom[threadIdx.x >> g_log] = (uint16_t)my_leaf_dom;
+    }
+    __syncthreads();
+    // chunk of leaf l; first leaf of chunk k
+    auto chunk_of = [&](uint64_t l) -> uint32_t {
+        return l < fz.L0 ? 0u : (uint32_t)(1 + (l - fz.L0) / fz.L);
+    };
+    auto first_leaf = [&](uint32_t k) -> uint64_t { return k == 0 ? 0 : (uint64_t)fz.L0 + (uint64_t)(k - 1) * fz.L; };
+    const uint32_t ka = nl ? chunk_of(l0) : 0, kb = nl ? chunk_of(l0 + nl - 1) : 0;
+    const uint32_t nseg = nl ? kb - ka + 1 : 0;
+    for (uint32_t sgi = warp; sgi < nseg; sgi += nw) {
+        const uint32_t k = ka + sgi;
+        const uint64_t f = first_leaf(k), e = first_leaf(k + 1);
+        const uint64_t a = max(f, l0), b = min(e, l0 + nl);
+        uint32_t acc[kLanes];
+        warp_fold(leaves + (a - l0), (uint32_t)(b - a), acc, false);
+        const uint32_t d = ldom[a - l0];
+        if (lane == 0) {
+            segs[sgi] = pack8(acc);
+            sdom[sgi] = (uint16_t)d;
+            if (fz.starts) reinterpret_cast<uint4 *>(fz.part_rows)[k + blockIdx.x] = pack8(acc);  // starts walk
+        }
+        if (!fz.rows) continue;
+        if (a == f && b == e) {
+            emit_chunk(T, p, fz, in, k, d, acc);  // the whole chunk is in this CTA
+            continue;
+        }
+        // a straddling chunk: publish this CTA's part (slot k + b), the last CTA to arrive
+        // folds the parts in order
+        const uint32_t slot = k + blockIdx.x;
+        if (lane == 0) {
+            reinterpret_cast<uint4 *>(fz.part_rows)[slot] = pack8(acc);
+            fz.part_doms[slot] = (uint16_t)d;
+        }
+        __syncwarp();
+        const uint32_t b_lo = (uint32_t)(f / LPC), b_hi = (uint32_t)((e - 1) / LPC);
+        uint32_t prev = 0;
+        if (lane == 0)
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.chunk_cnt + k) : "memory");
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev + 1 != b_hi - b_lo + 1) continue;
+        if (lane == 0) fz.chunk_cnt[k] = 0;  // every part has arrived: reset for the next launch
+        warp_fold(reinterpret_cast<const uint4 *>(fz.part_rows) + k + b_lo, b_hi - b_lo + 1, acc, true);
+        emit_chunk(T, p, fz, in, k, __ldcg(fz.part_doms + k + b_lo), acc);
+    }
+    __syncthreads();
+    // the CTA map: its segment maps in order
+    if (warp == 0 && nseg) {
+        uint32_t acc[kLanes];
+        warp_fold(segs, nseg, acc, false);
+        if (lane == 0) {
+            reinterpret_cast<uint4 *>(fz.cta_rows)[blockIdx.x] = pack8(acc);
+            fz.cta_doms[blockIdx.x] = sdom[0];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.ticket) : "memory");
+        s_last = prev + 1 == gridDim.x;
+        if (s_last) atomicExch(fz.ticket, 0u);  // every CTA has its ticket: reset for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (fz.starts) {
+        // rank code of the state at every CTA's first leaf: the prefix of Eq.SeqReduction
+        // over the CTA maps, staged in shared memory (the input's first state is rank 0 of {q0})
+        for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) leaves[b] = __ldcg(reinterpret_cast<const uint4 *>(fz.cta_rows) + b);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t code = kRank;
+            for (uint32_t b = 0; b < gridDim.x; b++) {
+                fz.cta_code[b] = (uint16_t)code;
+                if (is_rank(code)) code = reinterpret_cast<const uint16_t *>(leaves + b)[code - kRank];
+            }
+        }
+    }
+    if (warp != 0) return;
+    uint32_t acc[kLanes];
+    warp_fold(reinterpret_cast<const uint4 *>(fz.cta_rows), gridDim.x, acc, true);
+    if (lane == 0) {
+        const uint32_t fs = acc[0];  // absolute: the input's last sub-chunk ends in states
+        if (fs == T.poison) atomicMax(&status->err, 5u);
+        if (is_rank(fs)) atomicMax(&status->err, 8u);
+        status->final_state = fs;
+        status->accept = fs < T.nq ? (uint32_t)test_bit(T.accept_bits, fs) : 0u;
+        if (fz.final2) {
+            fz.final2[0] = (uint16_t)fs;
+            fz.final2[1] = (uint16_t)status->accept;
+        }
+    }
+}
+
 // COUNT: the DFA_OPT_COUNT_WORK instantiation (a live counter register would make the
 // timed kernel spill, so counting is a separate instantiation)
 template <int MODE, bool STICKY, bool COUNT>
@@ -652,7 +855,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
                                                     uint16_t *__restrict__ dom_of, int convergence,
                                                     uint16_t *__restrict__ amap, uint32_t g_log,
                                                     uint16_t *__restrict__ leaf_rows, uint16_t *__restrict__ leaf_dom,
-                                                    DevStatus *status, uint32_t cap) {
+                                                    DevStatus *status, uint32_t cap, Fuse fz) {
     pdl_trigger();  // one wave: the composition kernels may take SMs as CTAs retire
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMin(&g_tree_t[25], gtimer());
@@ -677,6 +880,8 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     tab.init(T, tsm);
     const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
     uint64_t work = 0;  // executed lane-steps of this thread (DFA_OPT_COUNT_WORK)
+    uint4 my_leaf = make_uint4(0, 0, 0, 0);  // fused tail: this thread's leaf (group leaders)
+    uint32_t my_leaf_dom = 0;
 
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -726,8 +931,13 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
                 v.y = (fin[2] & 0xFFFFu) | (fin[3] << 16);
                 v.z = (fin[4] & 0xFFFFu) | (fin[5] << 16);
                 v.w = (fin[6] & 0xFFFFu) | (fin[7] << 16);
-                reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
-                leaf_dom[leaf] = (uint16_t)dom;
+                if (fz.on) {  // kept for the CTA's composition tail
+                    my_leaf = v;
+                    my_leaf_dom = dom;
+                } else {
+                    reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
+                    leaf_dom[leaf] = (uint16_t)dom;
+                }
             }
         };
         // grouped with cap = 8 (u <= 8): one pass, the map stays in registers and every
@@ -808,6 +1018,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[29], gtimer());
 #endif
     if constexpr (COUNT) add_work(p.work + 1, work);
+    if (fz.on) fused_tail(T, p, fz, in, smem4, g_log, my_leaf, my_leaf_dom, status);
 }
 
 // ---------------------------------------------------------------------------
@@ -2055,15 +2266,52 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
                             converge_smem_bytes(T, warps_per_cta), s);
 }
 
+int fused_tail_smem_bytes(int threads, uint32_t g_log, int grid) {
+    const int lpc = threads >> g_log;
+    return std::max(lpc * 16 * 2 + lpc * 2 * 2 + 16, grid * 16 + 16);
+}
+
+// fused_starts_kernel: true start of every reporting chunk for the fused tail.  CTA b
+// stages the segment maps of lanes-CTA b (slots k + b, k = its chunks) and walks them
+// from its start code (rank codes decode through I_sigma of the byte before b_k).
+__global__ void __launch_bounds__(128) fused_starts_kernel(DevTables T, Plan p, Fuse fz, const uint8_t *in,
+                                                           uint32_t lpc, uint32_t g_log) {
+    __shared__ uint4 seg[1024];
+    pdl_wait();
+    const uint64_t NL = p.NS >> g_log, l0 = (uint64_t)blockIdx.x * lpc;
+    if (l0 >= NL) return;
+    const uint64_t l1 = min(NL, l0 + lpc);
+    auto chunk_of = [&](uint64_t l) -> uint32_t {
+        return l < fz.L0 ? 0u : (uint32_t)(1 + (l - fz.L0) / fz.L);
+    };
+    const uint32_t ka = chunk_of(l0), kb = chunk_of(l1 - 1);
+    for (uint32_t t = threadIdx.x; t <= kb - ka; t += blockDim.x)
+        seg[t] = __ldcg(reinterpret_cast<const uint4 *>(fz.part_rows) + ka + t + blockIdx.x);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    uint32_t code = __ldcg(fz.cta_code + blockIdx.x);
+    for (uint32_t k = ka; k <= kb; k++) {
+        const uint64_t f = k == 0 ? 0 : (uint64_t)fz.L0 + (uint64_t)(k - 1) * fz.L;
+        if (f >= l0) {
+            const uint32_t d = k == 0 ? p.first_dom : (uint32_t)T.byte_class[__ldg(in + p.bounds[k] - 1)];
+            fz.starts[k] = (uint16_t)(is_rank(code) ? __ldg(T.dom_list + (uint64_t)d * T.rs + (code - kRank)) : code);
+        }
+        if (is_rank(code)) code = reinterpret_cast<const uint16_t *>(seg + (k - ka))[code - kRank];
+    }
+}
+
 cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, const uint16_t *surv,
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
                          uint16_t *dom_of, int convergence, uint16_t *amap, uint32_t g_log,
                          uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, uint32_t cap, int threads,
-                         int grid, cudaStream_t s) {
+                         int grid, cudaStream_t s, const Fuse &fz) {
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
                     (void *)&sfin, (void *)&sk, (void *)&dom_of, (void *)&convergence, (void *)&amap,
-                    (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status, (void *)&cap};
-    return cudaLaunchKernel(lanes_fn(T, p.work != nullptr), dim3(grid), dim3(threads), args, lanes_smem_bytes(T), s);
+                    (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status, (void *)&cap,
+                    (void *)&fz};
+    int smem = lanes_smem_bytes(T);
+    if (fz.on) smem = std::max(smem, fused_tail_smem_bytes(threads, g_log, grid));
+    return cudaLaunchKernel(lanes_fn(T, p.work != nullptr), dim3(grid), dim3(threads), args, smem, s);
 }
 
 const void *tree_fn() { return (const void *)tree_kernel; }
@@ -2130,6 +2378,11 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+cudaError_t launch_fused_starts(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in, uint32_t lpc,
+                                uint32_t g_log, int grid, cudaStream_t s) {
+    return launch_pdl(fused_starts_kernel, dim3(grid), dim3(128), 0, s, T, p, fz, in, lpc, g_log);
 }
 
 cudaError_t launch_batch_out(const DevTables &T, const uint16_t *rep_rows, uint32_t rs, const int32_t *kidx,

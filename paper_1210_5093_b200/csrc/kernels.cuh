@@ -64,6 +64,28 @@ struct Plan {
     unsigned long long *work; // DFA_OPT_COUNT_WORK: [0] converge, [1] lanes lane-steps; else null
 };
 
+// Fused composition tail of lanes_kernel (grouped path, one execution sub-chunk
+// per thread, so CTA b holds the contiguous leaves [b LPC, (b+1) LPC)): each CTA
+// composes its own leaves per reporting chunk (Eq.MapReduction), chunks that
+// straddle CTAs are finished by the last CTA to arrive (acq_rel counters), and
+// the last CTA overall folds the CTA maps into the final state (Eq.SeqReduction,
+// Alg.seqmatch l.4-6).  Replaces leaf_fold_kernel + compose8_kernel.
+struct Fuse {
+    uint32_t on;             // 1: the tail runs (then leaf_rows/leaf_dom are not written)
+    uint32_t rows;           // 1: reporting rows are wanted (rep_rows and the API outputs)
+    uint32_t L0, L;          // leaves of chunk 0 / of every chunk k >= 1
+    uint32_t P;
+    uint16_t *rep_rows, *rep_doms;     // [P][8] rank-space reporting maps, their domains
+    uint16_t *user_rows, *user_row0, *e0;
+    uint16_t *part_rows, *part_doms;   // [P + grid] partial maps of straddling chunks, slot k + b
+    uint32_t *chunk_cnt;               // [P] arrival counters, reset by the last arriver
+    uint16_t *cta_rows, *cta_doms;     // [grid] CTA maps
+    uint32_t *ticket;
+    uint16_t *final2;
+    uint16_t *starts;        // [P] true chunk starts (optional; then every segment map is
+    uint16_t *cta_code;      //  published and the last CTA writes each CTA's start code)
+};
+
 struct DevStatus {
     uint32_t err;            // 0 ok, 5 bad symbol, 8 internal
     uint32_t final_state;
@@ -128,7 +150,10 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
                          const uint8_t *surv_n, const uint64_t *surv_pos, uint16_t *sfin, uint32_t sk,
                          uint16_t *dom_of, int convergence, uint16_t *amap, uint32_t g_log,
                          uint16_t *leaf_rows, uint16_t *leaf_dom, DevStatus *status, uint32_t cap, int threads,
-                         int grid, cudaStream_t s);
+                         int grid, cudaStream_t s, const Fuse &fz);
+int fused_tail_smem_bytes(int threads, uint32_t g_log, int grid);
+cudaError_t launch_fused_starts(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in, uint32_t lpc,
+                                uint32_t g_log, int grid, cudaStream_t s);
 int lanes_smem_bytes(const DevTables &T);
 int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);

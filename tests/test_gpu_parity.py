@@ -884,3 +884,18 @@ def test_work_counter_is_L_alg(name):
         assert x.size <= st["work"]["lanes"] <= L
     finally:
         d.close()
+
+
+@pytest.mark.parametrize("fused", [0, 1])
+@pytest.mark.parametrize("name", ["tiny", "random", "keyword"])
+def test_fused_tail_and_compose8(name, fused):
+    """Maps of <= 8 entries: the match kernel's fused composition tail (default) and the
+    separate leaf_fold + compose8 launches (DFA_OPT_FUSED_TAIL = 0) give the oracle's
+    bounds, e0, every map entry, every chunk start and the final state -- one chunk
+    spanning every CTA (P = 1, 2), chunks straddling CTA boundaries, many chunks per CTA."""
+    w = W.get(name)
+    x = w.input(min(w.small_n, 1 << 21) + 4321)
+    c = Case(w.automaton, x, name)
+    for P in (1, 2, 3, 64, 777, 4096):
+        check_chunk_maps(c, P, opts={D.DFA_OPT_FUSED_TAIL: fused})
+    check_match(c, opts={D.DFA_OPT_FUSED_TAIL: fused})
