@@ -797,6 +797,9 @@ __device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const
         emit_chunk(T, p, fz, in, k, __ldcg(fz.part_doms + k + b_lo), acc);
     }
     __syncthreads();
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[12], gtimer());
+#endif
     // the CTA map: its segment maps in order
     if (warp == 0 && nseg) {
         uint32_t acc[kLanes];
@@ -814,6 +817,9 @@ __device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const
         if (s_last) atomicExch(fz.ticket, 0u);  // every CTA has its ticket: reset for the next launch
     }
     __syncthreads();
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[16], gtimer());
+#endif
     if (!s_last) return;
     if (fz.starts) {
         // rank code of the state at every CTA's first leaf: the prefix of Eq.SeqReduction
@@ -841,6 +847,9 @@ __device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const
             fz.final2[0] = (uint16_t)fs;
             fz.final2[1] = (uint16_t)status->accept;
         }
+#ifdef DFA_TREE_TIMING
+        atomicMax(&g_tree_t[19], gtimer());
+#endif
     }
 }
 

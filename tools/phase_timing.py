@@ -6,7 +6,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 lib = "/tmp/libdfa_timing.so"
 src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1210_5093_b200", "csrc")
 if not os.path.exists(lib):
+    # one translation unit (DFA_TU_MODE=0: every layout's match kernels beside the composition
+    # kernels) so that all kernels write the same g_tree_t
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-DDFA_TREE_TIMING",
+                           "-DDFA_TU_MODE=0", "-DDFA_TU_MAIN=1", "-diag-suppress", "177",
                            "-Xcompiler", "-fPIC", "-shared", "-o", lib] +
                           [os.path.join(src, f) for f in ("api.cpp", "prep.cpp", "kernels.cu")])
 os.environ["DFA_LIB"] = lib
@@ -20,6 +23,7 @@ for name in sys.argv[1:]:
     x = w.input()
     dx = torch.from_numpy(x).cuda()
     d = D.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accept_bitmap)
+    D.dfa_set_option(d.h, D.DFA_OPT_FUSED_TAIL, int(os.environ.get("FUSED", "1")))
     for rep in range(6):
         L.dfa_debug_tree_timing(buf, 1)
         d.chunk_maps(dx, w.chunks)
