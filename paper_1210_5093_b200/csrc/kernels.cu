@@ -695,8 +695,8 @@ __device__ __forceinline__ void warp_fold(const uint4 *rows, uint32_t n, uint32_
 // Reporting chunk k's map (lane 0's acc, domain d0): rank-space row, domain, and the API
 // outputs -- the user-order row with states (rank codes decoded through the next chunk's
 // I_sigma, sigma = the byte before b_{k+1}), chunk 0's e0 / user row.  One warp.
-__device__ __forceinline__ void emit_chunk(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
-                                           uint32_t k, uint32_t d0, const uint32_t (&acc)[kLanes]) {
+__device__ __forceinline__ void emit_chunk(const DevTables &T, const Fuse &fz, uint32_t k, uint32_t d0, uint32_t nd,
+                                           const uint32_t (&acc)[kLanes]) {
     const uint32_t lane = threadIdx.x & 31, j = lane & 7;
     uint32_t av = 0;
 #pragma unroll
@@ -704,20 +704,8 @@ __device__ __forceinline__ void emit_chunk(const DevTables &T, const Plan &p, co
         const uint32_t v = __shfl_sync(0xffffffffu, acc[e], 0);
         if (j == (uint32_t)e) av = v;
     }
-    if (lane < 8) fz.rep_rows[(uint64_t)k * 8 + j] = (uint16_t)av;
-    if (lane == 0) fz.rep_doms[k] = (uint16_t)d0;
-    uint32_t dl = kNone;
-    if (k + 1 < fz.P && lane < 8) {
-        const uint32_t nd = T.byte_class[__ldg(in + p.bounds[k + 1] - 1)];
-        dl = __ldg(T.dom_list + (uint64_t)nd * T.rs + j);
-    }
-    const uint32_t rr = av - kRank;
-    const uint32_t dv = __shfl_sync(0xffffffffu, dl, rr & 7u);
-    const uint32_t sv = rr < (uint32_t)kLanes ? dv : av;
-    if (fz.e0 && k == 0 && lane == 0) fz.e0[0] = (uint16_t)sv;
-    uint16_t *urow = nullptr;
-    if (fz.user_rows && k > 0) urow = fz.user_rows + (uint64_t)(k - 1) * T.imax_user;
-    else if (fz.user_row0 && k == 0) urow = fz.user_row0;
+    // independent loads first: the decode row, the user-order translation
+    const uint32_t dl = k + 1 < fz.P && lane < 8 ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.rs + j) : kNone;
     uint32_t du, xl;
     if (d0 < T.nclass) {
         du = T.dom_user_size[d0];
@@ -726,44 +714,83 @@ __device__ __forceinline__ void emit_chunk(const DevTables &T, const Plan &p, co
         du = d0 == T.start_dom ? 1u : 0u;
         xl = j;
     }
+    if (lane < 8) fz.rep_rows[(uint64_t)k * 8 + j] = (uint16_t)av;
+    if (lane == 0) fz.rep_doms[k] = (uint16_t)d0;
+    const uint32_t rr = av - kRank;
+    const uint32_t dv = __shfl_sync(0xffffffffu, dl, rr & 7u);
+    const uint32_t sv = rr < (uint32_t)kLanes ? dv : av;
+    if (fz.e0 && k == 0 && lane == 0) fz.e0[0] = (uint16_t)sv;
+    uint16_t *urow = nullptr;
+    if (fz.user_rows && k > 0) urow = fz.user_rows + (uint64_t)(k - 1) * T.imax_user;
+    else if (fz.user_row0 && k == 0) urow = fz.user_row0;
     const uint32_t v = __shfl_sync(0xffffffffu, sv, xl & 7u);
     if (urow && lane < 8 && j < T.imax_user) urow[j] = (uint16_t)(j < du ? v : kNone);
 }
 
+// Segment geometry of the fused tail: CTA b holds leaves [l0, l0 + nl), which lie in
+// reporting chunks ka..ka+nseg-1 (a "segment" = one chunk's leaves inside this CTA).
+struct TailGeom {
+    uint32_t LPC, nl, ka, nseg;
+    uint64_t l0;
+};
+__device__ __forceinline__ uint32_t fuse_chunk_of(const Fuse &fz, uint64_t l) {
+    return l < fz.L0 ? 0u : (uint32_t)(1 + (l - fz.L0) / fz.L);
+}
+__device__ __forceinline__ uint64_t fuse_first_leaf(const Fuse &fz, uint32_t k) {
+    return k == 0 ? 0 : (uint64_t)fz.L0 + (uint64_t)(k - 1) * fz.L;
+}
+__device__ __forceinline__ TailGeom tail_geom(const Plan &p, const Fuse &fz, uint32_t g_log) {
+    TailGeom g;
+    g.LPC = blockDim.x >> g_log;
+    const uint64_t NL = p.NS >> g_log;
+    g.l0 = (uint64_t)blockIdx.x * g.LPC;
+    g.nl = (uint32_t)min((uint64_t)g.LPC, NL > g.l0 ? NL - g.l0 : (uint64_t)0);
+    g.ka = g.nl ? fuse_chunk_of(fz, g.l0) : 0;
+    g.nseg = g.nl ? fuse_chunk_of(fz, g.l0 + g.nl - 1) - g.ka + 1 : 0;
+    return g;
+}
+// At kernel start (latency hidden by the match loop): the decode domain of each segment's
+// chunk -- I_sigma of the byte before b_{k+1} -- into the tail's info area.
+__device__ __forceinline__ void tail_prefetch(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
+                                              uint4 *smem, uint32_t g_log) {
+    const TailGeom g = tail_geom(p, fz, g_log);
+    uint16_t *info = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off);
+    for (uint32_t t = threadIdx.x; t < g.nseg; t += blockDim.x) {
+        const uint32_t k = g.ka + t;
+        info[t] = k + 1 < fz.P ? (uint16_t)T.byte_class[__ldg(in + p.bounds[k + 1] - 1)] : (uint16_t)0;
+    }
+}
+
 // The tail proper (every thread of the CTA; the CTA's matching is done).  Shared
 // memory (the table's, no longer read): leaves [LPC] uint4, their domains, the
-// per-chunk segment maps.
-__device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
-                                        uint4 *smem, uint32_t g_log, uint4 my_leaf, uint32_t my_leaf_dom,
-                                        DevStatus *status) {
+// per-chunk segment maps; the info area (after everything) holds the decode domains.
+__device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
+                                           uint4 *smem, uint32_t g_log, uint4 my_leaf, uint32_t my_leaf_dom,
+                                           DevStatus *status) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const uint32_t LPC = blockDim.x >> g_log;
-    const uint64_t NL = p.NS >> g_log;
-    const uint64_t l0 = (uint64_t)blockIdx.x * LPC;
-    const uint32_t nl = (uint32_t)min((uint64_t)LPC, NL > l0 ? NL - l0 : (uint64_t)0);
+    const TailGeom g = tail_geom(p, fz, g_log);
+    const uint32_t LPC = g.LPC, nl = g.nl, ka = g.ka, nseg = g.nseg;
+    const uint64_t l0 = g.l0;
     uint4 *leaves = smem;                                                  // [LPC]
     uint4 *segs = smem + LPC;                                              // [LPC]
     uint16_t *ldom = reinterpret_cast<uint16_t *>(smem + 2 * LPC);         // [LPC]
     uint16_t *sdom = ldom + LPC;                                           // [LPC]
+    const uint16_t *info = reinterpret_cast<const uint16_t *>(reinterpret_cast<const uint8_t *>(smem) + fz.info_off);
     // (no static __shared__ in the lanes kernel: it would move the table's shared address,
     // which the IdentU8 state bias is derived from)
-    uint32_t &s_last = *reinterpret_cast<uint32_t *>(sdom + LPC + (LPC & 1));
+    uint32_t &s_last = *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off + 2u * LPC + 4u);
     __syncthreads();  // every warp is past its match loop: the table's space is free
     if ((threadIdx.x & ((1u << g_log) - 1)) == 0 && (threadIdx.x >> g_log) < nl) {
         leaves[threadIdx.x >> g_log] = my_leaf;
         ldom[threadIdx.x >> g_log] = (uint16_t)my_leaf_dom;
     }
     __syncthreads();
-    // chunk of leaf l; first leaf of chunk k
-    auto chunk_of = [&](uint64_t l) -> uint32_t {
-        return l < fz.L0 ? 0u : (uint32_t)(1 + (l - fz.L0) / fz.L);
-    };
-    auto first_leaf = [&](uint32_t k) -> uint64_t { return k == 0 ? 0 : (uint64_t)fz.L0 + (uint64_t)(k - 1) * fz.L; };
-    const uint32_t ka = nl ? chunk_of(l0) : 0, kb = nl ? chunk_of(l0 + nl - 1) : 0;
-    const uint32_t nseg = nl ? kb - ka + 1 : 0;
+#ifdef DFA_TREE_TIMING
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[11], gtimer());
+#endif
     for (uint32_t sgi = warp; sgi < nseg; sgi += nw) {
         const uint32_t k = ka + sgi;
-        const uint64_t f = first_leaf(k), e = first_leaf(k + 1);
+        const uint64_t f = fuse_first_leaf(fz, k), e = fuse_first_leaf(fz, k + 1);
         const uint64_t a = max(f, l0), b = min(e, l0 + nl);
         uint32_t acc[kLanes];
         warp_fold(leaves + (a - l0), (uint32_t)(b - a), acc, false);
@@ -775,7 +802,7 @@ __device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const
         }
         if (!fz.rows) continue;
         if (a == f && b == e) {
-            emit_chunk(T, p, fz, in, k, d, acc);  // the whole chunk is in this CTA
+            emit_chunk(T, fz, k, d, info[sgi], acc);  // the whole chunk is in this CTA
             continue;
         }
         // a straddling chunk: publish this CTA's part (slot k + b), the last CTA to arrive
@@ -794,7 +821,7 @@ __device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const
         if (prev + 1 != b_hi - b_lo + 1) continue;
         if (lane == 0) fz.chunk_cnt[k] = 0;  // every part has arrived: reset for the next launch
         warp_fold(reinterpret_cast<const uint4 *>(fz.part_rows) + k + b_lo, b_hi - b_lo + 1, acc, true);
-        emit_chunk(T, p, fz, in, k, __ldcg(fz.part_doms + k + b_lo), acc);
+        emit_chunk(T, fz, k, __ldcg(fz.part_doms + k + b_lo), info[sgi], acc);
     }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
@@ -807,36 +834,42 @@ __device__ __noinline__ void fused_tail(const DevTables &T, const Plan &p, const
         if (lane == 0) {
             reinterpret_cast<uint4 *>(fz.cta_rows)[blockIdx.x] = pack8(acc);
             fz.cta_doms[blockIdx.x] = sdom[0];
+            uint32_t prev;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.ticket) : "memory");
+            s_last = prev + 1 == gridDim.x;
+            if (s_last) atomicExch(fz.ticket, 0u);  // every CTA has its ticket: reset for the next launch
         }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t prev;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.ticket) : "memory");
-        s_last = prev + 1 == gridDim.x;
-        if (s_last) atomicExch(fz.ticket, 0u);  // every CTA has its ticket: reset for the next launch
+    } else if (threadIdx.x == 0) {
+        s_last = 0;
     }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[16], gtimer());
 #endif
     if (!s_last) return;
-    if (fz.starts) {
+    // last CTA: stage the CTA maps, fold 32 per warp, then the warp results
+    const uint32_t G = gridDim.x, ng = (G + 31) / 32;
+    uint4 *crow = smem, *wres = smem + G;
+    for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) crow[b] = __ldcg(reinterpret_cast<const uint4 *>(fz.cta_rows) + b);
+    __syncthreads();
+    if (fz.starts && threadIdx.x == 0) {
         // rank code of the state at every CTA's first leaf: the prefix of Eq.SeqReduction
-        // over the CTA maps, staged in shared memory (the input's first state is rank 0 of {q0})
-        for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) leaves[b] = __ldcg(reinterpret_cast<const uint4 *>(fz.cta_rows) + b);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t code = kRank;
-            for (uint32_t b = 0; b < gridDim.x; b++) {
-                fz.cta_code[b] = (uint16_t)code;
-                if (is_rank(code)) code = reinterpret_cast<const uint16_t *>(leaves + b)[code - kRank];
-            }
+        // over the CTA maps (the input's first state is rank 0 of {q0})
+        uint32_t code = kRank;
+        for (uint32_t b = 0; b < G; b++) {
+            fz.cta_code[b] = (uint16_t)code;
+            if (is_rank(code)) code = reinterpret_cast<const uint16_t *>(crow + b)[code - kRank];
         }
     }
+    if (warp < ng) {
+        uint32_t acc[kLanes];
+        warp_fold(crow + 32 * warp, min(32u, G - 32 * warp), acc, false);
+        if (lane == 0) wres[warp] = pack8(acc);
+    }
+    __syncthreads();
     if (warp != 0) return;
     uint32_t acc[kLanes];
-    warp_fold(reinterpret_cast<const uint4 *>(fz.cta_rows), gridDim.x, acc, true);
+    warp_fold(wres, ng, acc, false);
     if (lane == 0) {
         const uint32_t fs = acc[0];  // absolute: the input's last sub-chunk ends in states
         if (fs == T.poison) atomicMax(&status->err, 5u);
@@ -891,6 +924,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     uint64_t work = 0;  // executed lane-steps of this thread (DFA_OPT_COUNT_WORK)
     uint4 my_leaf = make_uint4(0, 0, 0, 0);  // fused tail: this thread's leaf (group leaders)
     uint32_t my_leaf_dom = 0;
+    if (fz.on && fz.rows) tail_prefetch(T, p, fz, in, smem4, g_log);
 
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -2275,10 +2309,13 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
                             converge_smem_bytes(T, warps_per_cta), s);
 }
 
+// tail area (leaves, segment maps, their domains; or the last CTA's CTA maps and warp
+// results), rounded to 16 bytes: the info area (decode domains, s_last) follows
 int fused_tail_smem_bytes(int threads, uint32_t g_log, int grid) {
     const int lpc = threads >> g_log;
-    return std::max(lpc * 16 * 2 + lpc * 2 * 2 + 16, grid * 16 + 16);
+    return std::max(lpc * 16 * 2 + lpc * 2 * 2, (grid + 32) * 16 + 16) + 15 & ~15;
 }
+int fused_info_bytes(int threads, uint32_t g_log) { return 2 * (threads >> g_log) + 16; }
 
 // fused_starts_kernel: true start of every reporting chunk for the fused tail.  CTA b
 // stages the segment maps of lanes-CTA b (slots k + b, k = its chunks) and walks them
@@ -2319,7 +2356,13 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
                     (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status, (void *)&cap,
                     (void *)&fz};
     int smem = lanes_smem_bytes(T);
-    if (fz.on) smem = std::max(smem, fused_tail_smem_bytes(threads, g_log, grid));
+    Fuse f2 = fz;
+    if (fz.on) {
+        // info area after both the table image and the tail area (it is written at kernel start)
+        f2.info_off = (uint32_t)((std::max(smem, fused_tail_smem_bytes(threads, g_log, grid)) + 15) & ~15);
+        smem = (int)f2.info_off + fused_info_bytes(threads, g_log);
+    }
+    args[16] = (void *)&f2;
     return cudaLaunchKernel(lanes_fn(T, p.work != nullptr), dim3(grid), dim3(threads), args, smem, s);
 }
 

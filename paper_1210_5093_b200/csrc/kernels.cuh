@@ -84,6 +84,7 @@ struct Fuse {
     uint16_t *final2;
     uint16_t *starts;        // [P] true chunk starts (optional; then every segment map is
     uint16_t *cta_code;      //  published and the last CTA writes each CTA's start code)
+    uint32_t info_off;       // (set by launch_lanes) shared-memory offset of the tail's info area
 };
 
 struct DevStatus {
