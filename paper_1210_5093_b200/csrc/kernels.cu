@@ -641,90 +641,117 @@ __device__ __forceinline__ void warp_compose(uint32_t mask, uint32_t g_log, uint
     }
 }
 
+// One lane's view of a map: entry v (j = lane & 7), the map's domain (its
+// first sub-chunk's, replicated over the 8 lanes), ok = the map exists.
+struct LMap {
+    uint32_t v, dom, ok;
+};
+
+// Tree step over the 4 maps of a warp: group g (g % 2gs == 0) <- group g+gs o g.
+__device__ __forceinline__ void lmap_merge(LMap &m, uint32_t gs) {
+    const uint32_t lane = threadIdx.x & 31, g = lane >> 3;
+    const uint32_t sb = ((g + gs) & 3) * 8;
+    const uint32_t bdom = __shfl_sync(0xffffffffu, m.dom, sb);
+    const uint32_t bok = __shfl_sync(0xffffffffu, m.ok, sb);
+    const bool lead = (g & (2 * gs - 1)) == 0 && bok;
+    const uint32_t rr = m.v - kRank;
+    const bool take = lead && (!m.ok || rr < (uint32_t)kLanes);
+    const uint32_t nv = __shfl_sync(0xffffffffu, m.v, sb + (m.ok ? (rr & 7u) : (lane & 7u)));
+    if (take) m.v = nv;
+    if (lead && !m.ok) { m.dom = bdom; m.ok = 1; }
+}
+
+// Tree fold of the n >= 1 maps (rows, doms) in shared memory: each level,
+// warp w folds maps 4w..4w+3 into slot w of the other buffer (trows/tdoms,
+// >= ceil(n/4) slots; the two alternate).  Result in warp 0, lanes 0..7.
+__device__ __forceinline__ LMap cta_tree_fold(uint16_t *rows, uint16_t *doms, uint16_t *trows, uint16_t *tdoms,
+                                              uint32_t n) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t g = lane >> 3, j = lane & 7;
+    LMap m{kNone, 0, 0};
+    for (;;) {
+        const uint32_t groups = (n + 3) / 4;
+#pragma unroll 1
+        for (uint32_t w = warp; w < groups; w += nw) {
+            const uint32_t r = 4 * w + g;
+            m.ok = r < n;
+            m.v = m.ok ? rows[r * 8 + j] : (uint32_t)kNone;
+            m.dom = m.ok ? doms[r] : 0u;
+            lmap_merge(m, 1);
+            lmap_merge(m, 2);
+            if (groups > 1) {
+                if (lane < 8) trows[w * 8 + j] = (uint16_t)m.v;
+                if (lane == 0) tdoms[w] = (uint16_t)m.dom;
+            }
+        }
+        if (groups == 1) break;
+        n = groups;
+        uint16_t *t = rows; rows = trows; trows = t;
+        t = doms; doms = tdoms; tdoms = t;
+        __syncthreads();
+    }
+    return m;
+}
+
 // ---------------------------------------------------------------------------
 // Fused composition tail (struct Fuse in kernels.cuh).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void unpack8(uint4 v, uint32_t (&f)[kLanes]) {
-    f[0] = v.x & 0xFFFFu; f[1] = v.x >> 16; f[2] = v.y & 0xFFFFu; f[3] = v.y >> 16;
-    f[4] = v.z & 0xFFFFu; f[5] = v.z >> 16; f[6] = v.w & 0xFFFFu; f[7] = v.w >> 16;
-}
-__device__ __forceinline__ uint4 pack8(const uint32_t (&f)[kLanes]) {
-    return make_uint4((f[0] & 0xFFFFu) | (f[1] << 16), (f[2] & 0xFFFFu) | (f[3] << 16),
-                      (f[4] & 0xFFFFu) | (f[5] << 16), (f[6] & 0xFFFFu) | (f[7] << 16));
-}
-// acc <- next o acc (Eq.MapReduction on rank-space maps: a rank code of acc indexes next)
-__device__ __forceinline__ void compose_into(uint32_t (&acc)[kLanes], const uint32_t (&nx)[kLanes]) {
-#pragma unroll
-    for (int q = 0; q < kLanes; q++) {
-        const uint32_t rr = acc[q] - kRank;
-        if (rr >= (uint32_t)kLanes) continue;
-        uint32_t v = 0;
-#pragma unroll
-        for (int t = 0; t < kLanes; t++) v |= nx[t] & (0u - (uint32_t)(rr == (uint32_t)t));
-        acc[q] = v;
-    }
-}
-// One warp folds the n >= 1 maps rows[0..n) in order; lane 0 returns the composition.
-// Lane = map, butterfly over 32 maps (L_t <- L_{t+step} o L_t), batches of 32 chained.
-__device__ __forceinline__ void warp_fold(const uint4 *rows, uint32_t n, uint32_t (&acc)[kLanes], bool cg) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
-        uint32_t f[kLanes];
-        const bool valid = b0 + lane < n;
-        if (valid) unpack8(cg ? __ldcg(rows + b0 + lane) : rows[b0 + lane], f);
-        else {
-#pragma unroll
-            for (int q = 0; q < kLanes; q++) f[q] = kNone;
-        }
-#pragma unroll
-        for (uint32_t step = 1; step < 32; step *= 2) {
-            uint32_t pm[kLanes];
-#pragma unroll
-            for (int q = 0; q < kLanes; q++) pm[q] = __shfl_down_sync(0xffffffffu, f[q], step);
-            const bool pv = __shfl_down_sync(0xffffffffu, valid, step);
-            if ((lane & (2 * step - 1)) == 0 && pv && lane + step < 32) compose_into(f, pm);
-        }
-        if (b0 == 0) {
-#pragma unroll
-            for (int q = 0; q < kLanes; q++) acc[q] = f[q];
-        } else {
-            compose_into(acc, f);
-        }
-    }
-}
-// Reporting chunk k's map (lane 0's acc, domain d0): rank-space row, domain, and the API
-// outputs -- the user-order row with states (rank codes decoded through the next chunk's
-// I_sigma, sigma = the byte before b_{k+1}), chunk 0's e0 / user row.  One warp.
-__device__ __forceinline__ void emit_chunk(const DevTables &T, const Fuse &fz, uint32_t k, uint32_t d0, uint32_t nd,
-                                           const uint32_t (&acc)[kLanes]) {
-    const uint32_t lane = threadIdx.x & 31, j = lane & 7;
-    uint32_t av = 0;
-#pragma unroll
-    for (int e = 0; e < kLanes; e++) {
-        const uint32_t v = __shfl_sync(0xffffffffu, acc[e], 0);
-        if (j == (uint32_t)e) av = v;
-    }
+// Reporting chunk k's map, 8-lane group view (lane gb + j holds entry j, domain d0):
+// the rank-space row and domain, and the API outputs -- the user-order row with states
+// (rank codes decoded through the next chunk's I_sigma nd, sigma = the byte before
+// b_{k+1}), chunk 0's e0 / user row.  Every lane of the warp calls (has = this group's).
+__device__ __forceinline__ void emit_chunk(const DevTables &T, const Fuse &fz, bool has, uint32_t k, uint32_t d0,
+                                           uint32_t nd, uint32_t av) {
+    const uint32_t lane = threadIdx.x & 31, j = lane & 7, gb = lane & ~7u;
     // independent loads first: the decode row, the user-order translation
-    const uint32_t dl = k + 1 < fz.P && lane < 8 ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.rs + j) : kNone;
-    uint32_t du, xl;
-    if (d0 < T.nclass) {
+    const uint32_t dl = has && k + 1 < fz.P ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.rs + j) : kNone;
+    uint32_t du = 0, xl = j;
+    if (has && d0 < T.nclass) {
         du = T.dom_user_size[d0];
         xl = j < T.imax_user ? T.xlat[(uint64_t)d0 * T.imax_user + j] : 0u;
-    } else {
+    } else if (has) {
         du = d0 == T.start_dom ? 1u : 0u;
-        xl = j;
     }
-    if (lane < 8) fz.rep_rows[(uint64_t)k * 8 + j] = (uint16_t)av;
-    if (lane == 0) fz.rep_doms[k] = (uint16_t)d0;
+    if (has) {
+        fz.rep_rows[(uint64_t)k * 8 + j] = (uint16_t)av;
+        if (j == 0) fz.rep_doms[k] = (uint16_t)d0;
+    }
     const uint32_t rr = av - kRank;
-    const uint32_t dv = __shfl_sync(0xffffffffu, dl, rr & 7u);
+    const uint32_t dv = __shfl_sync(0xffffffffu, dl, gb + (rr & 7u));
     const uint32_t sv = rr < (uint32_t)kLanes ? dv : av;
-    if (fz.e0 && k == 0 && lane == 0) fz.e0[0] = (uint16_t)sv;
+    if (has && fz.e0 && k == 0 && j == 0) fz.e0[0] = (uint16_t)sv;
     uint16_t *urow = nullptr;
-    if (fz.user_rows && k > 0) urow = fz.user_rows + (uint64_t)(k - 1) * T.imax_user;
-    else if (fz.user_row0 && k == 0) urow = fz.user_row0;
-    const uint32_t v = __shfl_sync(0xffffffffu, sv, xl & 7u);
-    if (urow && lane < 8 && j < T.imax_user) urow[j] = (uint16_t)(j < du ? v : kNone);
+    if (has && fz.user_rows && k > 0) urow = fz.user_rows + (uint64_t)(k - 1) * T.imax_user;
+    else if (has && fz.user_row0 && k == 0) urow = fz.user_row0;
+    const uint32_t v = __shfl_sync(0xffffffffu, sv, gb + (xl & 7u));
+    if (urow && j < T.imax_user) urow[j] = (uint16_t)(j < du ? v : kNone);
+}
+
+// Group-sequential fold (compose8's chunk phase): group g of the warp folds its n maps
+// rows[0..n) (u16 rows of 8, in order); returns entry j of the composition.  Every lane
+// of the warp calls; groups may have different n (0 = none).
+__device__ __forceinline__ uint32_t group_fold(const uint16_t *rows, uint32_t n, bool cg) {
+    const uint32_t lane = threadIdx.x & 31, j = lane & 7, gb = lane & ~7u;
+    const uint32_t nmax = __reduce_max_sync(0xffffffffu, n);
+    uint32_t av = kNone, aok = 0;
+#pragma unroll 1
+    for (uint32_t t0 = 0; t0 < nmax; t0 += 8) {
+        uint32_t lv[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            lv[q] = t0 + q < n ? (uint32_t)(cg ? __ldcg(rows + (uint64_t)(t0 + q) * 8 + j) : rows[(t0 + q) * 8 + j])
+                               : (uint32_t)kNone;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const bool bok = t0 + q < n;
+            const uint32_t rr = av - kRank;
+            const bool take = bok && (!aok || rr < (uint32_t)kLanes);
+            const uint32_t nv = __shfl_sync(0xffffffffu, lv[q], gb + (aok ? (rr & 7u) : j));
+            if (take) av = nv;
+            aok |= bok;
+        }
+    }
+    return av;
 }
 
 // Segment geometry of the fused tail: CTA b holds leaves [l0, l0 + nl), which lie in
@@ -749,6 +776,22 @@ __device__ __forceinline__ TailGeom tail_geom(const Plan &p, const Fuse &fz, uin
     g.nseg = g.nl ? fuse_chunk_of(fz, g.l0 + g.nl - 1) - g.ka + 1 : 0;
     return g;
 }
+// Tail shared-memory layout for N = max(leaves per CTA, grid) maps: [rows N][segs N]
+// [parts N][scratch N/4+1] (uint4 each), then u16 [ldom N][sdom N][pdom N][scratch N/4+1].
+struct TailSmem {
+    uint16_t *rows, *segs, *prow, *scr, *ldom, *sdom, *pdom, *sdoms;
+    __device__ __forceinline__ TailSmem(uint4 *smem, uint32_t N) {
+        const uint32_t ns = N / 4 + 1;
+        rows = reinterpret_cast<uint16_t *>(smem);
+        segs = reinterpret_cast<uint16_t *>(smem + N);
+        prow = reinterpret_cast<uint16_t *>(smem + 2 * N);
+        scr = reinterpret_cast<uint16_t *>(smem + 3 * N);
+        ldom = reinterpret_cast<uint16_t *>(smem + 3 * N + ns);
+        sdom = ldom + N;
+        pdom = sdom + N;
+        sdoms = pdom + N;
+    }
+};
 // At kernel start (latency hidden by the match loop): the decode domain of each segment's
 // chunk -- I_sigma of the byte before b_{k+1} -- into the tail's info area.
 __device__ __forceinline__ void tail_prefetch(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
@@ -761,96 +804,155 @@ __device__ __forceinline__ void tail_prefetch(const DevTables &T, const Plan &p,
     }
 }
 
-// The tail proper (every thread of the CTA; the CTA's matching is done).  Shared
-// memory (the table's, no longer read): leaves [LPC] uint4, their domains, the
-// per-chunk segment maps; the info area (after everything) holds the decode domains.
-__device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
-                                           uint4 *smem, uint32_t g_log, uint4 my_leaf, uint32_t my_leaf_dom,
-                                           DevStatus *status) {
+// The tail proper (every thread of the CTA; the CTA's matching is done).  Shared memory
+// is the table's (no longer read), laid out as TailSmem; the info area follows it.
+__device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, const Fuse &fz, uint4 *smem,
+                                           uint32_t g_log, uint4 my_leaf, uint32_t my_leaf_dom, DevStatus *status) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t j = lane & 7, grp = lane >> 3;
     const TailGeom g = tail_geom(p, fz, g_log);
     const uint32_t LPC = g.LPC, nl = g.nl, ka = g.ka, nseg = g.nseg;
     const uint64_t l0 = g.l0;
-    uint4 *leaves = smem;                                                  // [LPC]
-    uint4 *segs = smem + LPC;                                              // [LPC]
-    uint16_t *ldom = reinterpret_cast<uint16_t *>(smem + 2 * LPC);         // [LPC]
-    uint16_t *sdom = ldom + LPC;                                           // [LPC]
+    TailSmem S(smem, max(LPC, gridDim.x));
     const uint16_t *info = reinterpret_cast<const uint16_t *>(reinterpret_cast<const uint8_t *>(smem) + fz.info_off);
     // (no static __shared__ in the lanes kernel: it would move the table's shared address,
     // which the IdentU8 state bias is derived from)
     uint32_t &s_last = *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off + 2u * LPC + 4u);
     __syncthreads();  // every warp is past its match loop: the table's space is free
     if ((threadIdx.x & ((1u << g_log) - 1)) == 0 && (threadIdx.x >> g_log) < nl) {
-        leaves[threadIdx.x >> g_log] = my_leaf;
-        ldom[threadIdx.x >> g_log] = (uint16_t)my_leaf_dom;
+        reinterpret_cast<uint4 *>(S.rows)[threadIdx.x >> g_log] = my_leaf;
+        S.ldom[threadIdx.x >> g_log] = (uint16_t)my_leaf_dom;
     }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[11], gtimer());
 #endif
-    for (uint32_t sgi = warp; sgi < nseg; sgi += nw) {
+    // segment sgi: chunk k = ka + sgi, its leaves [a, b) in this CTA (relative to l0); a
+    // chunk wholly in this CTA yields its reporting row here, a straddling chunk publishes
+    // this CTA's part (slot k + b) and the last CTA to arrive folds the parts in order
+    auto seg_range = [&](uint32_t sgi, uint32_t &a, uint32_t &n, bool &whole, uint32_t &b_lo, uint32_t &nparts) {
         const uint32_t k = ka + sgi;
         const uint64_t f = fuse_first_leaf(fz, k), e = fuse_first_leaf(fz, k + 1);
-        const uint64_t a = max(f, l0), b = min(e, l0 + nl);
-        uint32_t acc[kLanes];
-        warp_fold(leaves + (a - l0), (uint32_t)(b - a), acc, false);
-        const uint32_t d = ldom[a - l0];
-        if (lane == 0) {
-            segs[sgi] = pack8(acc);
-            sdom[sgi] = (uint16_t)d;
-            if (fz.starts) reinterpret_cast<uint4 *>(fz.part_rows)[k + blockIdx.x] = pack8(acc);  // starts walk
+        const uint64_t a64 = max(f, l0), b64 = min(e, l0 + nl);
+        a = (uint32_t)(a64 - l0);
+        n = (uint32_t)(b64 - a64);
+        whole = f >= l0 && e <= l0 + nl;
+        b_lo = (uint32_t)(f / LPC);
+        nparts = (uint32_t)((e - 1) / LPC) - b_lo + 1;
+    };
+    // short segments (<= 64 leaves, <= 8 parts): an 8-lane group each, sequential folds
+    auto is_big = [&](uint32_t sgi) {
+        uint32_t a, n, b_lo, np;
+        bool whole;
+        seg_range(sgi, a, n, whole, b_lo, np);
+        return n > 64 || (!whole && np > 8);
+    };
+    for (uint32_t s0 = warp * 4; s0 < nseg; s0 += nw * 4) {
+        const uint32_t sgi = s0 + grp, k = ka + sgi;
+        uint32_t a = 0, n = 0, b_lo = 0, nparts = 0;
+        bool whole = true;
+        bool has = sgi < nseg;
+        if (has) {
+            seg_range(sgi, a, n, whole, b_lo, nparts);
+            if (n > 64 || (!whole && nparts > 8)) has = false;  // the CTA-wide pass below
+        }
+        const uint32_t av = group_fold(S.rows + a * 8, has ? n : 0u, false);
+        const uint32_t d = has ? S.ldom[a] : 0u;
+        if (has) {
+            S.segs[sgi * 8 + j] = (uint16_t)av;
+            if (j == 0) S.sdom[sgi] = (uint16_t)d;
+            if (fz.starts) fz.part_rows[((uint64_t)k + blockIdx.x) * 8 + j] = (uint16_t)av;  // starts walk
         }
         if (!fz.rows) continue;
-        if (a == f && b == e) {
-            emit_chunk(T, fz, k, d, info[sgi], acc);  // the whole chunk is in this CTA
-            continue;
-        }
-        // a straddling chunk: publish this CTA's part (slot k + b), the last CTA to arrive
-        // folds the parts in order
-        const uint32_t slot = k + blockIdx.x;
-        if (lane == 0) {
-            reinterpret_cast<uint4 *>(fz.part_rows)[slot] = pack8(acc);
-            fz.part_doms[slot] = (uint16_t)d;
+        const bool part = has && !whole;
+        if (part) {
+            fz.part_rows[((uint64_t)k + blockIdx.x) * 8 + j] = (uint16_t)av;
+            if (j == 0) fz.part_doms[k + blockIdx.x] = (uint16_t)d;
         }
         __syncwarp();
-        const uint32_t b_lo = (uint32_t)(f / LPC), b_hi = (uint32_t)((e - 1) / LPC);
         uint32_t prev = 0;
-        if (lane == 0)
+        if (part && j == 0)
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.chunk_cnt + k) : "memory");
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev + 1 != b_hi - b_lo + 1) continue;
-        if (lane == 0) fz.chunk_cnt[k] = 0;  // every part has arrived: reset for the next launch
-        warp_fold(reinterpret_cast<const uint4 *>(fz.part_rows) + k + b_lo, b_hi - b_lo + 1, acc, true);
-        emit_chunk(T, fz, k, __ldcg(fz.part_doms + k + b_lo), info[sgi], acc);
+        prev = __shfl_sync(0xffffffffu, prev, lane & ~7u);
+        const bool last = part && prev + 1 == nparts;
+        if (last && j == 0) fz.chunk_cnt[k] = 0;  // every part has arrived: reset for the next launch
+        const uint32_t pv = group_fold(fz.part_rows + ((uint64_t)k + b_lo) * 8, last ? nparts : 0u, true);
+        const bool out = (has && whole) || last;
+        const uint32_t od = last ? (uint32_t)__ldcg(fz.part_doms + k + b_lo) : d;
+        emit_chunk(T, fz, out, k, od, out ? (uint32_t)info[sgi] : 0u, last ? pv : av);
+    }
+    // big segments (a chunk of > 64 leaves here, or one spanning > 8 CTAs; at most a few
+    // per CTA): the whole CTA folds each, and the parts when it arrives last
+    for (uint32_t sgi = 0; sgi < nseg; sgi++) {
+        if (!is_big(sgi)) continue;  // (uniform over the CTA)
+        const uint32_t k = ka + sgi;
+        uint32_t a, n, b_lo, nparts;
+        bool whole;
+        seg_range(sgi, a, n, whole, b_lo, nparts);
+        __syncthreads();
+        const uint32_t d = S.ldom[a];
+        const LMap m = cta_tree_fold(S.rows + a * 8, S.ldom + a, S.scr, S.sdoms, n);
+        if (warp == 0) {
+            if (lane < 8) {
+                S.segs[sgi * 8 + j] = (uint16_t)m.v;
+                if (fz.starts || (fz.rows && !whole)) fz.part_rows[((uint64_t)k + blockIdx.x) * 8 + j] = (uint16_t)m.v;
+            }
+            if (lane == 0) {
+                S.sdom[sgi] = (uint16_t)d;
+                s_last = 0;
+                if (fz.rows && !whole) {
+                    fz.part_doms[k + blockIdx.x] = (uint16_t)d;
+                    uint32_t prev;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.chunk_cnt + k) : "memory");
+                    if (prev + 1 == nparts) {
+                        fz.chunk_cnt[k] = 0;
+                        s_last = 1;
+                    }
+                }
+            }
+            if (fz.rows && whole) emit_chunk(T, fz, grp == 0, k, d, info[sgi], m.v);
+        }
+        __syncthreads();
+        if (!s_last) continue;
+        for (uint32_t t = threadIdx.x; t < nparts; t += blockDim.x) {
+            reinterpret_cast<uint4 *>(S.prow)[t] = __ldcg(reinterpret_cast<const uint4 *>(fz.part_rows) + k + b_lo + t);
+            S.pdom[t] = __ldcg(fz.part_doms + k + b_lo + t);
+        }
+        __syncthreads();
+        const uint32_t pd = S.pdom[0];
+        const LMap pm = cta_tree_fold(S.prow, S.pdom, S.scr, S.sdoms, nparts);
+        if (warp == 0) emit_chunk(T, fz, grp == 0, k, pd, info[sgi], pm.v);
     }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[12], gtimer());
 #endif
     // the CTA map: its segment maps in order
-    if (warp == 0 && nseg) {
-        uint32_t acc[kLanes];
-        warp_fold(segs, nseg, acc, false);
+    LMap cm{kNone, 0, 0};
+    if (nseg > 1) cm = cta_tree_fold(S.segs, S.sdom, S.scr, S.sdoms, nseg);
+    else cm.v = j < 8 ? S.segs[j] : kNone;
+    if (warp == 0) {
+        if (lane < 8) fz.cta_rows[(uint64_t)blockIdx.x * 8 + j] = (uint16_t)cm.v;
+        if (lane == 0) fz.cta_doms[blockIdx.x] = S.sdom[0];
+        __syncwarp();
         if (lane == 0) {
-            reinterpret_cast<uint4 *>(fz.cta_rows)[blockIdx.x] = pack8(acc);
-            fz.cta_doms[blockIdx.x] = sdom[0];
             uint32_t prev;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(fz.ticket) : "memory");
             s_last = prev + 1 == gridDim.x;
             if (s_last) atomicExch(fz.ticket, 0u);  // every CTA has its ticket: reset for the next launch
         }
-    } else if (threadIdx.x == 0) {
-        s_last = 0;
     }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[16], gtimer());
 #endif
     if (!s_last) return;
-    // last CTA: stage the CTA maps, fold 32 per warp, then the warp results
-    const uint32_t G = gridDim.x, ng = (G + 31) / 32;
-    uint4 *crow = smem, *wres = smem + G;
-    for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) crow[b] = __ldcg(reinterpret_cast<const uint4 *>(fz.cta_rows) + b);
+    // last CTA: the CTA maps staged in shared memory and folded by the whole CTA
+    const uint32_t G = gridDim.x;
+    for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) {
+        reinterpret_cast<uint4 *>(S.rows)[b] = __ldcg(reinterpret_cast<const uint4 *>(fz.cta_rows) + b);
+        S.ldom[b] = __ldcg(fz.cta_doms + b);
+    }
     __syncthreads();
     if (fz.starts && threadIdx.x == 0) {
         // rank code of the state at every CTA's first leaf: the prefix of Eq.SeqReduction
@@ -858,20 +960,15 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
         uint32_t code = kRank;
         for (uint32_t b = 0; b < G; b++) {
             fz.cta_code[b] = (uint16_t)code;
-            if (is_rank(code)) code = reinterpret_cast<const uint16_t *>(crow + b)[code - kRank];
+            if (is_rank(code)) code = S.rows[b * 8 + (code - kRank)];
         }
     }
-    if (warp < ng) {
-        uint32_t acc[kLanes];
-        warp_fold(crow + 32 * warp, min(32u, G - 32 * warp), acc, false);
-        if (lane == 0) wres[warp] = pack8(acc);
-    }
     __syncthreads();
-    if (warp != 0) return;
-    uint32_t acc[kLanes];
-    warp_fold(wres, ng, acc, false);
-    if (lane == 0) {
-        const uint32_t fs = acc[0];  // absolute: the input's last sub-chunk ends in states
+    LMap fm{kNone, 0, 0};
+    if (G > 1) fm = cta_tree_fold(S.rows, S.ldom, S.scr, S.sdoms, G);
+    else fm.v = j < 8 ? S.rows[j] : kNone;
+    if (threadIdx.x == 0) {
+        const uint32_t fs = fm.v;  // absolute: the input's last sub-chunk ends in states
         if (fs == T.poison) atomicMax(&status->err, 5u);
         if (is_rank(fs)) atomicMax(&status->err, 8u);
         status->final_state = fs;
@@ -1061,7 +1158,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[29], gtimer());
 #endif
     if constexpr (COUNT) add_work(p.work + 1, work);
-    if (fz.on) fused_tail(T, p, fz, in, smem4, g_log, my_leaf, my_leaf_dom, status);
+    if (fz.on) fused_tail(T, p, fz, smem4, g_log, my_leaf, my_leaf_dom, status);
 }
 
 // ---------------------------------------------------------------------------
@@ -1665,58 +1762,6 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
 // a warp holds 4 maps, lane 8g + j = entry j of map g, so composing two maps
 // is one shuffle per lane (Eq.MapReduction) -- no table lookups at all.
 // ---------------------------------------------------------------------------
-// One lane's view of a map: entry v (j = lane & 7), the map's domain (its
-// first sub-chunk's, replicated over the 8 lanes), ok = the map exists.
-struct LMap {
-    uint32_t v, dom, ok;
-};
-
-// Tree step over the 4 maps of a warp: group g (g % 2gs == 0) <- group g+gs o g.
-__device__ __forceinline__ void lmap_merge(LMap &m, uint32_t gs) {
-    const uint32_t lane = threadIdx.x & 31, g = lane >> 3;
-    const uint32_t sb = ((g + gs) & 3) * 8;
-    const uint32_t bdom = __shfl_sync(0xffffffffu, m.dom, sb);
-    const uint32_t bok = __shfl_sync(0xffffffffu, m.ok, sb);
-    const bool lead = (g & (2 * gs - 1)) == 0 && bok;
-    const uint32_t rr = m.v - kRank;
-    const bool take = lead && (!m.ok || rr < (uint32_t)kLanes);
-    const uint32_t nv = __shfl_sync(0xffffffffu, m.v, sb + (m.ok ? (rr & 7u) : (lane & 7u)));
-    if (take) m.v = nv;
-    if (lead && !m.ok) { m.dom = bdom; m.ok = 1; }
-}
-
-// Tree fold of the n >= 1 maps (rows, doms) in shared memory: each level,
-// warp w folds maps 4w..4w+3 into slot w of the other buffer (trows/tdoms,
-// >= ceil(n/4) slots; the two alternate).  Result in warp 0, lanes 0..7.
-__device__ __forceinline__ LMap cta_tree_fold(uint16_t *rows, uint16_t *doms, uint16_t *trows, uint16_t *tdoms,
-                                              uint32_t n) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const uint32_t g = lane >> 3, j = lane & 7;
-    LMap m{kNone, 0, 0};
-    for (;;) {
-        const uint32_t groups = (n + 3) / 4;
-#pragma unroll 1
-        for (uint32_t w = warp; w < groups; w += nw) {
-            const uint32_t r = 4 * w + g;
-            m.ok = r < n;
-            m.v = m.ok ? rows[r * 8 + j] : (uint32_t)kNone;
-            m.dom = m.ok ? doms[r] : 0u;
-            lmap_merge(m, 1);
-            lmap_merge(m, 2);
-            if (groups > 1) {
-                if (lane < 8) trows[w * 8 + j] = (uint16_t)m.v;
-                if (lane == 0) tdoms[w] = (uint16_t)m.dom;
-            }
-        }
-        if (groups == 1) break;
-        n = groups;
-        uint16_t *t = rows; rows = trows; trows = t;
-        t = doms; doms = tdoms; tdoms = t;
-        __syncthreads();
-    }
-    return m;
-}
-
 // A rank-space entry as a state: rank codes index the next map's domain nd.
 __device__ __forceinline__ uint32_t decode_entry(const DevTables &T, uint32_t v, uint32_t nd) {
     return is_rank(v) ? (uint32_t)__ldg(T.dom_list + (uint64_t)nd * T.rs + (v - kRank)) : v;
@@ -2312,8 +2357,8 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 // tail area (leaves, segment maps, their domains; or the last CTA's CTA maps and warp
 // results), rounded to 16 bytes: the info area (decode domains, s_last) follows
 int fused_tail_smem_bytes(int threads, uint32_t g_log, int grid) {
-    const int lpc = threads >> g_log;
-    return std::max(lpc * 16 * 2 + lpc * 2 * 2, (grid + 32) * 16 + 16) + 15 & ~15;
+    const int N = std::max(threads >> g_log, grid), ns = N / 4 + 1;
+    return ((3 * N + ns) * 16 + (3 * N + ns) * 2 + 15) & ~15;  // TailSmem
 }
 int fused_info_bytes(int threads, uint32_t g_log) { return 2 * (threads >> g_log) + 16; }
 
