@@ -756,42 +756,47 @@ __device__ __forceinline__ uint32_t group_fold(const uint16_t *rows, uint32_t n,
 
 // Segment geometry of the fused tail: CTA b holds leaves [l0, l0 + nl), which lie in
 // reporting chunks ka..ka+nseg-1 (a "segment" = one chunk's leaves inside this CTA).
+// (32-bit: the fused path has one sub-chunk per thread of one wave, NS < 2^21)
 struct TailGeom {
-    uint32_t LPC, nl, ka, nseg;
-    uint64_t l0;
+    uint32_t LPC, nl, ka, nseg, l0;
 };
-__device__ __forceinline__ uint32_t fuse_chunk_of(const Fuse &fz, uint64_t l) {
-    return l < fz.L0 ? 0u : (uint32_t)(1 + (l - fz.L0) / fz.L);
+__device__ __forceinline__ uint32_t fuse_chunk_of(const Fuse &fz, uint32_t l) {
+    return l < fz.L0 ? 0u : 1u + (l - fz.L0) / fz.L;
 }
-__device__ __forceinline__ uint64_t fuse_first_leaf(const Fuse &fz, uint32_t k) {
-    return k == 0 ? 0 : (uint64_t)fz.L0 + (uint64_t)(k - 1) * fz.L;
+__device__ __forceinline__ uint32_t fuse_first_leaf(const Fuse &fz, uint32_t k) {
+    return k == 0 ? 0u : fz.L0 + (k - 1) * fz.L;
 }
 __device__ __forceinline__ TailGeom tail_geom(const Plan &p, const Fuse &fz, uint32_t g_log) {
     TailGeom g;
     g.LPC = blockDim.x >> g_log;
-    const uint64_t NL = p.NS >> g_log;
-    g.l0 = (uint64_t)blockIdx.x * g.LPC;
-    g.nl = (uint32_t)min((uint64_t)g.LPC, NL > g.l0 ? NL - g.l0 : (uint64_t)0);
+    const uint32_t NL = (uint32_t)(p.NS >> g_log);
+    g.l0 = blockIdx.x * g.LPC;
+    g.nl = min(g.LPC, NL > g.l0 ? NL - g.l0 : 0u);
     g.ka = g.nl ? fuse_chunk_of(fz, g.l0) : 0;
     g.nseg = g.nl ? fuse_chunk_of(fz, g.l0 + g.nl - 1) - g.ka + 1 : 0;
     return g;
 }
 // Tail shared-memory layout for N = max(leaves per CTA, grid) maps: [rows N][segs N]
-// [parts N][scratch N/4+1] (uint4 each), then u16 [ldom N][sdom N][pdom N][scratch N/4+1].
+// [parts N][scratch N/4+1] (uint4 each), [segment info N] (uint2), then u16 [ldom N]
+// [sdom N][pdom N][scratch N/4+1].
 struct TailSmem {
     uint16_t *rows, *segs, *prow, *scr, *ldom, *sdom, *pdom, *sdoms;
+    uint2 *sinfo;
     __device__ __forceinline__ TailSmem(uint4 *smem, uint32_t N) {
         const uint32_t ns = N / 4 + 1;
         rows = reinterpret_cast<uint16_t *>(smem);
         segs = reinterpret_cast<uint16_t *>(smem + N);
         prow = reinterpret_cast<uint16_t *>(smem + 2 * N);
         scr = reinterpret_cast<uint16_t *>(smem + 3 * N);
-        ldom = reinterpret_cast<uint16_t *>(smem + 3 * N + ns);
+        sinfo = reinterpret_cast<uint2 *>(smem + 3 * N + ns);
+        ldom = reinterpret_cast<uint16_t *>(sinfo + N);
         sdom = ldom + N;
         pdom = sdom + N;
         sdoms = pdom + N;
     }
 };
+// segment info: x = a | n << 11 | whole << 22 | big << 23 (a, n <= 1024), y = b_lo | nparts << 16
+constexpr uint32_t kSegWhole = 1u << 22, kSegBig = 1u << 23;
 // At kernel start (latency hidden by the match loop): the decode domain of each segment's
 // chunk -- I_sigma of the byte before b_{k+1} -- into the tail's info area.
 __device__ __forceinline__ void tail_prefetch(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in,
@@ -811,51 +816,42 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t j = lane & 7, grp = lane >> 3;
     const TailGeom g = tail_geom(p, fz, g_log);
-    const uint32_t LPC = g.LPC, nl = g.nl, ka = g.ka, nseg = g.nseg;
-    const uint64_t l0 = g.l0;
+    const uint32_t LPC = g.LPC, nl = g.nl, ka = g.ka, nseg = g.nseg, l0 = g.l0;
     TailSmem S(smem, max(LPC, gridDim.x));
     const uint16_t *info = reinterpret_cast<const uint16_t *>(reinterpret_cast<const uint8_t *>(smem) + fz.info_off);
     // (no static __shared__ in the lanes kernel: it would move the table's shared address,
     // which the IdentU8 state bias is derived from)
-    uint32_t &s_last = *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off + 2u * LPC + 4u);
+    uint32_t &s_last = *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off + ((2u * LPC + 7u) & ~3u));
     __syncthreads();  // every warp is past its match loop: the table's space is free
     if ((threadIdx.x & ((1u << g_log) - 1)) == 0 && (threadIdx.x >> g_log) < nl) {
         reinterpret_cast<uint4 *>(S.rows)[threadIdx.x >> g_log] = my_leaf;
         S.ldom[threadIdx.x >> g_log] = (uint16_t)my_leaf_dom;
     }
+    // segment geometry, once per segment: leaves [a, a + n) of the CTA, whole chunk or
+    // straddling (parts b_lo .. b_lo + nparts - 1), big = the CTA-wide pass
+    for (uint32_t t = threadIdx.x; t < nseg; t += blockDim.x) {
+        const uint32_t k = ka + t;
+        const uint32_t f = fuse_first_leaf(fz, k), e = fuse_first_leaf(fz, k + 1);
+        const uint32_t a = max(f, l0) - l0, n = min(e, l0 + nl) - l0 - a;
+        const bool whole = f >= l0 && e <= l0 + nl;
+        const uint32_t b_lo = f / LPC, np = (e - 1) / LPC - b_lo + 1;
+        const bool big = n > 64 || (!whole && np > 8);
+        S.sinfo[t] = make_uint2(a | n << 11 | (whole ? kSegWhole : 0u) | (big ? kSegBig : 0u), b_lo | np << 16);
+    }
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[11], gtimer());
 #endif
-    // segment sgi: chunk k = ka + sgi, its leaves [a, b) in this CTA (relative to l0); a
-    // chunk wholly in this CTA yields its reporting row here, a straddling chunk publishes
-    // this CTA's part (slot k + b) and the last CTA to arrive folds the parts in order
-    auto seg_range = [&](uint32_t sgi, uint32_t &a, uint32_t &n, bool &whole, uint32_t &b_lo, uint32_t &nparts) {
-        const uint32_t k = ka + sgi;
-        const uint64_t f = fuse_first_leaf(fz, k), e = fuse_first_leaf(fz, k + 1);
-        const uint64_t a64 = max(f, l0), b64 = min(e, l0 + nl);
-        a = (uint32_t)(a64 - l0);
-        n = (uint32_t)(b64 - a64);
-        whole = f >= l0 && e <= l0 + nl;
-        b_lo = (uint32_t)(f / LPC);
-        nparts = (uint32_t)((e - 1) / LPC) - b_lo + 1;
-    };
-    // short segments (<= 64 leaves, <= 8 parts): an 8-lane group each, sequential folds
-    auto is_big = [&](uint32_t sgi) {
-        uint32_t a, n, b_lo, np;
-        bool whole;
-        seg_range(sgi, a, n, whole, b_lo, np);
-        return n > 64 || (!whole && np > 8);
-    };
+    // segment sgi = chunk ka + sgi: a chunk wholly in this CTA yields its reporting row here,
+    // a straddling chunk publishes this CTA's part (slot k + b) and the last CTA to arrive
+    // folds the parts in order.  Short segments (<= 64 leaves, <= 8 parts): an 8-lane group
+    // each, sequential folds.
     for (uint32_t s0 = warp * 4; s0 < nseg; s0 += nw * 4) {
         const uint32_t sgi = s0 + grp, k = ka + sgi;
-        uint32_t a = 0, n = 0, b_lo = 0, nparts = 0;
-        bool whole = true;
-        bool has = sgi < nseg;
-        if (has) {
-            seg_range(sgi, a, n, whole, b_lo, nparts);
-            if (n > 64 || (!whole && nparts > 8)) has = false;  // the CTA-wide pass below
-        }
+        const uint2 si = sgi < nseg ? S.sinfo[sgi] : make_uint2(0u, 0u);
+        const uint32_t a = si.x & 2047u, n = (si.x >> 11) & 2047u, b_lo = si.y & 0xFFFFu, nparts = si.y >> 16;
+        const bool whole = (si.x & kSegWhole) != 0;
+        const bool has = sgi < nseg && !(si.x & kSegBig);  // big: the CTA-wide pass below
         const uint32_t av = group_fold(S.rows + a * 8, has ? n : 0u, false);
         const uint32_t d = has ? S.ldom[a] : 0u;
         if (has) {
@@ -884,11 +880,11 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
     // big segments (a chunk of > 64 leaves here, or one spanning > 8 CTAs; at most a few
     // per CTA): the whole CTA folds each, and the parts when it arrives last
     for (uint32_t sgi = 0; sgi < nseg; sgi++) {
-        if (!is_big(sgi)) continue;  // (uniform over the CTA)
+        const uint2 si = S.sinfo[sgi];
+        if (!(si.x & kSegBig)) continue;  // (uniform over the CTA)
         const uint32_t k = ka + sgi;
-        uint32_t a, n, b_lo, nparts;
-        bool whole;
-        seg_range(sgi, a, n, whole, b_lo, nparts);
+        const uint32_t a = si.x & 2047u, n = (si.x >> 11) & 2047u, b_lo = si.y & 0xFFFFu, nparts = si.y >> 16;
+        const bool whole = (si.x & kSegWhole) != 0;
         __syncthreads();
         const uint32_t d = S.ldom[a];
         const LMap m = cta_tree_fold(S.rows + a * 8, S.ldom + a, S.scr, S.sdoms, n);
@@ -2358,7 +2354,7 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
 // results), rounded to 16 bytes: the info area (decode domains, s_last) follows
 int fused_tail_smem_bytes(int threads, uint32_t g_log, int grid) {
     const int N = std::max(threads >> g_log, grid), ns = N / 4 + 1;
-    return ((3 * N + ns) * 16 + (3 * N + ns) * 2 + 15) & ~15;  // TailSmem
+    return ((3 * N + ns) * 16 + N * 8 + (3 * N + ns) * 2 + 15) & ~15;  // TailSmem
 }
 int fused_info_bytes(int threads, uint32_t g_log) { return 2 * (threads >> g_log) + 16; }
 
