@@ -552,7 +552,8 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
             fz.starts = o.starts;
             fz.cta_code = h->cta_start.as<uint16_t>();
         }
-    } else if (grouped) {
+    }
+    if (grouped) {
         CK(h->leaf_rows.ensure(((NS >> sp.g_log) + 1) * T.rs * 2));
         CK(h->leaf_dom.ensure(((NS >> sp.g_log) + 1) * 2));
     }

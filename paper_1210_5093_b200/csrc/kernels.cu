@@ -812,7 +812,8 @@ __device__ __forceinline__ void tail_prefetch(const DevTables &T, const Plan &p,
 // The tail proper (every thread of the CTA; the CTA's matching is done).  Shared memory
 // is the table's (no longer read), laid out as TailSmem; the info area follows it.
 __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, const Fuse &fz, uint4 *smem,
-                                           uint32_t g_log, uint4 my_leaf, uint32_t my_leaf_dom, DevStatus *status) {
+                                           uint32_t g_log, const uint16_t *leaf_rows, const uint16_t *leaf_dom,
+                                           DevStatus *status) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t j = lane & 7, grp = lane >> 3;
     const TailGeom g = tail_geom(p, fz, g_log);
@@ -822,10 +823,10 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
     // (no static __shared__ in the lanes kernel: it would move the table's shared address,
     // which the IdentU8 state bias is derived from)
     uint32_t &s_last = *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off + ((2u * LPC + 7u) & ~3u));
-    __syncthreads();  // every warp is past its match loop: the table's space is free
-    if ((threadIdx.x & ((1u << g_log) - 1)) == 0 && (threadIdx.x >> g_log) < nl) {
-        reinterpret_cast<uint4 *>(S.rows)[threadIdx.x >> g_log] = my_leaf;
-        S.ldom[threadIdx.x >> g_log] = (uint16_t)my_leaf_dom;
+    __syncthreads();  // every warp is past its match loop (its leaves are written): the table's space is free
+    for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) {
+        reinterpret_cast<uint4 *>(S.rows)[t] = __ldcg(reinterpret_cast<const uint4 *>(leaf_rows) + l0 + t);
+        S.ldom[t] = __ldcg(leaf_dom + l0 + t);
     }
     // segment geometry, once per segment: leaves [a, a + n) of the CTA, whole chunk or
     // straddling (parts b_lo .. b_lo + nparts - 1), big = the CTA-wide pass
@@ -1015,8 +1016,6 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     tab.init(T, tsm);
     const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
     uint64_t work = 0;  // executed lane-steps of this thread (DFA_OPT_COUNT_WORK)
-    uint4 my_leaf = make_uint4(0, 0, 0, 0);  // fused tail: this thread's leaf (group leaders)
-    uint32_t my_leaf_dom = 0;
     if (fz.on && fz.rows) tail_prefetch(T, p, fz, in, smem4, g_log);
 
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
@@ -1067,13 +1066,10 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
                 v.y = (fin[2] & 0xFFFFu) | (fin[3] << 16);
                 v.z = (fin[4] & 0xFFFFu) | (fin[5] << 16);
                 v.w = (fin[6] & 0xFFFFu) | (fin[7] << 16);
-                if (fz.on) {  // kept for the CTA's composition tail
-                    my_leaf = v;
-                    my_leaf_dom = dom;
-                } else {
-                    reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
-                    leaf_dom[leaf] = (uint16_t)dom;
-                }
+                // (the fused tail reads its CTA's leaves back: holding them in registers
+                // across the grid-stride loop made the match loop spill)
+                reinterpret_cast<uint4 *>(leaf_rows)[leaf] = v;
+                leaf_dom[leaf] = (uint16_t)dom;
             }
         };
         // grouped with cap = 8 (u <= 8): one pass, the map stays in registers and every
@@ -1154,7 +1150,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     if ((threadIdx.x & 31) == 0) atomicMax(&g_tree_t[29], gtimer());
 #endif
     if constexpr (COUNT) add_work(p.work + 1, work);
-    if (fz.on) fused_tail(T, p, fz, smem4, g_log, my_leaf, my_leaf_dom, status);
+    if (fz.on) fused_tail(T, p, fz, smem4, g_log, leaf_rows, leaf_dom, status);
 }
 
 // ---------------------------------------------------------------------------
