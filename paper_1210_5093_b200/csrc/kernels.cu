@@ -824,6 +824,9 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
     // which the IdentU8 state bias is derived from)
     uint32_t &s_last = *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(smem) + fz.info_off + ((2u * LPC + 7u) & ~3u));
     __syncthreads();  // every warp is past its match loop (its leaves are written): the table's space is free
+#ifdef DFA_TREE_TIMING
+    const unsigned long long t_tail0 = gtimer();
+#endif
     for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) {
         reinterpret_cast<uint4 *>(S.rows)[t] = __ldcg(reinterpret_cast<const uint4 *>(leaf_rows) + l0 + t);
         S.ldom[t] = __ldcg(leaf_dom + l0 + t);
@@ -842,6 +845,7 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[11], gtimer());
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[13], gtimer() - t_tail0);  // staging + geometry, per CTA
 #endif
     // segment sgi = chunk ka + sgi: a chunk wholly in this CTA yields its reporting row here,
     // a straddling chunk publishes this CTA's part (slot k + b) and the last CTA to arrive
@@ -878,6 +882,9 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
         const uint32_t od = last ? (uint32_t)__ldcg(fz.part_doms + k + b_lo) : d;
         emit_chunk(T, fz, out, k, od, out ? (uint32_t)info[sgi] : 0u, last ? pv : av);
     }
+#ifdef DFA_TREE_TIMING
+    if (lane == 0) atomicMax(&g_tree_t[18], gtimer() - t_tail0);  // short-segment phase, per warp
+#endif
     // big segments (a chunk of > 64 leaves here, or one spanning > 8 CTAs; at most a few
     // per CTA): the whole CTA folds each, and the parts when it arrives last
     for (uint32_t sgi = 0; sgi < nseg; sgi++) {
@@ -923,6 +930,7 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
     __syncthreads();
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMax(&g_tree_t[12], gtimer());
+    if (threadIdx.x == 0) atomicMax(&g_tree_t[17], gtimer() - t_tail0);  // whole chunk phase, per CTA
 #endif
     // the CTA map: its segment maps in order
     LMap cm{kNone, 0, 0};

@@ -1,5 +1,5 @@
 set -x
-O=gpurun_out/r02g
+O=gpurun_out/r02h
 mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "pipelined or fused or config_small or tiny_hard or segment or graph or starts or edge or 2_20" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log
 for c in tiny random keyword; do

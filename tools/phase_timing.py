@@ -32,6 +32,9 @@ for name in sys.argv[1:]:
         t0 = buf[25]
         names = {25: "lanes start", 26: "table loaded", 27: "run_lanes done(max)", 28: "warp_compose done(max)", 29: "lanes end(max)",
                  10: "compose8 start(min)", 11: "pdl_wait passed(max)", 12: "chunk phase done(max)", 16: "ticket(max)", 19: "final written"}
+        if rep >= 4 and os.environ.get("FUSED", "1") == "1":
+            print("  fused tail per-CTA max durations (us): staging+geometry", round(buf[13] / 1000, 2),
+                  "short-segment warp", round(buf[18] / 1000, 2), "chunk phase", round(buf[17] / 1000, 2))
         if rep >= 4:
             print(name, {v: round((buf[k] - t0) / 1000, 2) for k, v in names.items() if buf[k]},
                   "cta_fold_dur", round(buf[20] / 1000, 2), "ticket_dur", round(buf[21] / 1000, 2), "last_fold", round(buf[22] / 1000, 2))
