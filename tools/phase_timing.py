@@ -3,7 +3,10 @@ epilogue; compose8 PDL wait, chunk phase, ticket, last-CTA fold), in microsecond
 CTA starts.  Builds the library with -DDFA_TREE_TIMING into /tmp.  usage: tools/phase_timing.py random keyword"""
 import ctypes, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-lib = "/tmp/libdfa_timing.so"
+import hashlib
+_src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1210_5093_b200", "csrc")
+_h = hashlib.sha256(b"".join(open(os.path.join(_src, f), "rb").read() for f in sorted(os.listdir(_src)))).hexdigest()[:12]
+lib = f"/tmp/libdfa_timing_{_h}.so"  # keyed by the source: /tmp survives between calls on a reused box
 src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1210_5093_b200", "csrc")
 if not os.path.exists(lib):
     # one translation unit (DFA_TU_MODE=0: every layout's match kernels beside the composition
