@@ -75,7 +75,7 @@ struct dfa_handle {
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
     DevBuf cta_start, leaf_rows2, leaf_dom2;
     int warp_compose = 1;
-    int fused_tail = 1;           // DFA_OPT_FUSED_TAIL
+    int fused_tail = 0;           // DFA_OPT_FUSED_TAIL (measured slower than compose8: DESIGN.md)
     DevBuf part_rows, part_doms, chunk_cnt;
     std::vector<uint64_t> plan_key;
     // CUDA graph of a repeated dfa_chunk_maps call
