@@ -78,6 +78,25 @@ __device__ __forceinline__ uint64_t split_point(const Plan &p, uint64_t b0, uint
     return t - ((p.in_addr + t) & 31u);
 }
 
+// sub-chunk i's reporting chunk k (its bounds are p.bounds[k], p.bounds[k+1])
+__device__ __forceinline__ uint64_t sub_chunk_of(const Plan &p, uint64_t i) {
+    return i < p.m0 ? 0 : 1 + (i - p.m0) / p.m;
+}
+// sub_range with the chunk's bounds already loaded (b0, b1 = bounds of sub_chunk_of(i))
+__device__ __forceinline__ void sub_range_b(const Plan &p, uint64_t i, uint64_t b0, uint64_t b1, uint64_t &s,
+                                            uint64_t &e) {
+    uint64_t j, mk;
+    if (i < p.m0) { j = i; mk = p.m0; }
+    else { j = (i - p.m0) % p.m; mk = p.m; }
+    if (p.indep) {
+        b0 = min(b0, p.n);
+        b1 = min(max(b1, b0), p.n);
+    }
+    const uint64_t len = b1 - b0;
+    s = split_point(p, b0, len, j, mk);
+    e = split_point(p, b0, len, j + 1, mk);
+}
+
 __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s, uint64_t &e) {
     uint64_t k, j, mk;
     if (i < p.m0) { k = 0; j = i; mk = p.m0; }
@@ -1227,9 +1246,28 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
 
     const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
     uint64_t work = 0;  // lane-steps of this warp (counted on lane 0; DFA_OPT_COUNT_WORK)
-    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; i < p.NS; i += warps_total) {
+    // The stage is latency-bound (a few windows per sub-chunk, each a dependent chain):
+    // the next sub-chunk's bounds are loaded one iteration ahead, and the first 512 bytes
+    // of a sub-chunk are fetched at once (one 16-byte block per lane) before its domain
+    // is looked up, so the windows take their bytes by shuffle instead of a load each.
+    uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    uint64_t nb0 = 0, nb1 = 0;
+    if (i < p.NS) {
+        const uint64_t k = sub_chunk_of(p, i);
+        nb0 = p.bounds[k];
+        nb1 = p.bounds[k + 1];
+    }
+    for (; i < p.NS; i += warps_total) {
         uint64_t start, end;
-        sub_range(p, i, start, end);
+        sub_range_b(p, i, nb0, nb1, start, end);
+        if (i + warps_total < p.NS) {
+            const uint64_t k = sub_chunk_of(p, i + warps_total);
+            nb0 = p.bounds[k];
+            nb1 = p.bounds[k + 1];
+        }
+        const uint64_t ab0 = start - ((reinterpret_cast<uintptr_t>(in) + start) & 15u);
+        const uint64_t pb = ab0 + 16ull * lane;
+        const uint4 pre = pb + 16 <= p.n ? ldg16(reinterpret_cast<const uint4 *>(in + pb)) : make_uint4(0, 0, 0, 0);
         const uint32_t dom = sub_domain(T, p, in, i, start);
         const uint32_t u = T.dom_size[dom];
         for (uint32_t e = lane; e < u; e += 32) {
@@ -1250,7 +1288,13 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
             k1 = min(k1, k0 + wlen);
             wlen = min(wlen * 2, 16u);
             uint4 v;
-            if (abase + 16 <= p.n && abase <= pos) {
+            const uint64_t wi = (abase - ab0) >> 4;  // (uniform over the warp)
+            if (abase + 16 <= p.n && wi < 32) {
+                v.x = __shfl_sync(0xffffffffu, pre.x, (uint32_t)wi);
+                v.y = __shfl_sync(0xffffffffu, pre.y, (uint32_t)wi);
+                v.z = __shfl_sync(0xffffffffu, pre.z, (uint32_t)wi);
+                v.w = __shfl_sync(0xffffffffu, pre.w, (uint32_t)wi);
+            } else if (abase + 16 <= p.n && abase <= pos) {
                 v = ldg16(reinterpret_cast<const uint4 *>(in + abase));
             } else {  // last partial block of the input: byte loads, never past n
                 uint32_t wv[4] = {0, 0, 0, 0};
