@@ -266,26 +266,21 @@ def main():
         k, v = kv.split("=")
         D.dfa_set_option(d.h, OPTS[k], int(v))
     imax = d.info["i_max"]
-    bounds = torch.empty(P + 1, dtype=torch.int64, device=dev)
-    e0 = torch.empty(1, dtype=torch.int16, device=dev)
-    maps = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=dev)
-    final = torch.empty(2, dtype=torch.int16, device=dev)
     stream = torch.cuda.current_stream(dev)
-    seg = None
-    if world > 1:
-        # weak scaling: this rank's input is segment `rank` of one N-segment string
-        from paper_1210_5093_b200 import multi_gpu
-        smap, fold = multi_gpu.gpu_ops(d, dx, stream=stream)
-        seg = multi_gpu.SegmentMatcher(rank, world, dist, dx[-1:], smap, fold)
+    # one code path for every N: each rank runs dfa_segment_chunk_maps on its segment (P
+    # chunks; the same partition and kernels as dfa_chunk_maps), and for N > 1 the segment
+    # rows are all-gathered over NCCL and folded; weak scaling: rank r holds segment r of
+    # one N-segment string
+    from paper_1210_5093_b200 import multi_gpu
+    smap, fold = multi_gpu.gpu_ops(d, dx, stream=stream, chunks=P)
+    seg = multi_gpu.SegmentMatcher(rank, world, dist, dx[-1:], smap, fold)
+    bounds, maps, seg_row = smap.bounds, smap.maps, smap.row
 
     # inputs that fit in L2 are flushed between steps (timing rule): a 256 MiB write
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if n <= (126 << 20) else None
 
     def step():
-        if seg is not None:
-            seg.step()      # segment map, one all-gather of I_max uint16 per rank, fold
-        else:
-            D.dfa_chunk_maps(d.h, dx, P, bounds, e0, maps, None, final, stream=stream)
+        seg.step()      # segment chunk maps [, one all-gather of I_max uint16 per rank, fold]
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -330,9 +325,8 @@ def main():
     value = world * n / (ms * 1e-3) / 1e9
     if D.dfa_get_last_device_error(d.h) != 0:
         raise SystemExit("device error during bench")
-    if seg is None:
-        torch.cuda.synchronize(dev)
-        fin_dev = int(final.cpu().numpy().view(np.uint16)[0])
+    torch.cuda.synchronize(dev)
+    fin_dev = int(seg_row.cpu().numpy().view(np.uint16)[0])  # N = 1: the final state
 
     # executed work (frac_exec): the same step with the lane-step counters on, untimed
     work = None

@@ -246,6 +246,27 @@ dfa_status dfa_lookahead_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t
  */
 dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, int32_t lookahead,
                            void *stream, uint16_t *dev_row);
+/*
+ * dfa_segment_chunk_maps: the per-GPU step of the sharded path with the same
+ * partition and kernels as dfa_chunk_maps.  The segment (dev_input, len) is cut
+ * into num_chunks chunks (c-form, dfa_set_chunk_ratio); chunk 0 is matched from
+ * {q0} (lookahead = -1: the segment starts the string) or from I_sigma of
+ * sigma = lookahead (the byte before the segment, Eq.istates).
+ * Outputs (caller-owned device memory; asynchronous on `stream`):
+ *   dev_bounds       [num_chunks+1] uint64 chunk bounds (may be NULL)
+ *   dev_chunk0_row   lookahead = -1: [1] = e0 = delta-hat(q0, C_0); else
+ *                    [i_max] = chunk 0's map over the user's I_sigma (ascending, 0xFFFF padded)
+ *   dev_maps         [(num_chunks-1) * i_max] rows of chunks 1.., as dfa_chunk_maps
+ *   dev_segment_row  [i_max] the composed map of the whole segment over chunk 0's
+ *                    domain (Eq.MapReduction), i.e. the dfa_segment_map row; for
+ *                    lookahead = -1 entry 0 is the segment's final state
+ * Repeated identical calls replay a captured CUDA graph; the partition stays on
+ * the device (no host round trip per call).  Errors as dfa_chunk_maps, plus
+ * DFA_ERR_SYMBOL for lookahead >= |Sigma|.
+ */
+dfa_status dfa_segment_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
+                                  int32_t lookahead, void *stream, uint64_t *dev_bounds,
+                                  uint16_t *dev_chunk0_row, uint16_t *dev_maps, uint16_t *dev_segment_row);
 dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uint8_t *dev_lookahead,
                              uint32_t G, void *stream, uint16_t *dev_final);
 

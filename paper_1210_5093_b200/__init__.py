@@ -22,7 +22,8 @@ __all__ = [
     "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
     "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
     "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
-    "dfa_lookahead_maps", "dfa_match_batch", "dfa_gather_ceiling", "Dfa", "lib", "EXPORTED",
+    "dfa_lookahead_maps", "dfa_match_batch", "dfa_gather_ceiling", "dfa_segment_chunk_maps", "Dfa", "lib",
+    "EXPORTED",
 ]
 
 DFA_OK, DFA_ERR_ARG, DFA_ERR_STATES, DFA_ERR_ALPHABET, DFA_ERR_CHUNKS = 0, 1, 2, 3, 4
@@ -76,7 +77,7 @@ EXPORTED = ["dfa_create", "dfa_create_ex", "dfa_destroy", "dfa_get_info", "dfa_d
             "dfa_set_chunk_ratio", "dfa_plan_bounds", "dfa_match", "dfa_match_host", "dfa_chunk_maps",
             "dfa_chunk_maps_at", "dfa_get_last_device_error", "dfa_set_option", "dfa_get_stats",
             "dfa_status_string", "dfa_error_detail", "dfa_segment_map", "dfa_fold_segments",
-            "dfa_lookahead_maps", "dfa_match_batch", "dfa_gather_ceiling"]
+            "dfa_lookahead_maps", "dfa_match_batch", "dfa_gather_ceiling", "dfa_segment_chunk_maps"]
 
 _lib = None
 
@@ -110,6 +111,7 @@ def lib():
             "dfa_lookahead_maps": [V, V, u64, u32, V, V, u32, V, V, V, V],
             "dfa_match_batch": [V, V, u64, V, u32, V, V, V],
             "dfa_gather_ceiling": [V, V, u64, V, V, V, V],
+            "dfa_segment_chunk_maps": [V, V, u64, u32, ctypes.c_int32, V, V, V, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -268,6 +270,17 @@ def dfa_segment_map(h, dev_input, lookahead: int, dev_row, n: Optional[int] = No
     n = dev_input.numel() if n is None else int(n)
     _ck(lib().dfa_segment_map(h, _ptr(dev_input), n, int(lookahead), _stream(stream), _ptr(dev_row)),
         "dfa_segment_map")
+
+
+def dfa_segment_chunk_maps(h, dev_input, P: int, lookahead: int, dev_bounds, dev_chunk0_row, dev_maps,
+                           dev_segment_row, n: Optional[int] = None, stream=None):
+    """Per-GPU step of the sharded path (include/dfa.h): P chunks of the segment, chunk 0
+    from {q0} (lookahead -1) or I_sigma(lookahead); writes bounds, chunk 0's row, the maps of
+    chunks 1.. and the segment's composed map row."""
+    n = dev_input.numel() if n is None else int(n)
+    _ck(lib().dfa_segment_chunk_maps(h, _ptr(dev_input), n, P, int(lookahead), _stream(stream), _ptr(dev_bounds),
+                                     _ptr(dev_chunk0_row), _ptr(dev_maps), _ptr(dev_segment_row)),
+        "dfa_segment_chunk_maps")
 
 
 def dfa_gather_ceiling(h, dev_input=None, dev_out=None, stream=None, length=None):

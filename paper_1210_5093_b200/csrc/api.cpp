@@ -349,6 +349,7 @@ struct Outputs {
     uint16_t *user_maps = nullptr;   // [(P-1) * imax_user]
     uint16_t *starts = nullptr;      // [P]
     uint16_t *final2 = nullptr;      // [2]
+    uint16_t *seg_row = nullptr;     // [imax_user] composed map of the whole input over chunk 0's domain
     bool indep = false;              // batch: chunks are independent inputs, no fold
 };
 
@@ -512,7 +513,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
     // fused composition tail (one sub-chunk per thread, so CTAs hold contiguous leaves):
     // the lanes kernel composes its own leaves, no leaf_fold / compose8 launches
-    const bool fused = grouped && h->fused_tail && !o.indep && NS <= grid * (uint64_t)threads && P <= (1u << 20) &&
+    const bool fused = grouped && h->fused_tail && !o.indep && !o.seg_row && NS <= grid * (uint64_t)threads && P <= (1u << 20) &&
                        (threads >> sp.g_log) <= 1024;
     Fuse fz{};
     if (fused) {
@@ -619,7 +620,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         CK(launch_compose8(T, lrows, ldom, L0, Lm, P, cpc, rep_rows,
                            rep_doms, o.user_maps, o.user_row0, o.chunk0_end, h->fold_rows.as<uint16_t>(),
                            h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(), h->status.as<DevStatus>(), o.final2,
-                           h->cta_start.as<uint16_t>(), o.starts, s));
+                           h->cta_start.as<uint16_t>(), o.starts, o.seg_row, s));
         prof_end(h, s);
         kernels += o.starts ? 2 : 1;
         h->stats.num_kernels = kernels;
@@ -688,6 +689,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     tr.e0 = o.chunk0_end;
     tr.dev_final = o.final2;
     tr.user_row0 = o.user_row0;
+    tr.seg_row = o.seg_row;
     tr.status = h->status.as<DevStatus>();
     if (T.rs <= 16) {
         const uint64_t warps = tr.lv[1].nodes;
@@ -716,7 +718,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
             const uint16_t *rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
             CK(launch_fold_rows(T, rep_rows, tr.doms + tr.lv[tr.rep_level].off, P, per_cta,
                                 h->fold_rows.as<uint16_t>(), h->fold_doms.as<uint16_t>(), h->ticket.as<uint32_t>(),
-                                h->status.as<DevStatus>(), o.final2, s));
+                                h->status.as<DevStatus>(), o.final2, o.seg_row, s));
             kernels++;
         }
         prof_end(h, s);
@@ -1088,14 +1090,22 @@ dfa_status dfa_match_host(dfa_handle_t h, const uint8_t *host_input, uint64_t le
     return DFA_OK;
 }
 
-dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks, void *stream,
-                          uint64_t *dev_bounds, uint16_t *dev_chunk0_end, uint16_t *dev_maps,
-                          uint16_t *dev_chunk_start, uint16_t *dev_final) {
+}  // extern "C"
+
+namespace {
+// dfa_chunk_maps and dfa_segment_chunk_maps: lookahead < 0 -> the input starts the string
+// (chunk 0 from {q0}, chunk0_out = e0 [1]); lookahead = sigma -> the input is a segment that
+// follows a byte sigma (chunk 0 from I_sigma, chunk0_out = its row [i_max]); seg_row (optional)
+// = the composed map of the whole input over chunk 0's domain.  dev_bounds may be null.
+dfa_status chunk_maps_impl(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t P, int32_t lookahead,
+                           void *stream, uint64_t *dev_bounds, uint16_t *chunk0_out, uint16_t *dev_maps,
+                           uint16_t *dev_chunk_start, uint16_t *dev_final, uint16_t *seg_row) {
     dfa_status st = check_ready(h);
     if (st != DFA_OK) return st;
-    const uint32_t P = num_chunks;
     if (P == 0) return DFA_ERR_CHUNKS;
-    if (!dev_input || !dev_bounds || !dev_chunk0_end || (P > 1 && !dev_maps)) return DFA_ERR_ARG;
+    if (!dev_input || !chunk0_out || (P > 1 && !dev_maps)) return DFA_ERR_ARG;
+    if (lookahead < -1 || lookahead > 255) return DFA_ERR_ARG;
+    if (lookahead >= (int32_t)h->prep.ns) return DFA_ERR_SYMBOL;
     if ((unsigned __int128)len * h->c_den < (unsigned __int128)h->c_num + (unsigned __int128)h->c_den * (P - 1))
         return DFA_ERR_CHUNKS;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1123,25 +1133,51 @@ dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len
     sp.g_log = h->plan_split_c.g_log;
     sp.threads = h->plan_split_c.threads;
     Outputs o;
-    o.chunk0_end = dev_chunk0_end;
+    if (lookahead < 0) o.chunk0_end = chunk0_out;
+    else {
+        o.first_dom = h->prep.byte_class[lookahead];
+        o.user_row0 = chunk0_out;
+    }
     o.user_maps = P > 1 ? dev_maps : nullptr;
     o.starts = dev_chunk_start;
     o.final2 = dev_final;
+    o.seg_row = seg_row;
     auto body = [&](cudaStream_t cs) -> dfa_status {
-        CK(cudaMemcpyAsync(dev_bounds, h->plan_bounds.p, (size_t)(P + 1) * 8, cudaMemcpyDeviceToDevice, cs));
-        return run(h, dev_input, len, P, dev_bounds, sp, cs, o);
+        if (dev_bounds)
+            CK(cudaMemcpyAsync(dev_bounds, h->plan_bounds.p, (size_t)(P + 1) * 8, cudaMemcpyDeviceToDevice, cs));
+        return run(h, dev_input, len, P, h->plan_bounds.as<uint64_t>(), sp, cs, o);
     };
     // repeated identical calls replay a CUDA graph of the whole call (no launch gaps)
     std::vector<uint64_t> gkey = key;
     for (uint64_t v : {(uint64_t)(uintptr_t)dev_input, (uint64_t)(uintptr_t)dev_bounds,
-                       (uint64_t)(uintptr_t)dev_chunk0_end, (uint64_t)(uintptr_t)dev_maps,
-                       (uint64_t)(uintptr_t)dev_chunk_start, (uint64_t)(uintptr_t)dev_final, (uint64_t)h->profile,
+                       (uint64_t)(uintptr_t)chunk0_out, (uint64_t)(uintptr_t)dev_maps,
+                       (uint64_t)(uintptr_t)dev_chunk_start, (uint64_t)(uintptr_t)dev_final,
+                       (uint64_t)(uintptr_t)seg_row, (uint64_t)(int64_t)lookahead, (uint64_t)h->profile,
                        (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
                        (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
                        (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work, (uint64_t)h->fused_tail,
                        (uint64_t)g_scratch_gen.load()})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
+}
+}  // namespace
+
+extern "C" {
+
+dfa_status dfa_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks, void *stream,
+                          uint64_t *dev_bounds, uint16_t *dev_chunk0_end, uint16_t *dev_maps,
+                          uint16_t *dev_chunk_start, uint16_t *dev_final) {
+    if (h && !dev_bounds) return DFA_ERR_ARG;
+    return chunk_maps_impl(h, dev_input, len, num_chunks, -1, stream, dev_bounds, dev_chunk0_end, dev_maps,
+                           dev_chunk_start, dev_final, nullptr);
+}
+
+dfa_status dfa_segment_chunk_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
+                                  int32_t lookahead, void *stream, uint64_t *dev_bounds, uint16_t *dev_chunk0_row,
+                                  uint16_t *dev_maps, uint16_t *dev_segment_row) {
+    if (h && !dev_segment_row) return DFA_ERR_ARG;
+    return chunk_maps_impl(h, dev_input, len, num_chunks, lookahead, stream, dev_bounds, dev_chunk0_row, dev_maps,
+                           nullptr, nullptr, dev_segment_row);
 }
 
 dfa_status dfa_chunk_maps_at(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, uint32_t num_chunks,
@@ -1256,25 +1292,10 @@ dfa_status dfa_lookahead_maps(dfa_handle_t h, const uint8_t *dev_input, uint64_t
 
 dfa_status dfa_segment_map(dfa_handle_t h, const uint8_t *dev_input, uint64_t len, int32_t lookahead, void *stream,
                            uint16_t *dev_row) {
-    dfa_status st = check_ready(h);
-    if (st != DFA_OK) return st;
-    if (!dev_input || !dev_row || len == 0 || lookahead < -1 || lookahead > 255) return DFA_ERR_ARG;
-    if (lookahead >= (int32_t)h->prep.ns) return DFA_ERR_SYMBOL;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (h->staging_pending) { CK(cudaEventSynchronize(h->staging_done)); h->staging_pending = false; }
-    CK(h->h_bounds.ensure(16));
-    CK(h->bounds.ensure(16));
-    uint64_t *hb = h->h_bounds.as<uint64_t>();
-    hb[0] = 0;
-    hb[1] = len;
-    CK(cudaMemcpyAsync(h->bounds.p, hb, 16, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(h->staging_done, s));
-    h->staging_pending = true;
-    const Split sp = plan_split(h, len, 1, hb, false);
-    Outputs o;
-    o.first_dom = lookahead < 0 ? h->T.start_dom : h->prep.byte_class[lookahead];
-    o.user_row0 = dev_row;
-    return run(h, dev_input, len, 1, h->bounds.as<uint64_t>(), sp, s, o);
+    // one chunk: its row is the segment map (device-resident plan, graph replay when repeated)
+    if (!dev_input || !dev_row || len == 0) return h ? DFA_ERR_ARG : DFA_ERR_ARG;
+    return chunk_maps_impl(h, dev_input, len, 1, lookahead, stream, nullptr, dev_row, nullptr, nullptr, nullptr,
+                           dev_row);
 }
 
 dfa_status dfa_fold_segments(dfa_handle_t h, const uint16_t *dev_rows, const uint8_t *dev_lookahead, uint32_t G,

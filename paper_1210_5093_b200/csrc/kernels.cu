@@ -1587,6 +1587,12 @@ __global__ void __launch_bounds__(256) tree_kernel(DevTables T, Tree tr) {
 #endif
             if (L == tr.nlevels) {
                 // root: Alg.seqmatch lines 4-6 on delta-hat(q0, x) (unless fold_rows_kernel follows)
+                if (tr.seg_row && tr.root_final && node == 0) {
+                    // the segment map: the root's row over chunk 0's domain, in the user's order
+                    const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+                    for (uint32_t j = lane; j < T.imax_user; j += 32)
+                        tr.seg_row[j] = j < du ? row[d0 < T.nclass ? T.xlat[(uint64_t)d0 * T.imax_user + j] : j] : kNone;
+                }
                 if (lane == 0 && tr.root_final && node == 0) {
                     const uint32_t fs = row[0];
                     DevStatus *S = tr.status;
@@ -1678,6 +1684,15 @@ __global__ void __launch_bounds__(256) walk_kernel(DevTables T, Tree tr, uint32_
                 }
             }
         }
+        if (tr.seg_row && L == tr.nlevels && node == 0) {
+            // the segment map: the root's row over chunk 0's domain, in the user's order
+            const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+            if (j < T.imax_user && j >= du) tr.seg_row[j] = kNone;
+            if (j < u) {
+                const uint32_t ju = d0 < T.nclass ? T.ixlat[(uint64_t)d0 * T.rs + j] : j;
+                if (ju != kNone) tr.seg_row[ju] = (uint16_t)s;
+            }
+        }
         if (L == tr.nlevels && node == 0 && j == 0) {
             DevStatus *S = tr.status;
             if (s == T.poison) atomicMax(&S->err, 5u);
@@ -1720,7 +1735,7 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
                                                          uint32_t P, uint32_t per_cta, uint32_t lrs,
                                                          uint16_t *cta_rows, uint16_t *cta_doms,
                                                          uint32_t *ticket, DevStatus *status,
-                                                         uint16_t *dev_final) {
+                                                         uint16_t *dev_final, uint16_t *seg_row) {
     extern __shared__ uint4 smem4[];
     const uint32_t q4 = T.rs >> 3;
     // shared: [rank table u8][error bits][dom sizes][child doms][rows]
@@ -1787,6 +1802,13 @@ __global__ void __launch_bounds__(1024) fold_rows_kernel(DevTables T, const uint
     if (threadIdx.x == 0) atomicMax(&g_tree_t[24], gtimer());
 #endif
 
+    if (seg_row) {
+        // the segment map: the folded row over the first chunk's domain, in the user's order
+        const uint32_t d0 = dch[0];
+        const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+        for (uint32_t j = threadIdx.x; j < T.imax_user; j += blockDim.x)
+            seg_row[j] = j < du ? st[d0 < T.nclass ? T.xlat[(uint64_t)d0 * T.imax_user + j] : j] : kNone;
+    }
     if (threadIdx.x == 0) {
         const uint32_t fs = st[0];
         if (fs == T.poison) atomicMax(&status->err, 5u);
@@ -1907,7 +1929,7 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
                                                         uint16_t *rep_rows, uint16_t *rep_doms, uint16_t *user_rows,
                                                         uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
                                                         uint16_t *cta_doms, uint32_t *ticket, DevStatus *status,
-                                                        uint16_t *dev_final, uint16_t *cta_start) {
+                                                        uint16_t *dev_final, uint16_t *cta_start, uint16_t *seg_row) {
 #ifdef DFA_TREE_TIMING
     if (threadIdx.x == 0) atomicMin(&g_tree_t[10], gtimer());
 #endif
@@ -2035,6 +2057,21 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
 #endif
     }
     if (cta_start && gridDim.x == 1 && threadIdx.x == 0) cta_start[0] = (uint16_t)kRank;
+    if (seg_row && warp == 0) {
+        // the segment map: the fold of every chunk map over chunk 0's domain (absolute states:
+        // the input's last sub-chunk ends in states), in the user's order
+        const uint32_t d0 = __shfl_sync(0xffffffffu, acc.dom, 0);
+        uint32_t du, xl;
+        if (d0 < T.nclass) {
+            du = T.dom_user_size[d0];
+            xl = j < T.imax_user ? T.xlat[(uint64_t)d0 * T.imax_user + j] : 0u;
+        } else {
+            du = d0 == T.start_dom ? 1u : 0u;
+            xl = j;
+        }
+        const uint32_t v = __shfl_sync(0xffffffffu, acc.v, xl & 7u);
+        if (lane < 8 && j < T.imax_user) seg_row[j] = (uint16_t)(j < du ? v : kNone);
+    }
     if (threadIdx.x == 0) {
         const uint32_t fs = acc.v;  // absolute: the input's last sub-chunk ends in states
         if (fs == T.poison) atomicMax(&status->err, 5u);
@@ -2497,12 +2534,12 @@ size_t fold_rows_fixed_bytes(const DevTables &T) {
 
 cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uint16_t *doms, uint32_t P,
                              uint32_t per_cta, uint16_t *cta_rows, uint16_t *cta_doms, uint32_t *ticket,
-                             DevStatus *st, uint16_t *dev_final, cudaStream_t s) {
+                             DevStatus *st, uint16_t *dev_final, uint16_t *seg_row, cudaStream_t s) {
     const uint32_t lrs = tree_lrs(T);
     const uint32_t grid = (P + per_cta - 1) / per_cta;
     const size_t smem = fold_rows_fixed_bytes(T) + ((per_cta + 7) & ~7u) * 2 + ((size_t)per_cta << lrs) * 2;
     fold_rows_kernel<<<grid, 256, smem, s>>>(T, rows, doms, P, per_cta, lrs, cta_rows, cta_doms, ticket, st,
-                                              dev_final);
+                                              dev_final, seg_row);
     return cudaGetLastError();
 }
 
@@ -2545,13 +2582,13 @@ cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const ui
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
                             uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final,
-                            uint16_t *cta_start, uint16_t *starts, cudaStream_t s) {
+                            uint16_t *cta_start, uint16_t *starts, uint16_t *seg_row, cudaStream_t s) {
     // 4 chunks per warp per round: about one round per SM-resident CTA, cpc <= 1024
     const uint32_t warps = std::min<uint32_t>(32, std::max<uint32_t>(1, (cpc + 3) / 4));
     const uint32_t grid = (P + cpc - 1) / cpc;
     cudaError_t e = launch_pdl(compose8_kernel, dim3(grid), dim3(warps * 32), 0, s, T, leaves, leaf_dom, L0, L, P, cpc,
                                rep_rows, rep_doms, user_rows, user_row0, e0, cta_rows, cta_doms, ticket, st,
-                               dev_final, starts ? cta_start : nullptr);
+                               dev_final, starts ? cta_start : nullptr, seg_row);
     if (e != cudaSuccess || !starts) return e;
     return launch_pdl(starts8_kernel, dim3(grid), dim3(256), 0, s, T, (const uint16_t *)rep_rows,
                       (const uint16_t *)rep_doms, P, cpc, (const uint16_t *)cta_start, starts);

@@ -134,6 +134,7 @@ struct Tree {
     // outputs
     uint16_t *user_rows, *e0, *dev_final;
     uint16_t *user_row0;     // optional API row of reporting chunk 0 (segment maps)
+    uint16_t *seg_row;       // optional: the root map (the whole input over chunk 0's domain), user order
     DevStatus *status;
 };
 
@@ -169,11 +170,11 @@ cudaError_t launch_compose8(const DevTables &T, const uint16_t *leaves, const ui
                             uint32_t L, uint32_t P, uint32_t cpc, uint16_t *rep_rows, uint16_t *rep_doms,
                             uint16_t *user_rows, uint16_t *user_row0, uint16_t *e0, uint16_t *cta_rows,
                             uint16_t *cta_doms, uint32_t *ticket, DevStatus *st, uint16_t *dev_final,
-                            uint16_t *cta_start, uint16_t *starts, cudaStream_t s);
+                            uint16_t *cta_start, uint16_t *starts, uint16_t *seg_row, cudaStream_t s);
 size_t fold_rows_fixed_bytes(const DevTables &T);
 cudaError_t launch_fold_rows(const DevTables &T, const uint16_t *rows, const uint16_t *doms, uint32_t P,
                              uint32_t per_cta, uint16_t *cta_rows, uint16_t *cta_doms, uint32_t *ticket,
-                             DevStatus *st, uint16_t *dev_final, cudaStream_t s);
+                             DevStatus *st, uint16_t *dev_final, uint16_t *seg_row, cudaStream_t s);
 int tree_slice_bytes(const DevTables &T, uint32_t F);
 uint32_t tree_lrs(const DevTables &T);
 int tree_fixed_bytes(const DevTables &T, int rank_smem);

@@ -38,35 +38,48 @@ def gather_rows(row: torch.Tensor, dist, group=None) -> torch.Tensor:
 
 
 class SegmentMatcher:
-    """Per-rank driver: step() = segment map, one all-gather, fold."""
+    """Per-rank driver: step() = segment map, one all-gather, fold.  With one rank the
+    segment is the whole string (lookahead -1): step() returns its map row, whose entry
+    0 is the final state -- the same per-GPU work as every rank of a larger world."""
 
     def __init__(self, rank: int, world: int, dist, last_byte: torch.Tensor,
                  segment_map: Callable[[int], torch.Tensor],
                  fold: Callable[[torch.Tensor, List[int]], object], group=None):
         self.rank, self.world, self.dist, self.group = rank, world, dist, group
-        self.lookahead = exchange_halo(last_byte, dist, group)
+        self.lookahead = exchange_halo(last_byte, dist, group) if world > 1 else [-1]
         self.segment_map = segment_map
         self.fold = fold
 
     def step(self):
         row = self.segment_map(self.lookahead[self.rank])
+        if self.world == 1:
+            return row
         rows = gather_rows(row, self.dist, self.group)
         return self.fold(rows, self.lookahead)
 
 
-def gpu_ops(d, dev_input: torch.Tensor, stream=None):
+def gpu_ops(d, dev_input: torch.Tensor, stream=None, chunks: int = 1):
     """(segment_map, fold) for a D.Dfa handle on this rank's segment, all in the
-    library's kernels; results stay on the device (fold returns {final, accept})."""
+    library's kernels; results stay on the device (fold returns {final, accept}).
+    segment_map runs dfa_segment_chunk_maps with `chunks` reporting chunks -- the same
+    partition and kernels as dfa_chunk_maps on one GPU; its buffers are attributes
+    (segment_map.bounds / .chunk0 / .maps / .row)."""
     import paper_1210_5093_b200 as D
     dev = dev_input.device
     imax = d.info["i_max"]
+    P = int(chunks)
     row = torch.empty(imax, dtype=torch.int16, device=dev)
+    bounds = torch.empty(P + 1, dtype=torch.int64, device=dev)
+    chunk0 = torch.empty(imax, dtype=torch.int16, device=dev)
+    maps = torch.empty(max(P - 1, 1) * imax, dtype=torch.int16, device=dev)
     final = torch.empty(2, dtype=torch.int16, device=dev)
     la_dev: Optional[torch.Tensor] = None
 
     def segment_map(lookahead: int) -> torch.Tensor:
-        D.dfa_segment_map(d.h, dev_input, lookahead, row, stream=stream)
+        D.dfa_segment_chunk_maps(d.h, dev_input, P, lookahead, bounds, chunk0, maps, row, stream=stream)
         return row
+
+    segment_map.bounds, segment_map.chunk0, segment_map.maps, segment_map.row = bounds, chunk0, maps, row
 
     def fold(rows: torch.Tensor, lookahead: List[int]):
         nonlocal la_dev

@@ -766,7 +766,9 @@ def _nccl_worker(rank, world, port, q):
             d = D.Dfa(w.automaton.table, w.automaton.q0, w.automaton.accept_bitmap)
             smap, fold = multi_gpu.gpu_ops(d, dx)
             m = multi_gpu.SegmentMatcher(rank, world, dist, dx[-1:], smap, fold)
-            out = m.step()
+            row = m.step()  # world 1: the segment row (entry 0 = final state), no collective
+            # the N > 1 exchange over NCCL anyway: all-gather of the rows, then the fold kernel
+            out = fold(multi_gpu.gather_rows(row, dist), [-1])
             torch.cuda.synchronize()
             res.append((name, out.cpu().numpy().view(np.uint16).tolist(), D.dfa_get_last_device_error(d.h)))
             d.close()
@@ -899,3 +901,56 @@ def test_fused_tail_and_compose8(name, fused):
     for P in (1, 2, 3, 64, 777, 4096):
         check_chunk_maps(c, P, opts={D.DFA_OPT_FUSED_TAIL: fused})
     check_match(c, opts={D.DFA_OPT_FUSED_TAIL: fused})
+
+
+@pytest.mark.parametrize("name,G,P", [("random", 3, 64), ("keyword", 2, 129), ("protein", 2, 33), ("worst", 2, 17),
+                                      ("tiny", 4, 16)])
+def test_segment_chunk_maps(name, G, P):
+    """dfa_segment_chunk_maps (the per-GPU step of every N, Fig.Merge): for each
+    of G segments of one input, P chunks with chunk 0 from I_sigma of the byte before the
+    segment (segment 0 from q0): bounds, chunk 0's row (e0 for segment 0), every map row and
+    the segment's composed row against the oracle; the rows fold to the sequential final."""
+    w = W.get(name)
+    n = 3 << 19
+    x = w.input(n)
+    c = Case(w.automaton, x, name)
+    rng = np.random.default_rng(G + P)
+    cuts = np.sort(rng.choice(np.arange(P + 1, n - P - 1), G - 1, replace=False))
+    b = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    d = c.handle()
+    try:
+        imax = d.info["i_max"]
+        dx = torch.from_numpy(x).to(DEV)
+        rows = torch.empty(G, imax, dtype=torch.int16, device=DEV)
+        la = np.zeros(G, np.uint8)
+        for rep in range(2):  # the second pass replays captured graphs
+            for g in range(G):
+                lo, hi = int(b[g]), int(b[g + 1])
+                look = -1 if g == 0 else int(x[lo - 1])
+                la[g] = max(look, 0)
+                bounds = torch.empty(P + 1, dtype=torch.int64, device=DEV)
+                c0 = torch.empty(imax, dtype=torch.int16, device=DEV)
+                maps = torch.empty((P - 1) * imax, dtype=torch.int16, device=DEV)
+                D.dfa_segment_chunk_maps(d.h, dx[lo:hi], P, look, bounds, c0, maps, rows[g])
+                torch.cuda.synchronize()
+                assert D.dfa_get_last_device_error(d.h) == 0
+                ob = oracle.chunk_bounds_ratio(hi - lo, P, 1, 1)
+                assert np.array_equal(bounds.cpu().numpy().astype(np.uint64), ob), (g, "bounds")
+                xs = x[lo:hi]
+                oe0, omaps = c.od.maps(xs, ob, imax)
+                assert np.array_equal(u16(maps).reshape(omaps.shape), omaps), (g, "maps")
+                if g == 0:
+                    assert u16(c0)[0] == oe0, "e0"
+                    assert u16(rows[0])[0] == c.od.run(xs), "segment 0 final"
+                else:
+                    row0, _ = c.od.chunk_map(x, lo, lo + int(ob[1]), imax)
+                    assert np.array_equal(u16(c0), row0), (g, "chunk 0 row")
+                    srow, _ = c.od.chunk_map(x, lo, hi, imax)
+                    assert np.array_equal(u16(rows[g]), srow), (g, "segment row")
+        final = torch.empty(2, dtype=torch.int16, device=DEV)
+        D.dfa_fold_segments(d.h, rows, torch.from_numpy(la).to(DEV), G, final)
+        torch.cuda.synchronize()
+        fin = c.od.run(x)
+        assert u16(final).tolist() == [fin, int(c.a.accepting[fin])]
+    finally:
+        d.close()
