@@ -21,6 +21,30 @@
 #include <utility>
 #include <cstdint>
 
+// DFA_CHECKED (the bounds-checked build, tools/checked_run.sh): every table lookup,
+// data-dependent index and input read is range-checked on the device; a violation
+// prints where and traps.  compute-sanitizer is not available on the B200 pool
+// (DESIGN.md section 5), this is the memory-safety evidence instead.  Compiles to
+// nothing in the production build.
+#ifdef DFA_CHECKED
+#include <cstdio>
+namespace {
+__device__ __noinline__ void dfa_check_fail(const char *what, int line) {
+    printf("DFA_CHECK failed: %s (kernels.cu:%d) block %d thread %d\n", what, line, (int)blockIdx.x,
+           (int)threadIdx.x);
+    __trap();
+}
+}  // namespace
+#define DFA_CHECK(cond, what)                                  \
+    do {                                                       \
+        if (__builtin_expect(!(cond), 0)) dfa_check_fail(what, __LINE__); \
+    } while (0)
+#else
+#define DFA_CHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
+
 namespace dfa {
 
 namespace {
@@ -92,9 +116,11 @@ __device__ __forceinline__ void sub_range_b(const Plan &p, uint64_t i, uint64_t 
         b0 = min(b0, p.n);
         b1 = min(max(b1, b0), p.n);
     }
+    DFA_CHECK(b0 <= b1 && b1 <= p.n, "chunk bounds out of order or past n");
     const uint64_t len = b1 - b0;
     s = split_point(p, b0, len, j, mk);
     e = split_point(p, b0, len, j + 1, mk);
+    DFA_CHECK(b0 <= s && s <= e && e <= b1, "sub-chunk outside its chunk");
 }
 
 __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s, uint64_t &e) {
@@ -119,7 +145,9 @@ __device__ __forceinline__ bool chunk_first_sub(const Plan &p, uint64_t i) {
 
 __device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const Plan &p, const uint8_t *in, uint64_t i,
                                                uint64_t start) {
+    DFA_CHECK(i < p.NS, "sub-chunk index past NS");
     if (i == 0) return p.first_dom;
+    DFA_CHECK(start >= 1 && start <= p.n, "lookahead byte before the input");
     if (p.indep && chunk_first_sub(p, i)) return T.start_dom;  // batch: every input starts at q0
     return (uint32_t)T.byte_class[__ldg(in + start - 1)];
 }
@@ -196,23 +224,37 @@ struct Tab {
         // WindowU16: the table starts at a multiple of the row size and holds
         // s + bias, so s_enc * rowb is the row's shared address (no base add)
         if (MODE == kWindowU16) bias = tb / rowb;
+#ifdef DFA_CHECKED
+        tlim = smem_words<MODE>(T) * 4u;
+        glim = T.nq * 256u;
+#endif
     }
     __device__ __forceinline__ uint32_t enc(uint32_t s) const { return s + bias; }
     __device__ __forceinline__ uint32_t dec(uint32_t s) const { return s - bias; }
-    __device__ __forceinline__ static uint32_t lds_u8(uint32_t addr) {
+#ifdef DFA_CHECKED
+    uint32_t tlim, glim;  // table bytes in shared memory / entries of the global table
+#endif
+    __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) const {
+        DFA_CHECK(addr - tb < tlim, "u8 table lookup outside the shared-memory table");
         uint32_t r;
         asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(addr));
         return r;
     }
-    __device__ __forceinline__ static uint32_t lds_u16(uint32_t addr) {
+    __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) const {
+        DFA_CHECK(addr - tb < tlim && !(addr & 1u), "u16 table lookup outside the shared-memory table");
         uint32_t r;
         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r) : "r"(addr));
         return r;
     }
-    __device__ __forceinline__ static uint32_t lds_u32(uint32_t addr) {
+    __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) const {
+        DFA_CHECK(addr - tb < tlim && !(addr & 3u), "u32 table lookup outside the shared-memory table");
         uint32_t r;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
         return r;
+    }
+    __device__ __forceinline__ uint32_t ldg_tab(uint32_t idx) const {
+        DFA_CHECK(idx < glim, "global table lookup out of range");
+        return __ldg(g + idx);
     }
     // replicated modes: K(b) of a raw byte
     __device__ __forceinline__ uint32_t rep_k(uint32_t b) const {
@@ -252,7 +294,7 @@ struct Tab {
         else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
         else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
         else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
-        else return __ldg(g + (s << 8) + p.a);
+        else return ldg_tab((s << 8) + p.a);
     }
     // per raw byte b, shared by all lanes stepping on it (scalar paths)
     __device__ __forceinline__ Pre bpre(uint32_t b) const {
@@ -274,7 +316,7 @@ struct Tab {
         else if constexpr (MODE == kIdentU16 || MODE == kWindowU16) return lds_u16(s * rowb + p.a);
         else if constexpr (MODE == kWindowU8) return lds_u8(s * rowb + p.a);
         else if constexpr (MODE == kPacked9) return (lds_u32(s * rowb + p.a) >> p.sh) & 511u;
-        else return __ldg(g + (s << 8) + p.a);
+        else return ldg_tab((s << 8) + p.a);
     }
     // scalar step on an encoded state and a raw byte
     __device__ __forceinline__ uint32_t look_byte(uint32_t s, uint32_t b) const {
@@ -288,7 +330,7 @@ struct Tab {
             else return lds_u16(s * rowb + 2u * c);
         } else if constexpr (MODE == kPacked9) {
             return (t32[s * stride + b / 3u] >> ((b % 3u) * 9u)) & 511u;
-        } else return __ldg(g + (s << 8) + b);
+        } else return ldg_tab((s << 8) + b);
     }
 };
 
@@ -378,7 +420,7 @@ __device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t 
                     const uint32_t a = (xd >> (8 * k)) & 0xFFu;
 #pragma unroll
                     for (int l = 0; l < B; l++)
-                        if (act[l]) st[l] = Tab<MODE>::lds_u16(st[l] * tab.rowb + a);
+                        if (act[l]) st[l] = tab.lds_u16(st[l] * tab.rowb + a);
                 }
             }
             return;
@@ -560,6 +602,8 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
         bool restart = false;
         const uint32_t nblk = (uint32_t)((uint64_t)(endp - ptr) >> 5);  // sub-chunks < 128 GiB
         if (nblk) {
+            DFA_CHECK(ptr + 32 * (uint64_t)nblk <= endp && !(reinterpret_cast<uintptr_t>(ptr) & 31u),
+                      "sub-chunk block loads past its end or misaligned");
             U8x32 cur = ldg32(ptr);
             const uint8_t *nptr = ptr + 32;
             for (uint32_t bi = 0; bi < nblk && !restart; bi++, nptr += 32) {
@@ -1050,6 +1094,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
         uint64_t start, end;
         sub_range(p, i, start, end);
         const uint32_t dom = sub_domain(T, p, in, i, start);
+        DFA_CHECK(dom <= T.nclass && start <= end && end <= p.n, "lanes kernel: domain id or sub-chunk range");
         // the next sub-chunk's domain (its sigma = this sub-chunk's last byte), loaded now
         // beside this one's so that the epilogue's rank conversion waits for one load only
         const bool to_rank = g_log != kNoGroup && i + 1 < p.NS && !(p.indep && chunk_first_sub(p, i + 1));
@@ -1059,6 +1104,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
         uint64_t pos;
         if (surv) { u = surv_n[i]; pos = surv_pos[i]; }
         else { u = T.dom_size[dom]; pos = start; }
+        DFA_CHECK(u <= (surv ? (uint32_t)kLanes : T.imax) && pos >= start && pos <= end, "lanes kernel: lane count or start");
         // the grouped (rank-space) epilogue: convert, compose the warp's groups, write leaves
         auto grouped_epilogue = [&](uint32_t (&fin)[kLanes]) {
             const uint64_t wbase = i & ~31ull;
@@ -1357,6 +1403,8 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
                 const uint32_t peers = __match_any_sync(0xffffffffu, key);
                 const uint32_t leader_lane = __ffs(peers) - 1;
                 const uint32_t lid = __shfl_sync(0xffffffffu, id, leader_lane);
+                DFA_CHECK(!live || s < T.nq, "converge: state id past |Q|");
+                DFA_CHECK(!valid || id < T.imax, "converge: lane id past I_max");
                 const uint32_t f = live ? first[s] : kNone;
                 __syncwarp();
                 const bool new_leader = live && f == kNone && lane == leader_lane;
@@ -1490,6 +1538,7 @@ __device__ __forceinline__ void tree_compose_entry(const DevTables &T, const Tre
     if (rank8) { r = rank8[db * T.nq + s]; r = r == 0xFFu ? kNone : r; }
     else r = __ldg(T.rank + (uint64_t)db * T.nq + s);
     if (r == kNone) { atomicMax(&tr.status->err, 8u); r = 0; }
+    DFA_CHECK(r < T.rs && s < T.nq, "tree: rank past the row");
     st[(a << lrs) + j] = st[(b << lrs) + r];
 }
 
@@ -1658,6 +1707,7 @@ __global__ void __launch_bounds__(256) walk_kernel(DevTables T, Tree tr, uint32_
                 if (T.rank8) { r = __ldg(T.rank8 + (uint64_t)d * T.nq + s); r = r == 0xFFu ? kNone : r; }
                 else r = __ldg(T.rank + (uint64_t)d * T.nq + s);
                 if (r == kNone) { atomicMax(&tr.status->err, 8u); s = 0; break; }
+                DFA_CHECK(r < T.rs && d <= T.nclass, "walk: rank past the row");
                 s = reinterpret_cast<const uint16_t *>(tree_child_row(tr, T, L - 1, c))[r];
             }
         }
@@ -1953,6 +2003,7 @@ __global__ void __launch_bounds__(1024) compose8_kernel(DevTables T, const uint1
         const bool has = k < c1;
         const uint32_t a = k == 0 ? 0u : L0 + (k - 1) * L, b = L0 + k * L;
         const uint32_t nk = has ? b - a : 0u;
+        DFA_CHECK(!has || (a <= b && b <= L0 + (uint64_t)(P - 1) * L), "compose8: leaf range past the leaves");
         // the next chunk's domain (its first leaf's) decodes this chunk's rank codes
         const uint32_t nd = has && k + 1 < P ? (uint32_t)__ldcg(leaf_dom + b) : 0u;
         const uint32_t d0 = has ? (uint32_t)__ldcg(leaf_dom + a) : 0u;
@@ -2101,6 +2152,7 @@ __global__ void batch_out_kernel(DevTables T, const uint16_t *rep_rows, uint32_t
         if (offsets && (offsets[j + 1] < offsets[j] || offsets[j + 1] > data_len))
             atomicMax(&status->err, 1u);  // DFA_ERR_ARG: decreasing offsets or past data_len
         const int32_t k = kidx ? kidx[j] : (int32_t)j;
+        DFA_CHECK(k < (int32_t)count, "batch_out: input index past the batch");
         uint32_t q = k < 0 ? T.q0 : rep_rows[(uint64_t)k * rs];
         if (q >= T.nq || is_rank(q)) { atomicMax(&status->err, 8u); q = T.q0; }
         if (q == T.poison) atomicMax(&status->err, 5u);
@@ -2127,6 +2179,7 @@ __global__ void fold_segments_kernel(DevTables T, const uint16_t *rows, const ui
         const uint32_t r = T.rank[(uint64_t)d * T.nq + s];
         const uint32_t ju = r == kNone ? kNone : T.ixlat[(uint64_t)d * T.rs + r];
         if (ju == kNone) { atomicMax(&status->err, 8u); break; }
+        DFA_CHECK(ju < T.imax_user && d < T.nclass, "fold_segments: user index past the row");
         s = rows[(uint64_t)g * T.imax_user + ju];
     }
     uint32_t err = status->err;
