@@ -3,7 +3,7 @@
 // that trade shared-memory capacity for bank-conflict degree.
 // Not part of the library; results go to profiles/.
 //
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/ldsb tools/lds_gather_bench.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/ldsb tools/lds_gather_bench.cu -lcuda
 //   ./ldsb [MiB]
 //
 // Layouts (random DFA over 256 byte columns; each thread runs its own
@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1); } } while (0)
@@ -202,6 +203,95 @@ __global__ void __launch_bounds__(1024, 1) gather_tma(const uint8_t *img, uint32
     out[tid] = s - bias;
 }
 
+// Input staged CTA-cooperatively by 2-D tensor-map copies (cp.async.bulk.tensor.2d,
+// TMA): thread t's sub-chunk is row t of a [rows][per] byte matrix (a uniform stride),
+// one stage = a box of CH bytes x 256 rows per TMA op (4 ops for the CTA's 1024 rows),
+// full/empty mbarriers per stage, S stages; each thread reads its CH bytes back with
+// 16-byte shared loads.  L = 0 (ident_u8) or 1 (rep8_u8).
+template <int L, int CH, int S>
+__global__ void __launch_bounds__(1024, 1) gather_tma2d(const __grid_constant__ CUtensorMap tmap, const uint8_t *img,
+                                                        uint32_t img_bytes, uint32_t align, uint64_t per,
+                                                        uint32_t *out) {
+    extern __shared__ uint4 sm[];
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t base = (sb + align - 1) & ~(align - 1);
+    uint8_t *tab = reinterpret_cast<uint8_t *>(sm) + (base - sb);
+    const int shift = L == 0 ? 8 : 11;
+    const uint32_t bias = base >> shift, bias4 = bias * 0x01010101u;
+    for (uint32_t i = threadIdx.x; i < img_bytes / 16; i += blockDim.x) {
+        uint4 v = reinterpret_cast<const uint4 *>(img)[i];
+        v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4); v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
+        reinterpret_cast<uint4 *>(tab)[i] = v;
+    }
+    const uint32_t T = blockDim.x;
+    uint8_t *ring = tab + ((img_bytes + 1023) & ~1023u);                 // [S][T][CH], 1 KB aligned
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ring + (size_t)S * T * CH);  // full[S], empty[S]
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring), bar_s = (uint32_t)__cvta_generic_to_shared(bars);
+    const uint32_t t = threadIdx.x, lane = t & 31;
+    if (t == 0) {
+#pragma unroll
+        for (int k = 0; k < S; k++) {
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" :: "r"(bar_s + 8 * k));
+            asm volatile("mbarrier.init.shared.b64 [%0], %1;" :: "r"(bar_s + 8 * (S + k)), "r"(T));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t row0 = blockIdx.x * T;
+    auto issue = [&](uint64_t bi, int k) {  // thread 0: stage k <- bytes [bi CH, (bi+1) CH) of all rows
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" :: "r"(bar_s + 8 * k), "r"(T * (uint32_t)CH) : "memory");
+        for (uint32_t q = 0; q < T / 256; q++)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         :: "r"(ring_s + (uint32_t)(k * T * CH) + q * 256 * CH), "l"(&tmap), "r"((int)(bi * CH)),
+                            "r"((int)(row0 + q * 256)), "r"(bar_s + 8 * k) : "memory");
+    };
+    const uint64_t nblk = per / CH;
+    if (t == 0)
+        for (int k = 0; k < S; k++) if ((uint64_t)k < nblk) issue(k, k);
+    uint32_t s = L == 0 ? (base >> 8) : (base >> 11);
+    const uint32_t g4 = L == 1 ? ((lane & 7) << 4) * 0x01010101u : 0u;
+    for (uint64_t bi = 0; bi < nblk; bi++) {
+        const int k = (int)(bi % S);
+        const uint32_t par = (uint32_t)((bi / S) & 1);
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                         : "=r"(done) : "r"(bar_s + 8 * k), "r"(par) : "memory");
+        uint4 q[CH / 16];
+#pragma unroll
+        for (int j = 0; j < CH / 16; j++)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q[j].x), "=r"(q[j].y), "=r"(q[j].z), "=r"(q[j].w)
+                         : "r"(ring_s + (uint32_t)(k * T * CH) + t * CH + 16 * j));
+        asm volatile("mbarrier.arrive.shared.b64 _, [%0];" :: "r"(bar_s + 8 * (S + k)) : "memory");
+        if (t == 0 && bi + S < nblk) {  // the stage is free once every thread has read it
+            uint32_t e = 0;
+            while (!e)
+                asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                             : "=r"(e) : "r"(bar_s + 8 * (S + k)), "r"(par) : "memory");
+            issue(bi + S, k);
+        }
+#pragma unroll
+        for (int j = 0; j < CH / 16; j++) {
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+            for (int wq = 0; wq < 4; wq++) {
+                const uint32_t x = w4[wq];
+                if (L == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) s = lds_u8(__byte_perm(x, s, 0x6540 + kk));
+                } else {
+                    const uint32_t y = (x & 0x0F0F0F0Fu) | ((x & 0x10101010u) << 3) | g4;
+                    const uint32_t z = (x >> 5) & 0x07070707u;
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) s = lds_u8((s << 11) + prmt(y, z, 0xCC00 | ((4 + kk) << 4) | kk));
+                }
+            }
+        }
+    }
+    out[blockIdx.x * T + t] = s - bias;
+}
+
 static uint64_t rng = 88172645463325252ull;
 static uint32_t nxt() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return (uint32_t)rng; }
 
@@ -331,6 +421,65 @@ int main(int argc, char **argv) {
             ms /= 20;
             const double bytes_done = (double)per * grid * threads;
             printf("{\"tma\": 1, \"layout\": %d, \"name\": \"%s_tma\", \"stage_bytes\": %d, \"stages\": %d, \"ms\": %.4f, "
+                   "\"GBps\": %.1f, \"lookups_per_clk_per_sm_at_1965\": %.2f, \"check\": \"%s\"}\n",
+                   L, L == 0 ? "ident_u8" : "rep8_u8", CHv, Sv, ms, bytes_done / ms / 1e6,
+                   bytes_done / (ms * 1e-3) / sms / 1.965e9, bad ? "FAIL" : "ok");
+        }
+        CK(cudaFree(dimg));
+    }
+    // CTA-cooperative 2-D tensor-map staging (uniform sub-chunk stride)
+    for (int L = 0; L < 2; L++) {
+        const int nq = 64;
+        std::vector<uint8_t> delta(nq * 256);
+        for (auto &d : delta) d = nxt() % nq;
+        uint32_t bytes, align;
+        std::vector<uint8_t> img;
+        if (L == 0) { bytes = nq * 256; align = 256; img.assign(bytes, 0);
+            for (int s = 0; s < nq; s++) for (int b = 0; b < 256; b++) img[s * 256 + b] = delta[s * 256 + b]; }
+        else { bytes = nq * 2048; align = 2048; img.assign(bytes, 0);
+            for (int g = 0; g < 8; g++) for (int s = 0; s < nq; s++) for (int b = 0; b < 256; b++)
+                img[(s << 11) | (((b >> 5) & 7) << 8) | (((b >> 4) & 1) << 7) | (g << 4) | (b & 15)] = delta[s * 256 + b]; }
+        uint8_t *dimg; CK(cudaMalloc(&dimg, bytes + 16));
+        CK(cudaMemcpy(dimg, img.data(), bytes, cudaMemcpyHostToDevice));
+        for (int variant = 0; variant < 4; variant++) {
+            const int CHv = (variant & 1) ? 64 : 32, Sv = (variant & 2) ? 4 : 2;
+            void (*f)(const CUtensorMap, const uint8_t *, uint32_t, uint32_t, uint64_t, uint32_t *) =
+                L == 0 ? (variant == 0 ? gather_tma2d<0, 32, 2> : variant == 1 ? gather_tma2d<0, 64, 2>
+                          : variant == 2 ? gather_tma2d<0, 32, 4> : gather_tma2d<0, 64, 4>)
+                       : (variant == 0 ? gather_tma2d<1, 32, 2> : variant == 1 ? gather_tma2d<1, 64, 2>
+                          : variant == 2 ? gather_tma2d<1, 32, 4> : gather_tma2d<1, 64, 4>);
+            const int threads = 1024, grid = sms;
+            const size_t smem = align + ((bytes + 1023) & ~1023u) + (size_t)threads * Sv * CHv + 2 * Sv * 8 + 64;
+            if (smem > 232448) { printf("{\"tma2d\": 1, \"layout\": %d, \"stage_bytes\": %d, \"stages\": %d, \"skip\": \"smem %zu\"}\n", L, CHv, Sv, smem); continue; }
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            const uint64_t per = (n / ((uint64_t)grid * threads)) & ~(uint64_t)(CHv - 1);
+            CUtensorMap tm;
+            const cuuint64_t dims[2] = {(cuuint64_t)per, (cuuint64_t)grid * threads};
+            const cuuint64_t strides[1] = {(cuuint64_t)per};
+            const cuuint32_t box[2] = {(cuuint32_t)CHv, 256}, estr[2] = {1, 1};
+            CUresult cr = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, din, dims, strides, box, estr,
+                                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) { printf("{\"tma2d\": 1, \"error\": \"cuTensorMapEncodeTiled %d\"}\n", (int)cr); continue; }
+            f<<<grid, threads, smem>>>(tm, dimg, bytes, align, per, dout);
+            CK(cudaDeviceSynchronize());
+            std::vector<uint32_t> got(grid * threads);
+            CK(cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost));
+            int bad = 0;
+            for (uint32_t t : {0u, 777u, (uint32_t)(grid * threads - 1)}) {
+                uint32_t hs = 0;
+                for (uint64_t i = 0; i < per; i++) hs = delta[hs * 256 + hin[t * per + i]];
+                bad += got[t] != hs;
+            }
+            cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+            cudaEventRecord(a);
+            for (int r = 0; r < 20; r++) f<<<grid, threads, smem>>>(tm, dimg, bytes, align, per, dout);
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            ms /= 20;
+            const double bytes_done = (double)per * grid * threads;
+            printf("{\"tma2d\": 1, \"layout\": %d, \"name\": \"%s_tma2d\", \"stage_bytes\": %d, \"stages\": %d, \"ms\": %.4f, "
                    "\"GBps\": %.1f, \"lookups_per_clk_per_sm_at_1965\": %.2f, \"check\": \"%s\"}\n",
                    L, L == 0 ? "ident_u8" : "rep8_u8", CHv, Sv, ms, bytes_done / ms / 1e6,
                    bytes_done / (ms * 1e-3) / sms / 1.965e9, bad ? "FAIL" : "ok");
