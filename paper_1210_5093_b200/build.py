@@ -47,8 +47,6 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
     objdir = os.path.join(OBJDIR, tag)
     os.makedirs(objdir, exist_ok=True)
     extra = [f"-D{d}" for d in defines]
-    if "DFA_CHECKED" in defines:
-        extra += ["-Xptxas", "-O1"]  # checked build: the range checks make full ptxas optimisation take hours
 
     def compile_unit(src: str) -> str:
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")

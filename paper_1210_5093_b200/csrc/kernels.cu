@@ -23,21 +23,15 @@
 
 // DFA_CHECKED (the bounds-checked build, tools/checked_run.sh): every table lookup,
 // data-dependent index and input read is range-checked on the device; a violation
-// prints where and traps.  compute-sanitizer is not available on the B200 pool
+// traps.  compute-sanitizer is not available on the B200 pool
 // (DESIGN.md section 5), this is the memory-safety evidence instead.  Compiles to
 // nothing in the production build.
 #ifdef DFA_CHECKED
-#include <cstdio>
-namespace {
-__device__ __noinline__ void dfa_check_fail(const char *what, int line) {
-    printf("DFA_CHECK failed: %s (kernels.cu:%d) block %d thread %d\n", what, line, (int)blockIdx.x,
-           (int)threadIdx.x);
-    __trap();
-}
-}  // namespace
-#define DFA_CHECK(cond, what)                                  \
-    do {                                                       \
-        if (__builtin_expect(!(cond), 0)) dfa_check_fail(what, __LINE__); \
+// a failed check executes the trap instruction (the launch fails with an illegal-instruction
+// error at the next synchronisation); no call, so the checked build compiles like the product
+#define DFA_CHECK(cond, what)                       \
+    do {                                            \
+        if (__builtin_expect(!(cond), 0)) asm volatile("trap;"); \
     } while (0)
 #else
 #define DFA_CHECK(cond, what) \

@@ -48,7 +48,12 @@ DFA_HD constexpr uint32_t rep_log_of(int mode) { return mode == kRepU8x8 ? 3u : 
 // 512..1024 in DESIGN.md section 4).  packed9 (176 KB, Worst) is bounded at 704
 // threads for 88 registers with its sub-chunk count unchanged (6.80 vs 6.99 ms).
 // Every other layout: 1024 (64 registers).
-DFA_HD constexpr int lanes_max_threads(int mode) { return mode == kRepU8x8 ? 640 : mode == kPacked9 ? 704 : 1024; }
+#ifndef DFA_WIN16_MAX_THREADS
+#define DFA_WIN16_MAX_THREADS 1024  // window_u16 (Protein) CTA bound; -D for the register-budget experiment
+#endif
+DFA_HD constexpr int lanes_max_threads(int mode) {
+    return mode == kRepU8x8 ? 640 : mode == kPacked9 ? 704 : mode == kWindowU16 ? DFA_WIN16_MAX_THREADS : 1024;
+}
 
 struct Prep {
     // user view
