@@ -477,11 +477,17 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     h->stats.num_subchunks = NS;
 
     // stage A: lock-step convergence of large initial-state sets
-    const bool stageA = h->convergence && T.imax > (uint32_t)kLanes;
+    // (link codes of converge_kernel need |Q| <= 0x7F00; larger automata run every lane in
+    // lanes_kernel passes)
+    const bool stageA = h->convergence && T.imax > (uint32_t)kLanes && T.nq <= 0x7F00u;
     int wpc = 0;
     if (stageA) {
-        for (int w = 16; w >= 1; w /= 2)
+        // as many warps per SM as the table leaves scratch for (the stage is latency- and
+        // issue-bound: Worst 16 -> 27 warps), spread over the SMs when NS is small
+        for (int w = 32; w >= 1; w--)
             if (converge_smem_bytes(T, w) <= h->optin_smem) { wpc = w; break; }
+        const uint64_t per_sm = (NS + h->sms - 1) / h->sms;
+        if (wpc) wpc = (int)std::min<uint64_t>((uint64_t)wpc, std::max<uint64_t>(4, per_sm));
     }
     const uint32_t sk = stageA && wpc ? (uint32_t)kLanes : std::max<uint32_t>(kLanes, T.rs);
     CK(h->sfin.ensure(NS * sk * 2));

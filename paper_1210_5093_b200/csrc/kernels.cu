@@ -18,6 +18,7 @@
 
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <type_traits>
 #include <utility>
 #include <cstdint>
 
@@ -141,8 +142,8 @@ __device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const Plan &p
                                                uint64_t start) {
     DFA_CHECK(i < p.NS, "sub-chunk index past NS");
     if (i == 0) return p.first_dom;
-    DFA_CHECK(start >= 1 && start <= p.n, "lookahead byte before the input");
     if (p.indep && chunk_first_sub(p, i)) return T.start_dom;  // batch: every input starts at q0
+    DFA_CHECK(start >= 1 && start <= p.n, "lookahead byte before the input");
     return (uint32_t)T.byte_class[__ldg(in + start - 1)];
 }
 
@@ -381,6 +382,13 @@ __device__ __forceinline__ uint8_t *load_tables(const DevTables &T, uint4 *smem,
 
 __device__ __forceinline__ uint32_t bits_words(uint32_t nq) { return ((nq + 31) / 32 + 3) & ~3u; }
 
+// converge_kernel scratch per warp: pool_s, pool_id, link (u16 x I_max rounded to 8)
+// and first (u8 per state when lane ids fit a byte, else u16), 16-byte multiple
+__host__ __device__ __forceinline__ uint32_t converge_scratch_bytes(uint32_t imax, uint32_t nq) {
+    const uint32_t ip = (imax + 7u) & ~7u;
+    return (6u * ip + (imax <= 254u ? nq : 2u * nq) + 15u) & ~15u;
+}
+
 // DFA_OPT_COUNT_WORK: a warp's executed lane-steps into one 64-bit counter
 // (called by every thread of the warp at kernel end).
 __device__ __forceinline__ void add_work(unsigned long long *ctr, uint64_t v) {
@@ -394,8 +402,9 @@ __device__ __forceinline__ void add_work(unsigned long long *ctr, uint64_t v) {
 // ---------------------------------------------------------------------------
 // Lanes l >= nlive of a thread do not load: a warp gather in which only some
 // threads still carry a second lane costs wavefronts for those threads only.
-template <int B, int MODE>
-__device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t (&st)[kLanes], uint32_t nlive) {
+template <int B, int MODE, int N>
+__device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t (&st)[N], uint32_t nlive) {
+    static_assert(B <= N, "block16: more lanes than state registers");
     const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
     bool act[B];
 #pragma unroll
@@ -1256,17 +1265,27 @@ __global__ void __launch_bounds__(1024, 1) ceiling_kernel(DevTables T, const uin
 
 // ---------------------------------------------------------------------------
 // converge_kernel: one warp per sub-chunk, all |I_sigma| lanes in lock-step
-// (the lanes of Alg.MatchingInitialStates line 17 for one chunk), merging
-// lanes that reach equal states every kSubWindow bytes until <= kLanes remain.
-// Output: survivors (states + start position for lanes_kernel) and amap[i][j]
-// = final state of lane j, or kSurvBase + survivor index.
+// (the lanes of Alg.MatchingInitialStates line 17 for one chunk) over 16-byte
+// windows until <= cap (<= kLanes) distinct live states remain.
+//   Wide phase (more than 32 lanes): every thread steps ceil(lanes/32) lanes
+//   held in registers; after a window, lanes in equal states are merged from the
+//   registers (a lane claims first[state], the claim that survives the warp
+//   barrier leads, the others link to it), lanes in absorbing states retire
+//   (P:450-454), the leaders are compacted into the pool.
+//   Narrow phase (<= 32 lanes): one lane per thread, state and lane id in
+//   registers, no compaction (a warp step costs the same for 9 or 32 lanes);
+//   after each window the distinct live states are counted (match.any) and the
+//   stage ends at <= cap.
+// Output: survivors (states + position for lanes_kernel) and amap[i][j] = final
+// state of initial lane j, or kSurvBase + survivor index.
+// Scratch per warp: pool_s, pool_id, link (u16 x I_max each) and first (one
+// entry per state: u8 when I_max <= 254, else u16).  link[id] = final state,
+// survivor code, or kParent + leader id (needs |Q| <= kParent: converge_ok).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t scratch_u16(const DevTables &T) {
-    return (4 * T.imax + T.nq + 7) & ~7u;
-}
+constexpr uint32_t kParent = 0x8000u;
 
-template <int MODE>
-__global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) ? 1 : 2) converge_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
+template <int MODE, bool ID8>
+__global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                        uint16_t *__restrict__ surv, uint8_t *__restrict__ surv_n,
                                                        uint64_t *__restrict__ surv_pos,
                                                        uint16_t *__restrict__ amap, uint32_t cap) {
@@ -1276,12 +1295,17 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
     Tab<MODE> tab;
     tab.init(T, tsm);
     const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
+    const bool has_absorb = T.has_absorb != 0;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint16_t *scr = reinterpret_cast<uint16_t *>(reinterpret_cast<uint32_t *>(tsm) + smem_words<MODE>(T) + bw) +
-                    (size_t)warp * scratch_u16(T);
-    uint16_t *pool_s = scr, *pool_id = scr + T.imax, *parent = scr + 2 * T.imax, *res = scr + 3 * T.imax;
-    uint16_t *first = scr + 4 * T.imax;
-    for (uint32_t q = lane; q < T.nq; q += 32) first[q] = kNone;
+    const uint32_t ltmask = (1u << lane) - 1u;
+    const uint32_t ip = (T.imax + 7u) & ~7u;
+    using FirstT = typename std::conditional<ID8, uint8_t, uint16_t>::type;  // lane ids fit a byte (I_max <= 254)
+    constexpr uint32_t kFirstNone = ID8 ? 0xFFu : 0xFFFFu;
+    uint8_t *scr = reinterpret_cast<uint8_t *>(const_cast<uint32_t *>(absorb) + bw) +
+                   (size_t)warp * converge_scratch_bytes(T.imax, T.nq);
+    uint16_t *pool_s = reinterpret_cast<uint16_t *>(scr), *pool_id = pool_s + ip, *link = pool_id + ip;
+    FirstT *first = reinterpret_cast<FirstT *>(link + ip);
+    for (uint32_t q = lane; q < T.nq; q += 32) first[q] = (FirstT)kFirstNone;
     __syncthreads();
 
     const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -1310,24 +1334,19 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
         const uint4 pre = pb + 16 <= p.n ? ldg16(reinterpret_cast<const uint4 *>(in + pb)) : make_uint4(0, 0, 0, 0);
         const uint32_t dom = sub_domain(T, p, in, i, start);
         const uint32_t u = T.dom_size[dom];
-        for (uint32_t e = lane; e < u; e += 32) {
-            pool_s[e] = T.dom_list[(uint64_t)dom * T.rs + e];
-            pool_id[e] = (uint16_t)e;
-            parent[e] = (uint16_t)e;
-            res[e] = kNone;
-        }
+        const uint16_t *dl = T.dom_list + (uint64_t)dom * T.rs;
+        DFA_CHECK(dom <= T.nclass && u <= T.imax && start <= end && end <= p.n, "converge: domain or sub-chunk range");
         uint32_t np = u;
         uint64_t pos = start;
-        __syncwarp();
-        uint32_t wlen = 16;  // merge every 16 bytes (merging is dearer than stepping: measured)
-        while (np > cap && pos < end) {
-            // window [pos, min(pos + wlen, next 16-byte boundary of the *address*, end))
-            const uint64_t abase = pos - ((reinterpret_cast<uintptr_t>(in) + pos) & 15u);
-            const uint32_t k0 = (uint32_t)(pos - abase);
-            uint32_t k1 = (uint32_t)(end - abase < 16 ? end - abase : 16);
-            k1 = min(k1, k0 + wlen);
-            wlen = min(wlen * 2, 16u);
-            uint4 v;
+        bool fresh = true;  // the pool is still the domain list itself: entry e = (dl[e], id e)
+        // window [pos, min(next 16-byte boundary of the address, end)): bytes k0..k1-1 of v
+        uint4 v;
+        uint32_t k0, k1;
+        uint64_t abase;
+        auto fetch_window = [&]() {
+            abase = pos - ((reinterpret_cast<uintptr_t>(in) + pos) & 15u);
+            k0 = (uint32_t)(pos - abase);
+            k1 = (uint32_t)(end - abase < 16 ? end - abase : 16);
             const uint64_t wi = (abase - ab0) >> 4;  // (uniform over the warp)
             if (abase + 16 <= p.n && wi < 32) {
                 v.x = __shfl_sync(0xffffffffu, pre.x, (uint32_t)wi);
@@ -1341,27 +1360,36 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
                 for (uint32_t k = k0; k < k1; k++) wv[k >> 2] |= (uint32_t)__ldg(in + abase + k) << (8 * (k & 3));
                 v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
             }
+        };
+        // ---- wide phase
+        while (np > 32 && np > cap && pos < end) {
+            fetch_window();
+            uint32_t np_new = 0;
             for (uint32_t base = 0; base < np; base += 32 * kConvergeLA) {
-                uint32_t s[kConvergeLA];
+                uint32_t s[kConvergeLA], id[kConvergeLA];
 #pragma unroll
                 for (int l = 0; l < kConvergeLA; l++) {
                     const uint32_t e = base + lane + 32 * l;
-                    s[l] = tab.enc(e < np ? pool_s[e] : 0);
+                    uint32_t q = 0;
+                    id[l] = e;
+                    if (e < np) {
+                        q = fresh ? (uint32_t)__ldg(dl + e) : (uint32_t)pool_s[e];
+                        if (!fresh) id[l] = pool_id[e];
+                    }
+                    DFA_CHECK(q < T.nq && (e >= np || id[l] < T.imax), "converge: pool entry");
+                    s[l] = tab.enc(q);
                 }
+                const uint32_t rows = min((uint32_t)kConvergeLA, (np - base + 31u) / 32u);  // (uniform)
                 if (k0 == 0 && k1 == 16) {
                     // a full aligned window: the match kernel's 16-byte step (static byte
                     // selection, per-word column preparation) on B = ceil(lanes left / 32)
-                    // lanes per thread -- the pool shrinks fast (Worst: 240 lanes, ~30
-                    // after the first window), so later windows step 1-2 lanes, not 8
+                    // lanes per thread
                     const uint32_t nact = np > base + lane ? min((uint32_t)kConvergeLA, (np - base - lane + 31u) / 32u) : 0u;
-                    switch (min((uint32_t)kConvergeLA, (np - base + 31u) / 32u)) {
+                    // (three step variants only: the stage is instruction-fetch bound with
+                    // eight, Worst: stall no_instruction 4.2 per issue)
+                    switch (rows) {
                     case 1: block16<1, MODE>(tab, v, s, nact); break;
                     case 2: block16<2, MODE>(tab, v, s, nact); break;
-                    case 3: block16<3, MODE>(tab, v, s, nact); break;
-                    case 4: block16<4, MODE>(tab, v, s, nact); break;
-                    case 5: block16<5, MODE>(tab, v, s, nact); break;
-                    case 6: block16<6, MODE>(tab, v, s, nact); break;
-                    case 7: block16<7, MODE>(tab, v, s, nact); break;
                     default: block16<kConvergeLA, MODE>(tab, v, s, nact); break;
                     }
                 } else {
@@ -1369,70 +1397,118 @@ __global__ void __launch_bounds__(512, (MODE == kPacked9 || MODE == kGlobalU16) 
                         const uint32_t wsel = k >> 2;
                         const uint32_t word = wsel == 0 ? v.x : wsel == 1 ? v.y : wsel == 2 ? v.z : v.w;
                         const uint32_t b = (word >> (8 * (k & 3))) & 0xFFu;
-                        const typename Tab<MODE>::Pre pb = tab.bpre(b);
+                        const typename Tab<MODE>::Pre pbk = tab.bpre(b);
 #pragma unroll
-                        for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_pre(s[l], pb);
+                        for (int l = 0; l < kConvergeLA; l++) s[l] = tab.look_pre(s[l], pbk);
                     }
                 }
+                // merge from the registers.  A: absorbed lanes retire; a live lane whose
+                // state has no leader yet claims it (any claim may win: all claimants are
+                // in that state; a leader of an earlier batch stays)
+                uint32_t live = 0;
 #pragma unroll
                 for (int l = 0; l < kConvergeLA; l++) {
                     const uint32_t e = base + lane + 32 * l;
-                    if (e < np) pool_s[e] = (uint16_t)tab.dec(s[l]);
+                    s[l] = tab.dec(s[l]);
+                    if (e >= np) continue;
+                    DFA_CHECK(s[l] < T.nq, "converge: state id past |Q|");
+                    if (has_absorb && test_bit(absorb, s[l])) { link[id[l]] = (uint16_t)s[l]; continue; }
+                    live |= 1u << l;
+                    if (first[s[l]] == kFirstNone) first[s[l]] = (FirstT)id[l];
                 }
+                __syncwarp();
+                // B: the surviving claim leads; the others link to it; leaders are compacted
+#pragma unroll
+                for (int l = 0; l < kConvergeLA; l++) {
+                    if ((uint32_t)l >= rows) break;
+                    bool lead = false;
+                    if (live & (1u << l)) {
+                        const uint32_t w = first[s[l]];
+                        lead = w == id[l];
+                        if (!lead) link[id[l]] = (uint16_t)(kParent + w);
+                    }
+                    const uint32_t mask = __ballot_sync(0xffffffffu, lead);
+                    if (lead) {
+                        const uint32_t off = np_new + __popc(mask & ltmask);
+                        pool_s[off] = (uint16_t)s[l];
+                        pool_id[off] = (uint16_t)id[l];
+                    }
+                    np_new += __popc(mask);
+                }
+                __syncwarp();
             }
-            pos = abase + k1;
             if (lane == 0) work += (uint64_t)(k1 - k0) * np;
-            __syncwarp();
-            // merge lanes with equal states (leader = first in pool order),
-            // retire lanes in absorbing states, compact the pool in place.
-            uint32_t np_new = 0;
-            for (uint32_t row = 0; row * 32 < np; row++) {
-                const uint32_t e = row * 32 + lane;
-                const bool valid = e < np;
-                const uint32_t s = valid ? pool_s[e] : 0;
-                const uint32_t id = valid ? pool_id[e] : 0;
-                const bool absorbed = valid && test_bit(absorb, s);
-                const bool live = valid && !absorbed;
-                const uint32_t key = live ? s : (0x10000u | lane);
-                const uint32_t peers = __match_any_sync(0xffffffffu, key);
-                const uint32_t leader_lane = __ffs(peers) - 1;
-                const uint32_t lid = __shfl_sync(0xffffffffu, id, leader_lane);
-                DFA_CHECK(!live || s < T.nq, "converge: state id past |Q|");
-                DFA_CHECK(!valid || id < T.imax, "converge: lane id past I_max");
-                const uint32_t f = live ? first[s] : kNone;
-                __syncwarp();
-                const bool new_leader = live && f == kNone && lane == leader_lane;
-                if (new_leader) first[s] = (uint16_t)id;
-                if (live && !new_leader) parent[id] = (uint16_t)(f != kNone ? f : lid);
-                if (absorbed) res[id] = (uint16_t)s;
-                const uint32_t mask = __ballot_sync(0xffffffffu, new_leader);
-                if (new_leader) {
-                    const uint32_t off = np_new + __popc(mask & ((1u << lane) - 1u));
-                    pool_s[off] = (uint16_t)s;
-                    pool_id[off] = (uint16_t)id;
-                }
-                np_new += __popc(mask);
-                __syncwarp();
-            }
-            for (uint32_t e = lane; e < np_new; e += 32) first[pool_s[e]] = kNone;
+            for (uint32_t e = lane; e < np_new; e += 32) first[pool_s[e]] = (FirstT)kFirstNone;
             np = np_new;
+            fresh = false;
+            pos = abase + k1;
             __syncwarp();
         }
-        if (pos < end) {
-            for (uint32_t e = lane; e < np; e += 32) {
-                res[pool_id[e]] = (uint16_t)(kSurvBase + e);
-                surv[i * kLanes + e] = pool_s[e];
+        if (np <= 32) {
+            // ---- narrow phase
+            const bool act = lane < np;
+            uint32_t st1[kLanes];
+            uint32_t id = lane;
+            {
+                uint32_t q = 0;
+                if (act) {
+                    q = fresh ? (uint32_t)__ldg(dl + lane) : (uint32_t)pool_s[lane];
+                    if (!fresh) id = pool_id[lane];
+                }
+                st1[0] = tab.enc(q);
             }
-            if (lane == 0) { surv_n[i] = (uint8_t)np; surv_pos[i] = pos; }
+            uint32_t sd, peers, leadmask, nd;
+            bool absorbed, lead;
+            for (;;) {
+                sd = tab.dec(st1[0]);
+                DFA_CHECK(sd < T.nq, "converge: state id past |Q|");
+                absorbed = act && has_absorb && test_bit(absorb, sd);
+                const uint32_t key = act && !absorbed ? sd : (0x10000u | lane);
+                peers = __match_any_sync(0xffffffffu, key);
+                lead = act && !absorbed && (uint32_t)(__ffs(peers) - 1) == lane;
+                leadmask = __ballot_sync(0xffffffffu, lead);
+                nd = __popc(leadmask);
+                if (nd <= cap || pos >= end) break;
+                fetch_window();
+                if (act) {
+                    if (k0 == 0 && k1 == 16) block16<1, MODE>(tab, v, st1, 1u);
+                    else
+                        for (uint32_t k = k0; k < k1; k++) {
+                            const uint32_t wsel = k >> 2;
+                            const uint32_t word = wsel == 0 ? v.x : wsel == 1 ? v.y : wsel == 2 ? v.z : v.w;
+                            st1[0] = tab.look_pre(st1[0], tab.bpre((word >> (8 * (k & 3))) & 0xFFu));
+                        }
+                }
+                if (lane == 0) work += (uint64_t)(k1 - k0) * np;
+                pos = abase + k1;
+            }
+            // equal states share their leader's survivor slot; at the sub-chunk's end the
+            // lanes keep their states
+            const uint32_t slot = __popc(leadmask & ltmask);
+            const uint32_t lslot = __shfl_sync(0xffffffffu, slot, (uint32_t)(__ffs(peers) - 1));
+            const bool more = pos < end;
+            if (act) {
+                DFA_CHECK(id < T.imax && (!more || absorbed || lslot < (uint32_t)kLanes), "converge: lane id or survivor slot");
+                link[id] = (uint16_t)(absorbed || !more ? sd : kSurvBase + lslot);
+                if (lead && more) surv[i * kLanes + slot] = (uint16_t)sd;
+            }
+            if (lane == 0) { surv_n[i] = (uint8_t)(more ? nd : 0u); surv_pos[i] = more ? pos : end; }
         } else {
-            for (uint32_t e = lane; e < np; e += 32) res[pool_id[e]] = pool_s[e];
+            // the sub-chunk ended with more than 32 lanes: its map is the lanes' states
+            for (uint32_t e = lane; e < np; e += 32) {
+                if (fresh) link[e] = __ldg(dl + e);
+                else link[pool_id[e]] = pool_s[e];
+            }
             if (lane == 0) { surv_n[i] = 0; surv_pos[i] = end; }
         }
         __syncwarp();
         for (uint32_t j = lane; j < u; j += 32) {
-            uint32_t r = j;
-            while (parent[r] != r) r = parent[r];
-            amap[i * T.rs + j] = res[r];
+            uint32_t r = link[j];
+            while (r - kParent < (uint32_t)kSurvBase - kParent) {
+                DFA_CHECK(r - kParent < T.imax, "converge: parent link");
+                r = link[r - kParent];
+            }
+            amap[i * T.rs + j] = (uint16_t)r;
         }
         __syncwarp();
     }
@@ -2307,10 +2383,10 @@ __global__ void __launch_bounds__(512) starts_kernel(DevTables T, Plan p, const 
 // parallel, and the main unit dispatches through these.
 #ifdef DFA_TU_MODE
 template <int M>
-void *converge_or_null() {
+void *converge_or_null(bool id8) {
     // the converge kernel runs the byte-table modes on the padded copy (converge_fn)
     if constexpr (M == kIdentU8 || M == kRepU8x8 || M == kRepU8x4) return nullptr;
-    else return (void *)converge_kernel<M>;
+    else return id8 ? (void *)converge_kernel<M, true> : (void *)converge_kernel<M, false>;
 }
 #define DFA_DEFINE_MODE_ENTRIES(M)                                                                      \
     template <> void *lanes_entry<M>(bool sticky, bool count) {                                         \
@@ -2318,7 +2394,7 @@ void *converge_or_null() {
                      : (sticky ? (void *)lanes_kernel<M, true, false> : (void *)lanes_kernel<M, false, false>); \
     }                                                                                                   \
     template <> void *ceiling_entry<M>() { return (void *)ceiling_kernel<M>; }                          \
-    template <> void *converge_entry<M>() { return converge_or_null<M>(); }
+    template <> void *converge_entry<M>(bool id8) { return converge_or_null<M>(id8); }
 #if DFA_TU_MODE == 0
 DFA_DEFINE_MODE_ENTRIES(kIdentU8)
 DFA_DEFINE_MODE_ENTRIES(kIdentU16)
@@ -2368,17 +2444,18 @@ void *lanes_fn(const DevTables &T, bool count = false) {
 // The converge kernel steps all lanes of one sub-chunk on the same byte (a
 // warp per sub-chunk): with 256-byte rows they would all read one bank, so
 // every byte-table mode converges on the padded single copy of the same image.
-void *converge_fn(int mode) {
-    switch (mode) {
+void *converge_fn(const DevTables &T) {
+    const bool id8 = T.imax <= 254u;  // lane ids fit a byte (converge_scratch_bytes)
+    switch (T.mode) {
     case kIdentU8:
     case kIdentU8P:
     case kRepU8x8:
-    case kRepU8x4: return converge_entry<kIdentU8P>();
-    case kIdentU16: return converge_entry<kIdentU16>();
-    case kWindowU8: return converge_entry<kWindowU8>();
-    case kWindowU16: return converge_entry<kWindowU16>();
-    case kPacked9: return converge_entry<kPacked9>();
-    default: return converge_entry<kGlobalU16>();
+    case kRepU8x4: return converge_entry<kIdentU8P>(id8);
+    case kIdentU16: return converge_entry<kIdentU16>(id8);
+    case kWindowU8: return converge_entry<kWindowU8>(id8);
+    case kWindowU16: return converge_entry<kWindowU16>(id8);
+    case kPacked9: return converge_entry<kPacked9>(id8);
+    default: return converge_entry<kGlobalU16>(id8);
     }
 }
 
@@ -2413,9 +2490,8 @@ int lanes_smem_bytes(const DevTables &T) {
 }
 
 int converge_smem_bytes(const DevTables &T, int warps_per_cta) {
-    const uint32_t scr = (4 * T.imax + T.nq + 7) & ~7u;
     return table_smem_bytes(T, is_u8_mode(T.mode) ? kIdentU8P : T.mode) + bits_words_host(T.nq) * 4 +
-           warps_per_cta * (int)scr * 2;
+           warps_per_cta * (int)converge_scratch_bytes(T.imax, T.nq);
 }
 
 uint32_t tree_lrs(const DevTables &T) {
@@ -2446,7 +2522,7 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
         if (e != cudaSuccess) return e;
     }
     cudaError_t e;
-    e = cudaFuncSetAttribute(converge_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    e = cudaFuncSetAttribute(converge_fn(T), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(ceiling_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
@@ -2468,7 +2544,7 @@ int lanes_occupancy(const DevTables &T, int threads) {
 
 int converge_occupancy(const DevTables &T, int warps_per_cta) {
     int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, converge_fn(T.mode), warps_per_cta * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, converge_fn(T), warps_per_cta * 32,
                                                   converge_smem_bytes(T, warps_per_cta));
     return blocks;
 }
@@ -2478,7 +2554,7 @@ cudaError_t launch_converge(const DevTables &T, const Plan &p, const uint8_t *in
                             cudaStream_t s) {
     void *args[] = {(void *)&T, (void *)&p, (void *)&in, (void *)&surv, (void *)&surv_n, (void *)&surv_pos,
                     (void *)&amap, (void *)&cap};
-    return cudaLaunchKernel(converge_fn(T.mode), dim3(grid), dim3(warps_per_cta * 32), args,
+    return cudaLaunchKernel(converge_fn(T), dim3(grid), dim3(warps_per_cta * 32), args,
                             converge_smem_bytes(T, warps_per_cta), s);
 }
 

@@ -20,7 +20,7 @@
 namespace dfa {
 
 constexpr int kLanes = 8;          // register lanes per thread in lanes_kernel
-constexpr int kConvergeLA = 8;     // lanes per thread per pass in converge_kernel
+constexpr int kConvergeLA = 4;     // lanes per thread per batch in converge_kernel's wide phase
 constexpr uint32_t kSubWindow = 16;
 constexpr uint32_t kNoWarpGroup = 0xFFFFFFFFu;  // lanes_kernel g_log: per-sub-chunk maps
 
@@ -193,11 +193,11 @@ int probe_dynamic_smem_base(uint32_t *dev_scratch);
 // each (kernels_m<MODE>.cu); nullptr where a layout has no such kernel.
 template <int MODE> void *lanes_entry(bool sticky, bool count);
 template <int MODE> void *ceiling_entry();
-template <int MODE> void *converge_entry();
+template <int MODE> void *converge_entry(bool id8);
 #define DFA_DECLARE_MODE_ENTRIES(M)                  \
     template <> void *lanes_entry<M>(bool sticky, bool count); \
     template <> void *ceiling_entry<M>();            \
-    template <> void *converge_entry<M>();
+    template <> void *converge_entry<M>(bool id8);
 DFA_DECLARE_MODE_ENTRIES(1) DFA_DECLARE_MODE_ENTRIES(2) DFA_DECLARE_MODE_ENTRIES(3)
 DFA_DECLARE_MODE_ENTRIES(4) DFA_DECLARE_MODE_ENTRIES(5) DFA_DECLARE_MODE_ENTRIES(6)
 DFA_DECLARE_MODE_ENTRIES(7) DFA_DECLARE_MODE_ENTRIES(8) DFA_DECLARE_MODE_ENTRIES(9)
