@@ -314,8 +314,12 @@ enum {
     DFA_OPT_STICKY_PARKING = 12, /* 1 (default): park lanes in sticky states; 0 = off */
     DFA_OPT_COUNT_WORK = 13,     /* 1: the match kernels count the lane-steps (table lookups) they execute,
                                     summed into dfa_stats.work_* until dfa_get_stats reads them; 0 (default) */
-    DFA_OPT_FUSED_TAIL = 14      /* 1: maps of <= 8 entries are composed by the match kernel's CTAs themselves
+    DFA_OPT_FUSED_TAIL = 14,     /* 1: maps of <= 8 entries are composed by the match kernel's CTAs themselves
                                     (one launch); 0 (default, measured faster): leaf_fold_kernel + compose8_kernel */
+    DFA_OPT_FACTORED = 15        /* 1 (default): maps of more than 16 entries behind the converge stage are
+                                    composed in factored form (the first sub-chunk's converge map, then <= 8
+                                    survivor values per node; Eq.MapReduction on the image of the first map);
+                                    0: every node composes full rows (walk_kernel) */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 

@@ -74,7 +74,9 @@ struct dfa_handle {
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
     DevBuf cta_start, leaf_rows2, leaf_dom2;
+    DevBuf node_nv, node_fl, rep_full;  // factored composition (long rows behind the converge stage)
     int warp_compose = 1;
+    int factored = 1;             // DFA_OPT_FACTORED
     int fused_tail = 0;           // DFA_OPT_FUSED_TAIL (measured slower than compose8: DESIGN.md)
     DevBuf part_rows, part_doms, chunk_cnt;
     std::vector<uint64_t> plan_key;
@@ -471,7 +473,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     }
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
               o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in, o.indep ? 1u : 0u,
-              work};
+              work, 0u, plan_magic(m0), plan_magic(m)};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;
@@ -514,6 +516,10 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         surv_pos = h->surv_pos.as<uint64_t>();
     }
     const bool grouped = sp.g_log != kNoWarpGroup;
+    // long rows behind the converge stage compose in factored form (fwalk_kernel): the
+    // converge maps stay coded
+    const bool factored = amap && !grouped && T.rs > 16 && h->factored;
+    plan.keep_amap = factored ? 1u : 0u;
     const int threads = sp.threads;
     const int occ = std::max(1, lanes_occupancy(T, threads));
     const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
@@ -674,6 +680,11 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         tr.lrs = tree_lrs(T);
         CK(h->lvlA.ensure(total * T.rs * 2));
         CK(h->domA.ensure(total * 2));
+        if (factored) {
+            CK(h->node_nv.ensure(total * 2));
+            CK(h->node_fl.ensure(total * 4));
+            CK(h->rep_full.ensure((uint64_t)P * T.rs * 2));
+        }
         // arrival counters: valid across calls with the same tree (multiples of
         // the child counts), zeroed when the tree changes
         std::vector<uint64_t> sig = {total, F, L, (uint64_t)m0, (uint64_t)m, (uint64_t)P, (uint64_t)gl};
@@ -697,6 +708,12 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     tr.user_row0 = o.user_row0;
     tr.seg_row = o.seg_row;
     tr.status = h->status.as<DevStatus>();
+    if (factored) {
+        tr.leaf_nv = surv_n;
+        tr.node_nv = h->node_nv.as<uint16_t>();
+        tr.node_fl = h->node_fl.as<uint32_t>();
+        tr.rep_full = h->rep_full.as<uint16_t>();
+    }
     if (T.rs <= 16) {
         const uint64_t warps = tr.lv[1].nodes;
         int occ = 0;
@@ -732,15 +749,24 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         // long rows: one entry-parallel launch per level (small fan-in, see tree_fanin)
         prof_begin(h, s, 2);
         for (uint32_t L = 1; L <= tr.nlevels; L++) {
-            CK(launch_walk(T, tr, L, h->sms, s));
+            if (!factored) {
+                CK(launch_walk(T, tr, L, h->sms, s));
+                kernels++;
+                continue;
+            }
+            CK(launch_fwalk(T, tr, L, h->sms, s));
             kernels++;
+            if (L == tr.rep_level || (L == tr.nlevels && tr.root_final)) {
+                CK(launch_fexpand(T, tr, L, h->sms, s));
+                kernels++;
+            }
         }
         prof_end(h, s);
     }
-    h->rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
+    h->rep_rows = factored ? tr.rep_full : tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
     h->rep_rs = T.rs;
     if (o.starts) {
-        const uint16_t *rep_rows = tr.rows + (uint64_t)tr.lv[tr.rep_level].off * T.rs;
+        const uint16_t *rep_rows = h->rep_rows;
         CK(launch_starts(T, plan, rep_rows, rep_rows + T.rs, tr.doms + tr.lv[tr.rep_level].off, o.starts,
                          h->status.as<DevStatus>(), s));
         kernels++;
@@ -898,7 +924,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
         for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
         for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx,
-                          &h->work})
+                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full})
             b->release();
         h->h_hm.release();
         h->h_batch.release();
@@ -1162,6 +1188,7 @@ dfa_status chunk_maps_impl(dfa_handle_t h, const uint8_t *dev_input, uint64_t le
                        (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
                        (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
                        (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work, (uint64_t)h->fused_tail,
+                       (uint64_t)h->factored,
                        (uint64_t)g_scratch_gen.load()})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
@@ -1381,6 +1408,9 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
         return DFA_OK;
     case DFA_OPT_FUSED_TAIL:
         h->fused_tail = value ? 1 : 0;
+        return DFA_OK;
+    case DFA_OPT_FACTORED:
+        h->factored = value ? 1 : 0;
         return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         h->threads_auto = value == 0;

@@ -91,51 +91,88 @@ __device__ __forceinline__ uint4 ldg16(const uint4 *p) {
 // Internal split points (j > 0) are moved down to a 32-byte aligned address
 // when the parts are long enough, so that a sub-chunk is whole 32-byte sectors
 // except at reporting-chunk bounds; the split is internal, results unchanged.
-__device__ __forceinline__ uint64_t split_point(const Plan &p, uint64_t b0, uint64_t len, uint64_t j, uint64_t mk) {
-    const uint64_t t = b0 + len * j / mk;
-    if (j == 0 || j == mk || len < 64 * mk) return t;
-    return t - ((p.in_addr + t) & 31u);
+// n / d for 32-bit n with the plan's magic = min(floor(2^32 / d), 2^32 - 1): the estimate
+// umulhi(n, magic) is floor(n / d) or one less, one correction makes it exact.
+__device__ __forceinline__ uint32_t udiv_magic(uint32_t n, uint32_t d, uint32_t magic) {
+    const uint32_t q = __umulhi(n, magic);
+    return n - q * d >= d ? q + 1u : q;
+}
+
+// sub-chunk i -> its reporting chunk k, its index j in the chunk and the chunk's split mk
+__device__ __forceinline__ void sub_locate(const Plan &p, uint64_t i, uint64_t &k, uint64_t &j, uint64_t &mk) {
+    if (i < p.m0) { k = 0; j = i; mk = p.m0; return; }
+    mk = p.m;
+    const uint64_t t = i - p.m0;
+    if ((t >> 32) == 0) {
+        const uint32_t q = udiv_magic((uint32_t)t, p.m, p.magic_m);
+        k = 1ull + q;
+        j = (uint32_t)t - q * p.m;
+    } else {
+        k = 1 + t / p.m;
+        j = t % p.m;
+    }
+}
+
+// [b0 + floor(len j / mk), b0 + floor(len (j+1) / mk)) with internal split points moved down
+// to a 32-byte aligned address.  Exact: len = q mk + r gives floor(len j / mk) = q j +
+// floor(r j / mk), all 32-bit when len < 2^32 and mk <= 2^16 (r j < mk^2).
+__device__ __forceinline__ void split_range(const Plan &p, uint64_t b0, uint64_t len, uint64_t j, uint64_t mk,
+                                            uint64_t &s, uint64_t &e) {
+    uint64_t o0, o1;
+    if ((len >> 32) == 0 && mk <= 65536u) {
+        const uint32_t d = (uint32_t)mk, magic = mk == p.m ? p.magic_m : p.magic_m0, jj = (uint32_t)j;
+        const uint32_t q = udiv_magic((uint32_t)len, d, magic), r = (uint32_t)len - q * d;
+        o0 = (uint64_t)q * jj + udiv_magic(r * jj, d, magic);
+        o1 = (uint64_t)q * (jj + 1u) + udiv_magic(r * (jj + 1u), d, magic);
+    } else {
+        o0 = len * j / mk;
+        o1 = len * (j + 1) / mk;
+    }
+    s = b0 + o0;
+    e = b0 + o1;
+    if (len >= 64 * mk) {
+        if (j != 0) s -= (p.in_addr + s) & 31u;
+        if (j + 1 != mk) e -= (p.in_addr + e) & 31u;
+    }
 }
 
 // sub-chunk i's reporting chunk k (its bounds are p.bounds[k], p.bounds[k+1])
 __device__ __forceinline__ uint64_t sub_chunk_of(const Plan &p, uint64_t i) {
-    return i < p.m0 ? 0 : 1 + (i - p.m0) / p.m;
+    uint64_t k, j, mk;
+    sub_locate(p, i, k, j, mk);
+    return k;
 }
 // sub_range with the chunk's bounds already loaded (b0, b1 = bounds of sub_chunk_of(i))
 __device__ __forceinline__ void sub_range_b(const Plan &p, uint64_t i, uint64_t b0, uint64_t b1, uint64_t &s,
                                             uint64_t &e) {
-    uint64_t j, mk;
-    if (i < p.m0) { j = i; mk = p.m0; }
-    else { j = (i - p.m0) % p.m; mk = p.m; }
+    uint64_t k, j, mk;
+    sub_locate(p, i, k, j, mk);
     if (p.indep) {
         b0 = min(b0, p.n);
         b1 = min(max(b1, b0), p.n);
     }
     DFA_CHECK(b0 <= b1 && b1 <= p.n, "chunk bounds out of order or past n");
-    const uint64_t len = b1 - b0;
-    s = split_point(p, b0, len, j, mk);
-    e = split_point(p, b0, len, j + 1, mk);
+    split_range(p, b0, b1 - b0, j, mk, s, e);
     DFA_CHECK(b0 <= s && s <= e && e <= b1, "sub-chunk outside its chunk");
 }
 
 __device__ __forceinline__ void sub_range(const Plan &p, uint64_t i, uint64_t &s, uint64_t &e) {
     uint64_t k, j, mk;
-    if (i < p.m0) { k = 0; j = i; mk = p.m0; }
-    else { uint64_t t = i - p.m0; k = 1 + t / p.m; j = t % p.m; mk = p.m; }
+    sub_locate(p, i, k, j, mk);
     uint64_t b0 = p.bounds[k], b1 = p.bounds[k + 1];
     if (p.indep) {  // caller-given batch offsets: clamp (batch_out_kernel flags bad ones)
         b0 = min(b0, p.n);
         b1 = min(max(b1, b0), p.n);
     }
-    const uint64_t len = b1 - b0;
-    s = split_point(p, b0, len, j, mk);
-    e = split_point(p, b0, len, j + 1, mk);
+    split_range(p, b0, b1 - b0, j, mk, s, e);
 }
 
 // Reverse lookahead: the domain of sub-chunk i is I_sigma with
 // sigma the byte before it; the very first sub-chunk starts from {q0}.
 __device__ __forceinline__ bool chunk_first_sub(const Plan &p, uint64_t i) {
-    return i == 0 || (i >= p.m0 && (i - p.m0) % p.m == 0);
+    uint64_t k, j, mk;
+    sub_locate(p, i, k, j, mk);
+    return j == 0;
 }
 
 __device__ __forceinline__ uint32_t sub_domain(const DevTables &T, const Plan &p, const uint8_t *in, uint64_t i,
@@ -1196,7 +1233,7 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
             for (int e = 0; e < kLanes; e++) fin[e] = (uint32_t)e < u ? sfin[i * sk + e] : (uint32_t)kNone;
             grouped_epilogue(fin);
         }
-        if (surv) {
+        if (surv && !p.keep_amap) {
             // resolve this sub-chunk's converge_kernel map in place: survivor code
             // kSurvBase + e -> final state of survivor e (this thread just wrote them)
             uint32_t fin[kLanes];
@@ -1824,6 +1861,164 @@ __global__ void __launch_bounds__(256) walk_kernel(DevTables T, Tree tr, uint32_
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Factored composition for long rows behind the converge stage (I_max > kLanes):
+// a sub-chunk's map is its converge map amap (I_sigma -> absorbed state or
+// survivor code) followed by the <= kLanes survivor finals of lanes_kernel, so
+// every composed node is "the first leaf's amap, then nv values":
+//   FACT node: row[j] = amap_f[j] < kSurvBase ? amap_f[j] : vals[amap_f[j] - kSurvBase]
+//   FULL node: row[j] = vals[j]   (first leaf ended inside converge_kernel with
+//                                  all-absolute amap: vals = that row pushed on)
+// Composing a node costs nv (<= 8) chains instead of I_max (Eq.MapReduction,
+// P:819-830, on the image of the first map only); full rows are written for the
+// reporting chunks and the root alone (fexpand_kernel).
+// ---------------------------------------------------------------------------
+struct FNode {
+    const uint16_t *vals;
+    uint32_t nv, full, fl, dom;
+};
+
+__device__ __forceinline__ FNode fnode(const DevTables &T, const Tree &tr, uint32_t Lc, uint32_t c) {
+    FNode n;
+    if (Lc == 0) {
+        n.nv = tr.leaf_nv[c];
+        n.fl = c;
+        n.dom = tr.dom_of[c];
+        n.full = n.nv == 0;  // no survivor codes: the converge map holds final states only
+        if (n.full) { n.vals = tr.amap + (uint64_t)c * T.rs; n.nv = T.dom_size[n.dom]; }
+        else n.vals = tr.sfin + (uint64_t)c * tr.sk;
+    } else {
+        const uint32_t idx = tr.lv[Lc].off + c;
+        const uint32_t w = tr.node_nv[idx];
+        n.nv = w & 0x7FFFu;
+        n.full = w >> 15;
+        n.fl = tr.node_fl[idx];
+        n.dom = tr.doms[idx];
+        n.vals = tr.rows + (uint64_t)idx * T.rs;
+    }
+    DFA_CHECK(n.dom <= T.nclass && n.nv <= T.rs, "fnode: domain or value count");
+    return n;
+}
+
+// state s entering node B -> state leaving it (error states pass)
+__device__ __forceinline__ uint32_t fapply(const DevTables &T, const Tree &tr, const FNode &B, uint32_t s) {
+    if (T.has_dead && test_bit(T.dead_bits, s)) return s;
+    uint32_t r;
+    if (T.rank8) { r = __ldg(T.rank8 + (uint64_t)B.dom * T.nq + s); r = r == 0xFFu ? kNone : r; }
+    else r = __ldg(T.rank + (uint64_t)B.dom * T.nq + s);
+    if (r == kNone) { atomicMax(&tr.status->err, 8u); return 0; }
+    DFA_CHECK(r < T.rs, "fapply: rank past the row");
+    if (B.full) return B.vals[r];
+    const uint32_t c = tr.amap[(uint64_t)B.fl * T.rs + r];
+    if (c < kSurvBase) return c;
+    DFA_CHECK(c - kSurvBase < B.nv, "fapply: survivor code past the node's values");
+    return B.vals[c - kSurvBase];
+}
+
+// entry j of a node's full row
+__device__ __forceinline__ uint32_t frow(const DevTables &T, const Tree &tr, const FNode &N, uint32_t j) {
+    if (N.full) return N.vals[j];
+    const uint32_t c = tr.amap[(uint64_t)N.fl * T.rs + j];
+    return c < kSurvBase ? c : N.vals[c - kSurvBase];
+}
+
+// one level: 8 threads per node, thread e pushes value e (e + 8, ...) of the first child
+// through the node's other children
+__global__ void __launch_bounds__(256) fwalk_kernel(DevTables T, Tree tr, uint32_t L) {
+    const TreeLevel lv = tr.lv[L];
+    const uint64_t total = (uint64_t)lv.nodes * 8;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t node = (uint32_t)(t >> 3), e0 = (uint32_t)t & 7u;
+        uint32_t c0, c1;
+        group_range(lv, node, c0, c1);
+        const FNode A = fnode(T, tr, L - 1, c0);
+        const uint32_t idx = lv.off + node;
+        uint16_t *out = tr.rows + (uint64_t)idx * T.rs;
+        for (uint32_t e = e0; e < A.nv; e += 8) {
+            uint32_t s = A.vals[e];
+            for (uint32_t c = c0 + 1; c < c1; c++) s = fapply(T, tr, fnode(T, tr, L - 1, c), s);
+            out[e] = (uint16_t)s;
+        }
+        if (e0 == 0) {
+            tr.node_nv[idx] = (uint16_t)(A.nv | (A.full << 15));
+            tr.node_fl[idx] = A.fl;
+            tr.doms[idx] = (uint16_t)A.dom;
+        }
+    }
+}
+
+// full rows of level L's nodes: the reporting chunks (internal rows for starts/batch, API
+// rows in the user's order, e0) and the root (final state, accept, segment row)
+__global__ void __launch_bounds__(256) fexpand_kernel(DevTables T, Tree tr, uint32_t L) {
+    const TreeLevel lv = tr.lv[L];
+    const bool rep = L == tr.rep_level, root = L == tr.nlevels && tr.root_final;
+    const uint64_t total = (uint64_t)(rep ? lv.nodes : 1u) * T.rs;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t node = (uint32_t)(t / T.rs), j = (uint32_t)(t - (uint64_t)node * T.rs);
+        const FNode N = fnode(T, tr, L, node);
+        const uint32_t d0 = N.dom, u = T.dom_size[d0];
+        const uint32_t s = j < u ? frow(T, tr, N, j) : (uint32_t)kNone;
+        if (rep) {
+            tr.rep_full[(uint64_t)node * T.rs + j] = (uint16_t)s;
+            if (tr.user_rows && node > 0 && j < T.imax_user) {
+                // API row: user entry ju = internal entry xlat[ju]; padding 0xFFFF
+                const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : 0;
+                if (j >= du) tr.user_rows[(uint64_t)(node - 1) * T.imax_user + j] = kNone;
+            }
+            if (tr.user_rows && node > 0 && j < u && d0 < T.nclass) {
+                const uint32_t ju = T.ixlat[(uint64_t)d0 * T.rs + j];
+                if (ju != kNone) tr.user_rows[(uint64_t)(node - 1) * T.imax_user + ju] = (uint16_t)s;
+            }
+            if (tr.e0 && node == 0 && j == 0) tr.e0[0] = (uint16_t)s;
+            if (tr.user_row0 && node == 0) {
+                const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+                if (j < T.imax_user && j >= du) tr.user_row0[j] = kNone;
+                if (j < u) {
+                    const uint32_t ju = d0 < T.nclass ? T.ixlat[(uint64_t)d0 * T.rs + j] : j;
+                    if (ju != kNone) tr.user_row0[ju] = (uint16_t)s;
+                }
+            }
+        }
+        if (root && node == 0) {
+            if (tr.seg_row) {
+                // the segment map: the root's row over chunk 0's domain, in the user's order
+                const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+                if (j < T.imax_user && j >= du) tr.seg_row[j] = kNone;
+                if (j < u) {
+                    const uint32_t ju = d0 < T.nclass ? T.ixlat[(uint64_t)d0 * T.rs + j] : j;
+                    if (ju != kNone) tr.seg_row[ju] = (uint16_t)s;
+                }
+            }
+            if (j == 0) {
+                DevStatus *S = tr.status;
+                if (s == T.poison) atomicMax(&S->err, 5u);
+                S->final_state = s;
+                S->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
+                if (tr.dev_final) {
+                    tr.dev_final[0] = (uint16_t)s;
+                    tr.dev_final[1] = (uint16_t)S->accept;
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_fwalk_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
+    const uint64_t total = (uint64_t)tr.lv[L].nodes * 8;
+    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
+    fwalk_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fexpand_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
+    const uint64_t total = (uint64_t)(L == tr.rep_level ? tr.lv[L].nodes : 1u) * T.rs;
+    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
+    fexpand_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_walk_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
@@ -2729,6 +2924,12 @@ cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64
 
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
     return launch_walk_level(T, tr, L, sms, s);
+}
+cudaError_t launch_fwalk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
+    return launch_fwalk_level(T, tr, L, sms, s);
+}
+cudaError_t launch_fexpand(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
+    return launch_fexpand_level(T, tr, L, sms, s);
 }
 
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s) {

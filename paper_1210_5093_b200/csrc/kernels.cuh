@@ -62,7 +62,10 @@ struct Plan {
     uint64_t in_addr;        // device address of the input (split alignment)
     uint32_t indep;          // batch: every chunk is an independent input matched from q0
     unsigned long long *work; // DFA_OPT_COUNT_WORK: [0] converge, [1] lanes lane-steps; else null
+    uint32_t keep_amap;      // factored composition: lanes_kernel leaves the converge maps coded
+    uint32_t magic_m0, magic_m; // min(floor(2^32 / m0), 2^32 - 1), same for m: exact 32-bit division on the device
 };
+inline uint32_t plan_magic(uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : (uint32_t)((1ull << 32) / d); }
 
 // Fused composition tail of lanes_kernel (grouped path, one execution sub-chunk
 // per thread, so CTA b holds the contiguous leaves [b LPC, (b+1) LPC)): each CTA
@@ -128,6 +131,12 @@ struct Tree {
     const uint16_t *amap, *sfin;
     uint32_t sk;
     const uint16_t *dom_of;
+    // factored composition (fwalk_kernel / fexpand_kernel): survivor counts of the leaves,
+    // per node value count (bit 15: FULL) and first leaf, full rows of the reporting chunks
+    const uint8_t *leaf_nv;
+    uint16_t *node_nv;
+    uint32_t *node_fl;
+    uint16_t *rep_full;
     // nodes
     uint16_t *rows, *doms;
     uint32_t *counters;
@@ -161,6 +170,8 @@ int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s);
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
+cudaError_t launch_fwalk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
+cudaError_t launch_fexpand(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
 cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,
                              const uint16_t *maps, uint16_t *doms_out, uint16_t *sizes_out, uint16_t *maps_out,
                              DevStatus *st, int sms, cudaStream_t s);

@@ -903,6 +903,28 @@ def test_fused_tail_and_compose8(name, fused):
     check_match(c, opts={D.DFA_OPT_FUSED_TAIL: fused})
 
 
+@pytest.mark.parametrize("factored", [0, 1])
+@pytest.mark.parametrize("name", ["worst", "protein", "counter"])
+def test_factored_and_full_row_composition(name, factored):
+    """Maps of more than 16 entries behind the converge stage: the factored composition
+    (DFA_OPT_FACTORED = 1, the first sub-chunk's converge map then <= 8 survivor values per
+    node) and the full-row walk give the oracle's maps, starts and final -- long sub-chunks
+    (every node factored), chunks shorter than the convergence length (sub-chunks that end
+    inside converge_kernel: FULL nodes, also as a node's first child), a DFA whose lanes never
+    merge, several tree shapes (fan-in, sub-chunk targets)."""
+    if name == "counter":
+        a, x = automata.counter_dfa(37), inputs.uniform_bytes((1 << 19) + 77, seed=9)
+    else:
+        w = W.get(name)
+        a, x = w.automaton, w.input((1 << 20) + 1234)
+    c = Case(a, x, name)
+    for P, extra in ((1, {}), (2, {}), (17, {}), (300, {D.DFA_OPT_TREE_FANIN: 3}), (4099, {}),
+                     (33, {D.DFA_OPT_SUBCHUNK_TARGET: 5000}), (x.size // 24, {}),
+                     (x.size // 150, {D.DFA_OPT_SUBCHUNK_TARGET: 1 << 22, D.DFA_OPT_TREE_FANIN: 5})):
+        check_chunk_maps(c, P, opts={D.DFA_OPT_FACTORED: factored, **extra})
+    check_match(c, opts={D.DFA_OPT_FACTORED: factored})
+
+
 @pytest.mark.parametrize("name,G,P", [("random", 3, 64), ("keyword", 2, 129), ("protein", 2, 33), ("worst", 2, 17),
                                       ("tiny", 4, 16)])
 def test_segment_chunk_maps(name, G, P):
