@@ -760,6 +760,13 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
                 CK(launch_fexpand(T, tr, L, h->sms, s));
                 kernels++;
             }
+            // the levels above the reporting chunks: one CTA folds them in shared memory
+            // once they fit (no launch per level)
+            if (L >= tr.rep_level && L < tr.nlevels && tr.root_final && tr.lv[L].nodes <= ffold_cap()) {
+                CK(launch_ffold(T, tr, L, s));
+                kernels++;
+                break;
+            }
         }
         prof_end(h, s);
     }

@@ -1927,6 +1927,8 @@ __device__ __forceinline__ uint32_t frow(const DevTables &T, const Tree &tr, con
 // one level: 8 threads per node, thread e pushes value e (e + 8, ...) of the first child
 // through the node's other children
 __global__ void __launch_bounds__(256) fwalk_kernel(DevTables T, Tree tr, uint32_t L) {
+    pdl_trigger();
+    pdl_wait();
     const TreeLevel lv = tr.lv[L];
     const uint64_t total = (uint64_t)lv.nodes * 8;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -1952,7 +1954,33 @@ __global__ void __launch_bounds__(256) fwalk_kernel(DevTables T, Tree tr, uint32
 
 // full rows of level L's nodes: the reporting chunks (internal rows for starts/batch, API
 // rows in the user's order, e0) and the root (final state, accept, segment row)
+// the root's outputs for entry j of its row (value s): segment row, final state, accept bit
+__device__ __forceinline__ void froot_out(const DevTables &T, const Tree &tr, uint32_t d0, uint32_t u, uint32_t j,
+                                          uint32_t s) {
+    if (tr.seg_row) {
+        // the segment map: the root's row over chunk 0's domain, in the user's order
+        const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
+        if (j < T.imax_user && j >= du) tr.seg_row[j] = kNone;
+        if (j < u) {
+            const uint32_t ju = d0 < T.nclass ? T.ixlat[(uint64_t)d0 * T.rs + j] : j;
+            if (ju != kNone) tr.seg_row[ju] = (uint16_t)s;
+        }
+    }
+    if (j == 0) {
+        DevStatus *S = tr.status;
+        if (s == T.poison) atomicMax(&S->err, 5u);
+        S->final_state = s;
+        S->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
+        if (tr.dev_final) {
+            tr.dev_final[0] = (uint16_t)s;
+            tr.dev_final[1] = (uint16_t)S->accept;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) fexpand_kernel(DevTables T, Tree tr, uint32_t L) {
+    pdl_trigger();
+    pdl_wait();
     const TreeLevel lv = tr.lv[L];
     const bool rep = L == tr.rep_level, root = L == tr.nlevels && tr.root_final;
     const uint64_t total = (uint64_t)(rep ? lv.nodes : 1u) * T.rs;
@@ -1983,43 +2011,68 @@ __global__ void __launch_bounds__(256) fexpand_kernel(DevTables T, Tree tr, uint
                 }
             }
         }
-        if (root && node == 0) {
-            if (tr.seg_row) {
-                // the segment map: the root's row over chunk 0's domain, in the user's order
-                const uint32_t du = d0 < T.nclass ? T.dom_user_size[d0] : (d0 == T.start_dom ? 1u : 0u);
-                if (j < T.imax_user && j >= du) tr.seg_row[j] = kNone;
-                if (j < u) {
-                    const uint32_t ju = d0 < T.nclass ? T.ixlat[(uint64_t)d0 * T.rs + j] : j;
-                    if (ju != kNone) tr.seg_row[ju] = (uint16_t)s;
-                }
-            }
-            if (j == 0) {
-                DevStatus *S = tr.status;
-                if (s == T.poison) atomicMax(&S->err, 5u);
-                S->final_state = s;
-                S->accept = s < T.nq ? (uint32_t)test_bit(T.accept_bits, s) : 0u;
-                if (tr.dev_final) {
-                    tr.dev_final[0] = (uint16_t)s;
-                    tr.dev_final[1] = (uint16_t)S->accept;
-                }
-            }
-        }
+        if (root && node == 0) froot_out(T, tr, d0, u, j, s);
     }
 }
 
-cudaError_t launch_fwalk_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
-    const uint64_t total = (uint64_t)tr.lv[L].nodes * 8;
-    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
-    fwalk_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
-    return cudaGetLastError();
+// ffold_kernel: every level above Ls in one CTA (no launch per level): the N <= kFoldCap
+// nodes of level Ls are staged in shared memory (8 values each; FULL nodes keep their rows
+// in global memory) and folded in place with fan-in 4 -- node a absorbs a + s, a + 2s,
+// a + 3s at stride s = 1, 4, 16, ... (Eq.SeqReduction as a tree of Eq.MapReduction) -- then
+// the root's row gives the final state, accept bit and segment row (Alg.seqmatch l.4-6).
+constexpr uint32_t kFoldCap = 8192;
+__host__ __device__ __forceinline__ uint32_t ffold_smem_bytes(uint32_t N) { return N * 24u + 16u; }
+
+__global__ void __launch_bounds__(1024) ffold_kernel(DevTables T, Tree tr, uint32_t Ls) {
+    extern __shared__ uint4 smem4[];
+    pdl_wait();
+    const uint32_t N = tr.lv[Ls].nodes, off = tr.lv[Ls].off;
+    uint16_t *vals = reinterpret_cast<uint16_t *>(smem4);          // [N][8]
+    uint32_t *fl = reinterpret_cast<uint32_t *>(vals + (size_t)N * 8);  // [N]
+    uint16_t *dom = reinterpret_cast<uint16_t *>(fl + N);          // [N]
+    uint16_t *nvf = dom + N;                                       // [N] value count | FULL << 15
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        nvf[i] = tr.node_nv[off + i];
+        fl[i] = tr.node_fl[off + i];
+        dom[i] = tr.doms[off + i];
+        reinterpret_cast<uint4 *>(vals)[i] = *reinterpret_cast<const uint4 *>(tr.rows + (uint64_t)(off + i) * T.rs);
+    }
+    __syncthreads();
+    auto node = [&](uint32_t c) {
+        FNode n;
+        const uint32_t w = nvf[c];
+        n.nv = w & 0x7FFFu;
+        n.full = w >> 15;
+        n.fl = fl[c];
+        n.dom = dom[c];
+        n.vals = n.full ? tr.rows + (uint64_t)(off + c) * T.rs : vals + (size_t)c * 8;
+        DFA_CHECK(n.full || n.nv <= 8u, "ffold: factored node with more than 8 values");
+        return n;
+    };
+    for (uint64_t stride = 1; stride < N; stride *= 4) {
+        const uint32_t ngroups = (uint32_t)((N + 4 * stride - 1) / (4 * stride));
+        for (uint32_t g = threadIdx.x >> 3; g < ngroups; g += blockDim.x >> 3) {
+            const uint32_t a = (uint32_t)(g * 4 * stride);
+            const FNode A = node(a);
+            uint16_t *av = const_cast<uint16_t *>(A.vals);
+            for (uint32_t e = threadIdx.x & 7u; e < A.nv; e += 8) {
+                uint32_t s = av[e];
+                for (uint32_t q = 1; q < 4; q++) {
+                    const uint64_t c = a + q * stride;
+                    if (c >= N) break;
+                    s = fapply(T, tr, node((uint32_t)c), s);
+                }
+                av[e] = (uint16_t)s;
+            }
+        }
+        __syncthreads();
+    }
+    const FNode R = node(0);
+    const uint32_t u = T.dom_size[R.dom];
+    for (uint32_t j = threadIdx.x; j < T.rs; j += blockDim.x)
+        froot_out(T, tr, R.dom, u, j, j < u ? frow(T, tr, R, j) : (uint32_t)kNone);
 }
 
-cudaError_t launch_fexpand_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
-    const uint64_t total = (uint64_t)(L == tr.rep_level ? tr.lv[L].nodes : 1u) * T.rs;
-    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
-    fexpand_kernel<<<(unsigned)std::max<uint64_t>(grid, 1), 256, 0, s>>>(T, tr, L);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_walk_level(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
     const uint64_t total = (uint64_t)tr.lv[L].nodes * T.rs;
@@ -2728,6 +2781,9 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
     e = cudaFuncSetAttribute((void *)starts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
     if (e != cudaSuccess) return e;
 
+    e = cudaFuncSetAttribute((void *)ffold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ffold_smem_bytes(kFoldCap));
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute((void *)tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
@@ -2926,10 +2982,18 @@ cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms,
     return launch_walk_level(T, tr, L, sms, s);
 }
 cudaError_t launch_fwalk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
-    return launch_fwalk_level(T, tr, L, sms, s);
+    const uint64_t total = (uint64_t)tr.lv[L].nodes * 8;
+    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
+    return launch_pdl(fwalk_kernel, dim3((unsigned)std::max<uint64_t>(grid, 1)), dim3(256), 0, s, T, tr, L);
 }
 cudaError_t launch_fexpand(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s) {
-    return launch_fexpand_level(T, tr, L, sms, s);
+    const uint64_t total = (uint64_t)(L == tr.rep_level ? tr.lv[L].nodes : 1u) * T.rs;
+    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, (uint64_t)sms * 16);
+    return launch_pdl(fexpand_kernel, dim3((unsigned)std::max<uint64_t>(grid, 1)), dim3(256), 0, s, T, tr, L);
+}
+uint32_t ffold_cap() { return kFoldCap; }
+cudaError_t launch_ffold(const DevTables &T, const Tree &tr, uint32_t Ls, cudaStream_t s) {
+    return launch_pdl(ffold_kernel, dim3(1), dim3(1024), ffold_smem_bytes(tr.lv[Ls].nodes), s, T, tr, Ls);
 }
 
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s) {
