@@ -74,7 +74,7 @@ struct dfa_handle {
     DevBuf status, sfin, dom_of, surv, surv_n, surv_pos, amap;
     DevBuf lvlA, domA, counters, bounds, input, fold_rows, fold_doms, ticket, leaf_rows, leaf_dom, plan_bounds;
     DevBuf cta_start, leaf_rows2, leaf_dom2;
-    DevBuf node_nv, node_fl, rep_full;  // factored composition (long rows behind the converge stage)
+    DevBuf node_nv, node_fl, rep_full, clinks;  // factored composition (long rows behind the converge stage)
     int warp_compose = 1;
     int factored = 1;             // DFA_OPT_FACTORED
     int fused_tail = 0;           // DFA_OPT_FUSED_TAIL (measured slower than compose8: DESIGN.md)
@@ -684,6 +684,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
             CK(h->node_nv.ensure(total * 2));
             CK(h->node_fl.ensure(total * 4));
             CK(h->rep_full.ensure((uint64_t)P * T.rs * 2));
+            CK(h->clinks.ensure(((uint64_t)P / 8 + 1) * 16));
         }
         // arrival counters: valid across calls with the same tree (multiples of
         // the child counts), zeroed when the tree changes
@@ -748,14 +749,26 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     } else {
         // long rows: one entry-parallel launch per level (small fan-in, see tree_fanin)
         prof_begin(h, s, 2);
-        for (uint32_t L = 1; L <= tr.nlevels; L++) {
+        // factored: the levels up to the reporting chunks in one launch (a warp per chunk of
+        // <= fchunk_cap() leaves), else a launch per level
+        const bool chunk_pass = factored && tr.lv[1].S == P && tr.lv[1].f <= fchunk_cap() &&
+                                (P == 1 || tr.lv[1].m <= fchunk_cap());
+        if (chunk_pass) {
+            // (its group links feed ffold_kernel when the reporting level is the one it folds)
+            tr.clinks = tr.root_final && P > 1 && P <= ffold_cap() ? h->clinks.as<uint16_t>() : nullptr;
+            CK(launch_fchunk(T, tr, h->sms, s));
+            kernels++;
+        }
+        for (uint32_t L = chunk_pass ? tr.rep_level : 1; L <= tr.nlevels; L++) {
             if (!factored) {
                 CK(launch_walk(T, tr, L, h->sms, s));
                 kernels++;
                 continue;
             }
-            CK(launch_fwalk(T, tr, L, h->sms, s));
-            kernels++;
+            if (!(chunk_pass && L == tr.rep_level)) {  // (fchunk_kernel wrote the reporting level)
+                CK(launch_fwalk(T, tr, L, h->sms, s));
+                kernels++;
+            }
             if (L == tr.rep_level || (L == tr.nlevels && tr.root_final)) {
                 CK(launch_fexpand(T, tr, L, h->sms, s));
                 kernels++;
@@ -931,7 +944,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
         for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
         for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx,
-                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full})
+                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full, &h->clinks})
             b->release();
         h->h_hm.release();
         h->h_batch.release();

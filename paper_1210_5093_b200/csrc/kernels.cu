@@ -2015,6 +2015,152 @@ __global__ void __launch_bounds__(256) fexpand_kernel(DevTables T, Tree tr, uint
     }
 }
 
+// link values: state sv leaving a FACT node re-coded into the next FACT node's code space
+// (its first leaf nfl, domain nd): the next node's converge code amap[rank(sv)], or sv itself
+// for an error state.  U independent chains per thread, each stage's loads issued together
+// (the kernels that use it are latency-bound on these dependent L2 loads).
+template <int U>
+__device__ __forceinline__ void flink_batch(const DevTables &T, const Tree &tr, const bool (&ok)[U],
+                                            const uint32_t (&sv)[U], const uint32_t (&nd)[U],
+                                            const uint32_t (&nfl)[U], uint32_t (&c)[U]) {
+    bool lk[U];
+    uint32_t r[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) lk[u] = ok[u] && !(T.has_dead && test_bit(T.dead_bits, sv[u]));
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        r[u] = 0;
+        if (!lk[u]) continue;
+        if (T.rank8) { r[u] = __ldg(T.rank8 + (uint64_t)nd[u] * T.nq + sv[u]); r[u] = r[u] == 0xFFu ? (uint32_t)kNone : r[u]; }
+        else r[u] = __ldg(T.rank + (uint64_t)nd[u] * T.nq + sv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        c[u] = sv[u];
+        if (!lk[u]) continue;
+        if (r[u] == kNone) { atomicMax(&tr.status->err, 8u); r[u] = 0; }
+        DFA_CHECK(r[u] < T.rs, "flink: rank past the row");
+        c[u] = tr.amap[(uint64_t)nfl[u] * T.rs + r[u]];
+    }
+}
+
+// fchunk_kernel: the levels up to the reporting chunks in one launch, a warp per chunk of
+// n <= 64 leaves.  No FULL leaf (the common case): every survivor final of leaf i is
+// re-coded into leaf i+1's code space (link_i[e] = amap_{i+1}[rank_{i+1}(sfin_i[e])], the
+// last leaf keeps its states), all in parallel; the chunk's map is then a pairwise gather
+// between 8-entry rows in the warp's shared memory.  Otherwise: value e of the first leaf
+// is pushed through the leaves in order (fapply).  Writes the chunk's node like fwalk_kernel.
+constexpr uint32_t kChunkLeaves = 64;
+__global__ void __launch_bounds__(256) fchunk_kernel(DevTables T, Tree tr) {
+    __shared__ uint16_t Ls[8][kChunkLeaves * 8];
+    __shared__ uint16_t doms[8][kChunkLeaves];
+    __shared__ uint8_t nvs[8][kChunkLeaves];
+    pdl_trigger();
+    pdl_wait();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const TreeLevel l1 = tr.lv[1];
+    const uint32_t P = tr.lv[tr.rep_level].nodes, roff = tr.lv[tr.rep_level].off;
+    uint16_t *Lw = Ls[warp], *dw = doms[warp];
+    uint8_t *nw = nvs[warp];
+    // chunk k's values re-coded into chunk k+1's code space (the last chunk keeps its states),
+    // composed over the CTA's group of 8 chunks -> clinks[g]: ffold_kernel then folds P / 8
+    // rows with no lookups.  A FULL chunk or successor sets the status flag instead.
+    __shared__ uint16_t CL[8][8];
+    const uint32_t G = (P + 7) / 8;
+    for (uint32_t g = blockIdx.x; g < G; g += gridDim.x) {
+      const uint32_t k = g * 8 + warp;
+      if (k < P) {
+        const uint32_t c0 = k == 0 ? 0u : l1.f + (k - 1) * l1.m, n = k == 0 ? l1.f : l1.m;
+        bool full = false;
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t nv = tr.leaf_nv[c0 + i], d = tr.dom_of[c0 + i];
+            nw[i] = (uint8_t)nv;
+            dw[i] = (uint16_t)d;
+            full |= nv == 0 && T.dom_size[d] != 0;
+        }
+        full = __any_sync(0xffffffffu, full);
+        __syncwarp();
+        const uint32_t idx = roff + k;
+        uint16_t *out = tr.rows + (uint64_t)idx * T.rs;
+        if (!full) {
+            constexpr int U = 8;
+            for (uint32_t t0 = lane; t0 < n * 8; t0 += 32 * U) {
+                bool has[U], ok[U];
+                uint32_t sv[U], nd[U], nfl[U], c[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t t = t0 + 32 * u, i = t >> 3, e = t & 7u;
+                    has[u] = t < n * 8 && e < nw[i];
+                    ok[u] = has[u] && i + 1 < n;  // (the chunk's last leaf keeps its states)
+                    sv[u] = has[u] ? (uint32_t)tr.sfin[(uint64_t)(c0 + i) * tr.sk + e] : 0u;
+                    nd[u] = ok[u] ? (uint32_t)dw[i + 1] : 0u;
+                    nfl[u] = c0 + i + 1;
+                }
+                flink_batch<U>(T, tr, ok, sv, nd, nfl, c);
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    DFA_CHECK(!ok[u] || c[u] < kSurvBase || c[u] - kSurvBase < nw[((t0 + 32 * u) >> 3) + 1], "fchunk: link code");
+                    if (has[u]) Lw[t0 + 32 * u] = (uint16_t)c[u];
+                }
+            }
+            __syncwarp();
+            for (uint32_t stride = 1; stride < n; stride *= 2) {
+                const uint32_t pairs = (n + stride - 1) / (2 * stride);
+                for (uint32_t t = lane; t < pairs * 8; t += 32) {
+                    const uint32_t a = (t >> 3) * 2 * stride, b = a + stride;
+                    if (b >= n) continue;
+                    const uint32_t c = Lw[a * 8 + (t & 7u)];
+                    if (c >= kSurvBase && c != kNone && (t & 7u) < nw[a]) Lw[a * 8 + (t & 7u)] = Lw[b * 8 + (c - kSurvBase)];
+                }
+                __syncwarp();
+            }
+            if (lane < nw[0]) out[lane] = Lw[lane];
+            if (lane == 0) {
+                tr.node_nv[idx] = nw[0];
+                tr.node_fl[idx] = c0;
+                tr.doms[idx] = dw[0];
+            }
+            if (tr.clinks && lane < 8) {
+                const bool ok1[1] = {lane < nw[0] && k + 1 < P};
+                const uint32_t sv1[1] = {lane < nw[0] ? (uint32_t)Lw[lane] : (uint32_t)kNone};
+                uint32_t nd1[1] = {0}, c1[1];
+                const uint32_t nfl1[1] = {c0 + n};
+                if (k + 1 < P) {
+                    nd1[0] = tr.dom_of[c0 + n];
+                    if (tr.leaf_nv[c0 + n] == 0 && T.dom_size[nd1[0]] != 0) atomicOr(&tr.status->pad, 1u);  // FULL successor
+                }
+                flink_batch<1>(T, tr, ok1, sv1, nd1, nfl1, c1);
+                CL[warp][lane] = (uint16_t)c1[0];
+            }
+        } else {
+            if (tr.clinks && lane == 0) atomicOr(&tr.status->pad, 1u);
+            const FNode A = fnode(T, tr, 0, c0);
+            for (uint32_t e = lane; e < A.nv; e += 32) {
+                uint32_t sv = A.vals[e];
+                for (uint32_t c = c0 + 1; c < c0 + n; c++) sv = fapply(T, tr, fnode(T, tr, 0, c), sv);
+                out[e] = (uint16_t)sv;
+            }
+            if (lane == 0) {
+                tr.node_nv[idx] = (uint16_t)(A.nv | (A.full << 15));
+                tr.node_fl[idx] = A.fl;
+                tr.doms[idx] = (uint16_t)A.dom;
+            }
+        }
+        __syncwarp();
+      }
+      if (tr.clinks) {
+        __syncthreads();
+        if (warp == 0 && lane < 8) {
+            const uint32_t cnt = min(8u, P - g * 8);
+            uint32_t c = CL[0][lane];
+            for (uint32_t w = 1; w < cnt && c >= kSurvBase && c != kNone; w++) c = CL[w][c - kSurvBase];
+            tr.clinks[(uint64_t)g * 8 + lane] = (uint16_t)c;
+        }
+        __syncthreads();
+      }
+    }
+}
+
 // ffold_kernel: every level above Ls in one CTA (no launch per level): the N <= kFoldCap
 // nodes of level Ls are staged in shared memory (8 values each; FULL nodes keep their rows
 // in global memory) and folded in place with fan-in 4 -- node a absorbs a + s, a + 2s,
@@ -2028,6 +2174,33 @@ __global__ void __launch_bounds__(1024) ffold_kernel(DevTables T, Tree tr, uint3
     pdl_wait();
     const uint32_t N = tr.lv[Ls].nodes, off = tr.lv[Ls].off;
     uint16_t *vals = reinterpret_cast<uint16_t *>(smem4);          // [N][8]
+    // pairwise gather fold of M link rows in shared memory (row a absorbs row a + stride)
+    auto fold_rounds = [&](uint32_t M) {
+        for (uint64_t stride = 1; stride < M; stride *= 2) {
+            const uint64_t pairs = (M + stride - 1) / (2 * stride);  // rows a = 2 stride g with a + stride < M
+            for (uint64_t t = threadIdx.x; t < pairs * 8; t += blockDim.x) {
+                const uint64_t a = (t >> 3) * 2 * stride, b = a + stride;
+                if (b >= M) continue;
+                const uint32_t c = vals[a * 8 + (t & 7u)];
+                if (c >= kSurvBase && c != kNone) vals[a * 8 + (t & 7u)] = vals[b * 8 + (c - kSurvBase)];
+            }
+            __syncthreads();
+        }
+    };
+    if (tr.clinks && Ls == tr.rep_level && tr.status->pad == 0) {
+        // fchunk_kernel left the links composed per group of 8 chunks: fold those rows
+        const uint32_t G = (N + 7) / 8;
+        for (uint32_t i = threadIdx.x; i < G; i += blockDim.x)
+            reinterpret_cast<uint4 *>(vals)[i] = reinterpret_cast<const uint4 *>(tr.clinks)[i];
+        __syncthreads();
+        fold_rounds(G);
+        FNode R = fnode(T, tr, Ls, 0);
+        R.vals = vals;
+        const uint32_t u = T.dom_size[R.dom];
+        for (uint32_t j = threadIdx.x; j < T.rs; j += blockDim.x)
+            froot_out(T, tr, R.dom, u, j, j < u ? frow(T, tr, R, j) : (uint32_t)kNone);
+        return;
+    }
     uint32_t *fl = reinterpret_cast<uint32_t *>(vals + (size_t)N * 8);  // [N]
     uint16_t *dom = reinterpret_cast<uint16_t *>(fl + N);          // [N]
     uint16_t *nvf = dom + N;                                       // [N] value count | FULL << 15
@@ -2049,6 +2222,36 @@ __global__ void __launch_bounds__(1024) ffold_kernel(DevTables T, Tree tr, uint3
         DFA_CHECK(n.full || n.nv <= 8u, "ffold: factored node with more than 8 values");
         return n;
     };
+    // No FULL node (the common case): every node's values are first re-coded into the next
+    // node's code space -- link_k[e] = amap_{k+1}[rank_{k+1}(vals_k[e])], all N x 8 lookups
+    // in parallel -- then Eq.MapReduction is a gather between 8-entry rows in shared memory
+    // (absolute values pass: error and absorbing states), pairwise, log2 N rounds.
+    bool any_full = false;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) any_full |= (nvf[i] >> 15) != 0;
+    if (!__syncthreads_or(any_full)) {
+        constexpr int U = 8;
+        for (uint32_t t0 = threadIdx.x; t0 < (N - 1) * 8; t0 += blockDim.x * U) {
+            bool ok[U];
+            uint32_t sv[U], nd[U], nfl[U], c[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t t = t0 + blockDim.x * u, k = t >> 3;
+                ok[u] = t < (N - 1) * 8 && (t & 7u) < (nvf[k] & 0x7FFFu);
+                sv[u] = ok[u] ? (uint32_t)vals[t] : 0u;
+                nd[u] = ok[u] ? (uint32_t)dom[k + 1] : 0u;
+                nfl[u] = ok[u] ? fl[k + 1] : 0u;
+            }
+            flink_batch<U>(T, tr, ok, sv, nd, nfl, c);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t t = t0 + blockDim.x * u;
+                DFA_CHECK(!ok[u] || c[u] < kSurvBase || c[u] - kSurvBase < (nvf[(t >> 3) + 1] & 0x7FFFu), "ffold: link code");
+                if (t < (N - 1) * 8) vals[t] = ok[u] ? (uint16_t)c[u] : kNone;  // (unused entries: never followed)
+            }
+        }
+        __syncthreads();
+        fold_rounds(N);
+    } else
     for (uint64_t stride = 1; stride < N; stride *= 4) {
         const uint32_t ngroups = (uint32_t)((N + 4 * stride - 1) / (4 * stride));
         for (uint32_t g = threadIdx.x >> 3; g < ngroups; g += blockDim.x >> 3) {
@@ -2992,6 +3195,12 @@ cudaError_t launch_fexpand(const DevTables &T, const Tree &tr, uint32_t L, int s
     return launch_pdl(fexpand_kernel, dim3((unsigned)std::max<uint64_t>(grid, 1)), dim3(256), 0, s, T, tr, L);
 }
 uint32_t ffold_cap() { return kFoldCap; }
+uint32_t fchunk_cap() { return kChunkLeaves; }
+cudaError_t launch_fchunk(const DevTables &T, const Tree &tr, int sms, cudaStream_t s) {
+    const uint32_t P = tr.lv[tr.rep_level].nodes;
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((P + 7) / 8, (uint32_t)sms * 8));
+    return launch_pdl(fchunk_kernel, dim3(grid), dim3(256), 0, s, T, tr);
+}
 cudaError_t launch_ffold(const DevTables &T, const Tree &tr, uint32_t Ls, cudaStream_t s) {
     return launch_pdl(ffold_kernel, dim3(1), dim3(1024), ffold_smem_bytes(tr.lv[Ls].nodes), s, T, tr, Ls);
 }

@@ -94,7 +94,7 @@ struct DevStatus {
     uint32_t err;            // 0 ok, 5 bad symbol, 8 internal
     uint32_t final_state;
     uint32_t accept;
-    uint32_t pad;
+    uint32_t pad;            // factored composition: bit 0 = some chunk node is FULL (no group links)
 };
 
 struct Shape {
@@ -137,6 +137,7 @@ struct Tree {
     uint16_t *node_nv;
     uint32_t *node_fl;
     uint16_t *rep_full;
+    uint16_t *clinks;        // [ceil(P/8)][8] fchunk_kernel: links composed per group of 8 chunks (or null)
     // nodes
     uint16_t *rows, *doms;
     uint32_t *counters;
@@ -172,6 +173,8 @@ cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_b
 cudaError_t launch_walk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
 cudaError_t launch_fwalk(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
 cudaError_t launch_fexpand(const DevTables &T, const Tree &tr, uint32_t L, int sms, cudaStream_t s);
+uint32_t fchunk_cap(); // most leaves per reporting chunk fchunk_kernel takes
+cudaError_t launch_fchunk(const DevTables &T, const Tree &tr, int sms, cudaStream_t s);
 uint32_t ffold_cap();  // most nodes ffold_kernel stages in shared memory
 cudaError_t launch_ffold(const DevTables &T, const Tree &tr, uint32_t Ls, cudaStream_t s);
 cudaError_t launch_lookahead(const DevTables &T, const uint8_t *in, const uint64_t *bounds, uint32_t P, uint32_t r,
