@@ -51,8 +51,11 @@ DFA_HD constexpr uint32_t rep_log_of(int mode) { return mode == kRepU8x8 ? 3u : 
 #ifndef DFA_WIN16_MAX_THREADS
 #define DFA_WIN16_MAX_THREADS 1024  // window_u16 (Protein) CTA bound; -D for the register-budget experiment
 #endif
+#ifndef DFA_PACKED9_MAX_THREADS
+#define DFA_PACKED9_MAX_THREADS 704  // packed9 (Worst) CTA bound; -D for the register-budget experiment
+#endif
 DFA_HD constexpr int lanes_max_threads(int mode) {
-    return mode == kRepU8x8 ? 640 : mode == kPacked9 ? 704 : mode == kWindowU16 ? DFA_WIN16_MAX_THREADS : 1024;
+    return mode == kRepU8x8 ? 640 : mode == kPacked9 ? DFA_PACKED9_MAX_THREADS : mode == kWindowU16 ? DFA_WIN16_MAX_THREADS : 1024;
 }
 
 struct Prep {
