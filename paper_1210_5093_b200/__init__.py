@@ -42,6 +42,7 @@ DFA_OPT_STICKY_PARKING = 12
 DFA_OPT_COUNT_WORK = 13
 DFA_OPT_FUSED_TAIL = 14
 DFA_OPT_FACTORED = 15
+DFA_OPT_LOOKAHEAD2 = 16
 
 
 def DFA_CREATE_TABLE_MODE(m: int) -> int:

@@ -77,6 +77,8 @@ struct dfa_handle {
     DevBuf node_nv, node_fl, rep_full, clinks;  // factored composition (long rows behind the converge stage)
     int warp_compose = 1;
     int factored = 1;             // DFA_OPT_FACTORED
+    int lookahead2 = 1;           // DFA_OPT_LOOKAHEAD2
+    DevBuf dom2;                  // two-symbol initial sets + sizes (converge stage)
     int fused_tail = 0;           // DFA_OPT_FUSED_TAIL (measured slower than compose8: DESIGN.md)
     DevBuf part_rows, part_doms, chunk_cnt;
     std::vector<uint64_t> plan_key;
@@ -248,6 +250,43 @@ dfa_status upload(dfa_handle *h) {
     T.ixlat = reinterpret_cast<const uint16_t *>(at(12));
     T.dead_user_bits = reinterpret_cast<const uint32_t *>(at(13));
     T.sticky_bits = reinterpret_cast<const uint32_t *>(at(14));
+    // two-symbol initial sets for the converge stage (Eq.istatesm, r = 2): delta(I_c1, c2) \ Z
+    // as (state, rank in I_c2) pairs; skipped for small I_max (no converge stage), the Alg.2
+    // ablation and tables over 128 MiB
+    T.dom2 = nullptr;
+    T.dom2_size = nullptr;
+    T.dom2_stride = 0;
+    if (imax > (uint32_t)kLanes && !p.full_domain && nq <= 0x7F00u) {
+        std::vector<std::vector<uint32_t>> sets((size_t)nc * nc);
+        std::vector<uint8_t> mark(nq);
+        uint32_t smax = 0;
+        for (uint32_t c1 = 0; c1 < nc; c1++)
+            for (uint32_t c2 = 0; c2 < nc; c2++) {
+                std::fill(mark.begin(), mark.end(), 0);
+                const uint32_t b = p.class_rep[c2];
+                for (uint16_t q : p.dom[c1]) mark[p.full[(size_t)q * 256 + b]] = 1;
+                auto &v = sets[(size_t)c1 * nc + c2];
+                for (uint32_t j = 0; j < p.dom[c2].size(); j++)  // ascending states = ascending ranks
+                    if (mark[p.dom[c2][j]]) v.push_back((uint32_t)p.dom[c2][j] | (j << 16));
+                smax = std::max<uint32_t>(smax, (uint32_t)v.size());
+            }
+        const size_t entries = (size_t)nc * nc * smax;
+        if (smax && entries * 4 <= (size_t)128 << 20) {
+            std::vector<uint32_t> flat(entries, 0xFFFFFFFFu);
+            std::vector<uint16_t> sz((size_t)nc * nc);
+            for (size_t i = 0; i < sets.size(); i++) {
+                sz[i] = (uint16_t)sets[i].size();
+                std::copy(sets[i].begin(), sets[i].end(), flat.begin() + i * smax);
+            }
+            const size_t szoff = (entries * 4 + 255) & ~size_t(255);
+            CK(h->dom2.ensure(szoff + sz.size() * 2));
+            CK(cudaMemcpy(h->dom2.p, flat.data(), entries * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(static_cast<uint8_t *>(h->dom2.p) + szoff, sz.data(), sz.size() * 2, cudaMemcpyHostToDevice));
+            T.dom2 = h->dom2.as<uint32_t>();
+            T.dom2_size = reinterpret_cast<const uint16_t *>(static_cast<uint8_t *>(h->dom2.p) + szoff);
+            T.dom2_stride = smax;
+        }
+    }
     T.has_sticky = 0;
     for (uint32_t w : sticky) T.has_sticky |= w != 0;
     h->sticky_avail = T.has_sticky;
@@ -473,7 +512,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     }
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
               o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in, o.indep ? 1u : 0u,
-              work, 0u, plan_magic(m0), plan_magic(m)};
+              work, 0u, 0u, plan_magic(m0), plan_magic(m)};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;
@@ -498,6 +537,12 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     const uint8_t *surv_n = nullptr;
     const uint64_t *surv_pos = nullptr;
     int kernels = 0;
+    const bool grouped = sp.g_log != kNoWarpGroup;
+    // long rows behind the converge stage compose in factored form (fchunk/fwalk/ffold): the
+    // converge maps stay coded, and internal sub-chunks may start from the two-symbol sets
+    const bool factored = stageA && wpc && !grouped && T.rs > 16 && h->factored;
+    plan.keep_amap = factored ? 1u : 0u;
+    plan.use_dom2 = factored && h->lookahead2 ? 1u : 0u;
     if (stageA && wpc) {
         CK(h->surv.ensure(NS * kLanes * 2));
         CK(h->surv_n.ensure(NS));
@@ -515,11 +560,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
         surv_n = h->surv_n.as<uint8_t>();
         surv_pos = h->surv_pos.as<uint64_t>();
     }
-    const bool grouped = sp.g_log != kNoWarpGroup;
-    // long rows behind the converge stage compose in factored form (fwalk_kernel): the
-    // converge maps stay coded
-    const bool factored = amap && !grouped && T.rs > 16 && h->factored;
-    plan.keep_amap = factored ? 1u : 0u;
+
     const int threads = sp.threads;
     const int occ = std::max(1, lanes_occupancy(T, threads));
     const uint64_t grid = std::min<uint64_t>((uint64_t)h->sms * occ, (NS + threads - 1) / threads);
@@ -944,7 +985,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
         for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
         for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx,
-                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full, &h->clinks})
+                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full, &h->clinks, &h->dom2})
             b->release();
         h->h_hm.release();
         h->h_batch.release();
@@ -1208,7 +1249,7 @@ dfa_status chunk_maps_impl(dfa_handle_t h, const uint8_t *dev_input, uint64_t le
                        (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
                        (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
                        (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work, (uint64_t)h->fused_tail,
-                       (uint64_t)h->factored,
+                       (uint64_t)h->factored, (uint64_t)h->lookahead2,
                        (uint64_t)g_scratch_gen.load()})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
@@ -1431,6 +1472,9 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
         return DFA_OK;
     case DFA_OPT_FACTORED:
         h->factored = value ? 1 : 0;
+        return DFA_OK;
+    case DFA_OPT_LOOKAHEAD2:
+        h->lookahead2 = value ? 1 : 0;
         return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         h->threads_auto = value == 0;

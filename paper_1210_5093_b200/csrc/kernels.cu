@@ -143,9 +143,9 @@ __device__ __forceinline__ uint64_t sub_chunk_of(const Plan &p, uint64_t i) {
     return k;
 }
 // sub_range with the chunk's bounds already loaded (b0, b1 = bounds of sub_chunk_of(i))
-__device__ __forceinline__ void sub_range_b(const Plan &p, uint64_t i, uint64_t b0, uint64_t b1, uint64_t &s,
-                                            uint64_t &e) {
-    uint64_t k, j, mk;
+__device__ __forceinline__ void sub_range_b(const Plan &p, uint64_t i, uint64_t &b0, uint64_t b1, uint64_t &s,
+                                            uint64_t &e, uint64_t &j) {
+    uint64_t k, mk;
     sub_locate(p, i, k, j, mk);
     if (p.indep) {
         b0 = min(b0, p.n);
@@ -1359,8 +1359,8 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
         nb1 = p.bounds[k + 1];
     }
     for (; i < p.NS; i += warps_total) {
-        uint64_t start, end;
-        sub_range_b(p, i, nb0, nb1, start, end);
+        uint64_t start, end, jsub, cb0 = nb0;
+        sub_range_b(p, i, cb0, nb1, start, end, jsub);
         if (i + warps_total < p.NS) {
             const uint64_t k = sub_chunk_of(p, i + warps_total);
             nb0 = p.bounds[k];
@@ -1376,6 +1376,21 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
         uint32_t np = u;
         uint64_t pos = start;
         bool fresh = true;  // the pool is still the domain list itself: entry e = (dl[e], id e)
+        // An internal sub-chunk (not a reporting chunk's first: those report over all of
+        // I_sigma) starts from the two-symbol set I_{s1 s2} = delta(I_s1, s2) \ Z of the two
+        // bytes before it, a subset of I_s2 that holds every state the run can be in
+        // (Eq.istatesm, Lemma 1): fewer lanes (Worst 165 of 240, Protein 25 of 77).  Lane ids
+        // stay ranks in I_s2, so the map and the composition do not change; the entries of
+        // unreachable ranks are kNone and never looked up.
+        const uint32_t *dl2 = nullptr;
+        if (p.use_dom2 && T.dom2 && jsub != 0 && start >= cb0 + 2) {
+            const uint32_t pair = (uint32_t)T.byte_class[__ldg(in + start - 2)] * T.nclass + dom;
+            dl2 = T.dom2 + (uint64_t)pair * T.dom2_stride;
+            np = T.dom2_size[pair];
+            DFA_CHECK(dom < T.nclass && np <= u, "converge: two-symbol set");
+            for (uint32_t j = lane; j < u; j += 32) link[j] = kNone;
+            __syncwarp();
+        }
         // window [pos, min(next 16-byte boundary of the address, end)): bytes k0..k1-1 of v
         uint4 v;
         uint32_t k0, k1;
@@ -1410,8 +1425,9 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
                     uint32_t q = 0;
                     id[l] = e;
                     if (e < np) {
-                        q = fresh ? (uint32_t)__ldg(dl + e) : (uint32_t)pool_s[e];
-                        if (!fresh) id[l] = pool_id[e];
+                        if (!fresh) { q = pool_s[e]; id[l] = pool_id[e]; }
+                        else if (dl2) { const uint32_t w = __ldg(dl2 + e); q = w & 0xFFFFu; id[l] = w >> 16; }
+                        else q = __ldg(dl + e);
                     }
                     DFA_CHECK(q < T.nq && (e >= np || id[l] < T.imax), "converge: pool entry");
                     s[l] = tab.enc(q);
@@ -1489,8 +1505,9 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
             {
                 uint32_t q = 0;
                 if (act) {
-                    q = fresh ? (uint32_t)__ldg(dl + lane) : (uint32_t)pool_s[lane];
-                    if (!fresh) id = pool_id[lane];
+                    if (!fresh) { q = pool_s[lane]; id = pool_id[lane]; }
+                    else if (dl2) { const uint32_t w = __ldg(dl2 + lane); q = w & 0xFFFFu; id = w >> 16; }
+                    else q = __ldg(dl + lane);
                 }
                 st1[0] = tab.enc(q);
             }
@@ -1533,8 +1550,9 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
         } else {
             // the sub-chunk ended with more than 32 lanes: its map is the lanes' states
             for (uint32_t e = lane; e < np; e += 32) {
-                if (fresh) link[e] = __ldg(dl + e);
-                else link[pool_id[e]] = pool_s[e];
+                if (!fresh) link[pool_id[e]] = pool_s[e];
+                else if (dl2) { const uint32_t w = __ldg(dl2 + e); link[w >> 16] = (uint16_t)w; }
+                else link[e] = __ldg(dl + e);
             }
             if (lane == 0) { surv_n[i] = 0; surv_pos[i] = end; }
         }
@@ -1904,6 +1922,7 @@ __device__ __forceinline__ FNode fnode(const DevTables &T, const Tree &tr, uint3
 
 // state s entering node B -> state leaving it (error states pass)
 __device__ __forceinline__ uint32_t fapply(const DevTables &T, const Tree &tr, const FNode &B, uint32_t s) {
+    if (s == kNone) return s;  // (an unreachable rank of a FULL node behind a two-symbol start)
     if (T.has_dead && test_bit(T.dead_bits, s)) return s;
     uint32_t r;
     if (T.rank8) { r = __ldg(T.rank8 + (uint64_t)B.dom * T.nq + s); r = r == 0xFFu ? kNone : r; }

@@ -41,6 +41,12 @@ struct DevTables {
     const uint16_t *dom_user_size; // [nclass]
     const uint32_t *dead_user_bits; // user Z (reading R1) over the user states
     const uint32_t *sticky_bits;    // states kept by every byte that is not a universal kill byte
+    // two-symbol initial sets (Eq.istatesm with r = 2) for the converge stage:
+    // dom2[(c1 * nclass + c2) * dom2_stride + e] = state | rank in I_c2 << 16, ascending, of
+    // delta(I_c1, c2) \ Z; null when not built (small I_max, Alg.2 ablation, table too large)
+    const uint32_t *dom2;
+    const uint16_t *dom2_size;
+    uint32_t dom2_stride;
     uint32_t nq, nclass, start_dom, imax, imax_user;
     uint32_t nq_user, ns;       // user |Q| and |Sigma|
     uint32_t rs;                // map row stride: imax rounded up to 8 (16-byte rows)
@@ -63,6 +69,7 @@ struct Plan {
     uint32_t indep;          // batch: every chunk is an independent input matched from q0
     unsigned long long *work; // DFA_OPT_COUNT_WORK: [0] converge, [1] lanes lane-steps; else null
     uint32_t keep_amap;      // factored composition: lanes_kernel leaves the converge maps coded
+    uint32_t use_dom2;       // converge_kernel starts internal sub-chunks from the two-symbol sets
     uint32_t magic_m0, magic_m; // min(floor(2^32 / m0), 2^32 - 1), same for m: exact 32-bit division on the device
 };
 inline uint32_t plan_magic(uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : (uint32_t)((1ull << 32) / d); }

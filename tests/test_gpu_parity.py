@@ -922,6 +922,8 @@ def test_factored_and_full_row_composition(name, factored):
                      (33, {D.DFA_OPT_SUBCHUNK_TARGET: 5000}), (x.size // 24, {}),
                      (x.size // 150, {D.DFA_OPT_SUBCHUNK_TARGET: 1 << 22, D.DFA_OPT_TREE_FANIN: 5})):
         check_chunk_maps(c, P, opts={D.DFA_OPT_FACTORED: factored, **extra})
+        if factored:  # internal sub-chunks from I_sigma instead of the two-symbol sets (Eq.istatesm)
+            check_chunk_maps(c, P, opts={D.DFA_OPT_LOOKAHEAD2: 0, **extra})
     check_match(c, opts={D.DFA_OPT_FACTORED: factored})
 
 
