@@ -16,7 +16,7 @@ B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 --quiet-
 $B > $O/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 40 --csv --log-file $O/launches_worst.csv $B > /dev/null 2>&1
 for c in worst protein; do
   Q="python bench.py --config $c --n 1073741824 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --quiet-json --no-lookahead --no-batch --no-ceiling --no-work"
-  $Q > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"lanes_kernel|converge_kernel|walk_kernel" -s 9 -c 3 -o $O/$c $Q > /dev/null 2>&1
+  $Q > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"lanes_kernel|converge_kernel|fchunk_kernel|fexpand_kernel|ffold_kernel" -s 15 -c 5 -o $O/$c $Q > /dev/null 2>&1
 done
 for c in random keyword tiny; do
   K="python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 --quiet-json --no-lookahead --no-batch --no-ceiling --no-work"
