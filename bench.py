@@ -89,7 +89,7 @@ def parse():
 
 OPTS = {"subchunk_target": 1, "convergence": 2, "threads_per_cta": 4, "tree_fanin": 5, "fold_in_tree": 6,
         "warp_compose": 7, "graphs": 8, "max_lanes": 9, "host_piece": 10, "early_exit": 11, "sticky_parking": 12,
-        "fused_tail": 14}
+        "fused_tail": 14, "factored": 15, "lookahead2": 16, "tma_input": 17}
 
 
 def peaks():

@@ -320,9 +320,12 @@ enum {
                                     composed in factored form (the first sub-chunk's converge map, then <= 8
                                     survivor values per node; Eq.MapReduction on the image of the first map);
                                     0: every node composes full rows (walk_kernel) */
-    DFA_OPT_LOOKAHEAD2 = 16      /* 1 (default): with the factored composition, internal execution sub-chunks
+    DFA_OPT_LOOKAHEAD2 = 16,     /* 1 (default): with the factored composition, internal execution sub-chunks
                                     start from the two-symbol initial set I_{s1 s2} (Eq.istatesm, r = 2,
                                     PAPER.md 1129-1147) instead of I_{s2}; results identical, fewer lanes */
+    DFA_OPT_TMA_INPUT = 17       /* 1: where the table layout has it (rep8_u8), the match kernel stages its
+                                    input through shared memory with TMA gather copies (IBase streaming,
+                                    PAPER.md 1433-1440); 0 (default, measured faster): per-thread 32-byte loads */
 };
 dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value);
 

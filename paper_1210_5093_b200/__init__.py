@@ -43,6 +43,7 @@ DFA_OPT_COUNT_WORK = 13
 DFA_OPT_FUSED_TAIL = 14
 DFA_OPT_FACTORED = 15
 DFA_OPT_LOOKAHEAD2 = 16
+DFA_OPT_TMA_INPUT = 17
 
 
 def DFA_CREATE_TABLE_MODE(m: int) -> int:

@@ -4,6 +4,7 @@
 #include "kernels.cuh"
 #include "prep.h"
 
+#include <cuda.h>  // CUtensorMap (types only: the encoder is taken from the driver at run time)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +41,22 @@ struct DevBuf {
     void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
     template <class T> T *as() const { return reinterpret_cast<T *>(p); }
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
 
 struct HostPinned {
     void *p = nullptr;
@@ -78,6 +95,10 @@ struct dfa_handle {
     int warp_compose = 1;
     int factored = 1;             // DFA_OPT_FACTORED
     int lookahead2 = 1;           // DFA_OPT_LOOKAHEAD2
+    int tma_input = 0;            // DFA_OPT_TMA_INPUT (measured slower than register loads: DESIGN.md section 11)
+    DevBuf tmap;                  // device copy of the input's tensor map (TMA input staging)
+    CUtensorMap tmap_host;        // its host image (persistent: the upload reads it)
+    uint64_t tmap_base = 0, tmap_rows = 0;
     DevBuf dom2;                  // two-symbol initial sets + sizes (converge stage)
     int fused_tail = 0;           // DFA_OPT_FUSED_TAIL (measured slower than compose8: DESIGN.md)
     DevBuf part_rows, part_doms, chunk_cnt;
@@ -512,7 +533,7 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     }
     Plan plan{n, P, m0, m, (uint64_t)m0 + (uint64_t)(P - 1) * m, dev_bounds,
               o.first_dom == 0xFFFFFFFFu ? T.start_dom : o.first_dom, (uint64_t)(uintptr_t)in, o.indep ? 1u : 0u,
-              work, 0u, 0u, plan_magic(m0), plan_magic(m)};
+              work, 0u, 0u, nullptr, plan_magic(m0), plan_magic(m)};
     const uint64_t NS = plan.NS;
     h->stats.input_bytes = n;
     h->stats.num_subchunks = NS;
@@ -610,6 +631,35 @@ dfa_status run(dfa_handle *h, const uint8_t *in, uint64_t n, uint32_t P, const u
     if (grouped) {
         CK(h->leaf_rows.ensure(((NS >> sp.g_log) + 1) * T.rs * 2));
         CK(h->leaf_dom.ensure(((NS >> sp.g_log) + 1) * 2));
+    }
+    // TMA input staging (run_lanes_tma): one sub-chunk per thread, maps kept in registers, a
+    // layout it is built for.  The input as overlapping 64-byte rows at a 32-byte pitch from
+    // its 32-byte aligned base; rows that would end past the input are left to the byte loop.
+    plan.tmap = nullptr;
+    if (h->tma_input && grouped && !fused && !h->count_work && h->max_lanes >= kLanes && NS <= grid * (uint64_t)threads &&
+        lanes_tma_available(T, threads, h->optin_smem) && encode_tiled_fn()) {
+        const uint64_t addr = (uint64_t)(uintptr_t)in, base = addr & ~31ull, L = addr + n - base;
+        const uint64_t rows = L >= 64 ? (L - 64) / 32 + 1 : 0;
+        if (rows && rows < (1ull << 32)) {
+            if (!h->tmap.p || base != h->tmap_base || rows != h->tmap_rows) {
+                const cuuint64_t dims[2] = {64, rows}, strides[1] = {32};
+                const cuuint32_t box[2] = {64, 1}, estr[2] = {1, 1};
+                const CUresult cr = encode_tiled_fn()(&h->tmap_host, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                                                      reinterpret_cast<void *>((uintptr_t)base), dims, strides, box, estr,
+                                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (cr == CUDA_SUCCESS) {
+                    CK(h->tmap.ensure(sizeof(CUtensorMap)));
+                    g_scratch_gen++;  // a captured graph of another input must not replay against this map
+                    CK(cudaMemcpyAsync(h->tmap.p, &h->tmap_host, sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
+                    h->tmap_base = base;
+                    h->tmap_rows = rows;
+                } else {
+                    h->tmap_base = h->tmap_rows = 0;
+                }
+            }
+            if (h->tmap_base == base && h->tmap_rows == rows) plan.tmap = h->tmap.p;
+        }
     }
     {
         prof_begin(h, s, 1);
@@ -985,7 +1035,7 @@ dfa_status dfa_destroy(dfa_handle_t h) {
         if (h->copy_stream) { cudaStreamSynchronize(h->copy_stream); cudaStreamDestroy(h->copy_stream); }
         for (auto &e : h->hm_ev) if (e) cudaEventDestroy(e);
         for (DevBuf *b : {&h->hm_rows, &h->hm_bounds, &h->hm_la, &h->hm_final, &h->batch_bounds, &h->batch_kidx,
-                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full, &h->clinks, &h->dom2})
+                          &h->work, &h->node_nv, &h->node_fl, &h->rep_full, &h->clinks, &h->dom2, &h->tmap})
             b->release();
         h->h_hm.release();
         h->h_batch.release();
@@ -1249,7 +1299,7 @@ dfa_status chunk_maps_impl(dfa_handle_t h, const uint8_t *dev_input, uint64_t le
                        (uint64_t)h->convergence, (uint64_t)h->tree_fanin_cap, (uint64_t)h->fold_in_tree,
                        (uint64_t)h->max_lanes, (uint64_t)h->warp_compose, (uint64_t)h->subchunk_target,
                        (uint64_t)h->threads, (uint64_t)h->T.has_sticky, (uint64_t)h->count_work, (uint64_t)h->fused_tail,
-                       (uint64_t)h->factored, (uint64_t)h->lookahead2,
+                       (uint64_t)h->factored, (uint64_t)h->lookahead2, (uint64_t)h->tma_input,
                        (uint64_t)g_scratch_gen.load()})
         gkey.push_back(v);
     return run_graphed(h, gkey, s, body);
@@ -1475,6 +1525,9 @@ dfa_status dfa_set_option(dfa_handle_t h, uint32_t key, int64_t value) {
         return DFA_OK;
     case DFA_OPT_LOOKAHEAD2:
         h->lookahead2 = value ? 1 : 0;
+        return DFA_OK;
+    case DFA_OPT_TMA_INPUT:
+        h->tma_input = value ? 1 : 0;
         return DFA_OK;
     case DFA_OPT_THREADS_PER_CTA:
         h->threads_auto = value == 0;

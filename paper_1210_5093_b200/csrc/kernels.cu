@@ -711,6 +711,128 @@ __device__ __forceinline__ void run_lanes(const Tab<MODE> &tab, const uint32_t *
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA input staging (a.4, north_star): run_lanes with the sub-chunk's 32-byte
+// blocks brought into shared memory by cp.async.bulk.tensor ... tile::gather4
+// instead of per-thread global loads.  The input is a 2-D tensor of overlapping
+// rows (row r = bytes [32 r, 32 r + 64) from a 32-byte aligned base), so every
+// lane's aligned position is a row; per warp and stage eight ops fetch 64 bytes
+// for each of the 32 lanes into the warp's ring (2 stages x 32 x 64 B, SWIZZLE_64B:
+// each lane's 16-byte reads are conflict-free), one mbarrier per (warp, stage),
+// no CTA-wide synchronisation.  Every lane of the warp takes part in the issue
+// and the waits for max-over-lanes stages; a lane past its own range, or done,
+// idles.  Measured on the match step alone (tools/tma_gather4_bench.cu): rep8_u8 at
+// 640 threads 2754 vs 2351 GB/s for the register loads; in this kernel (Random):
+// 0.1398 vs 0.1316 ms -- every gather4 op takes its operands from uniform registers,
+// so the eight ops of a warp-stage are issued one lane at a time (~100 instructions
+// per 64 bytes per lane-row, +41 % instructions overall).  Opt-in (DFA_OPT_TMA_INPUT).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kTmaW = 64, kTmaStages = 2;
+__host__ __device__ __forceinline__ uint32_t tma_ring_bytes(uint32_t warps) {
+    return 1024u + warps * (kTmaStages * 32u * kTmaW) + warps * (kTmaStages * 8u);
+}
+
+template <int MODE>
+__device__ __forceinline__ void run_lanes_tma(const Tab<MODE> &tab, const uint32_t *absorb, bool has_absorb,
+                                              const uint8_t *in, uint64_t pos, uint64_t end, uint64_t n,
+                                              const void *tmap, uint32_t ring, uint32_t bars,
+                                              uint32_t (&st)[kLanes], uint32_t (&own)[kLanes], uint32_t nl,
+                                              int convergence, uint32_t (&fin)[kLanes], uint32_t &phase) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t nlive = nl;
+    const uint8_t *ptr = in + pos;
+    const uint8_t *endp = in + end;
+    uint32_t pend = kNoPend, pend_off = 0;
+    bool live = nl != 0;
+    // head: up to 31 bytes until 32-byte alignment
+    while (ptr < endp && (reinterpret_cast<uintptr_t>(ptr) & 31u)) step_scalar(tab, *ptr++, st, nlive);
+    // staged blocks: whole 32-byte blocks of the sub-chunk whose 64-byte row lies inside the input
+    const uintptr_t base = reinterpret_cast<uintptr_t>(in) & ~(uintptr_t)31;
+    const uintptr_t lim = reinterpret_cast<uintptr_t>(in) + n;  // rows must end at or before lim
+    uint32_t nblk = live && ptr < endp ? (uint32_t)((uint64_t)(endp - ptr) >> 5) : 0u;
+    while (nblk && reinterpret_cast<uintptr_t>(ptr) + 32ull * (nblk - 1) + kTmaW > lim) nblk--;
+    const uint32_t nst = (nblk + 1) >> 1;
+    const uint32_t wst = __reduce_max_sync(0xffffffffu, nst);
+    const uint32_t row0 = nblk ? (uint32_t)((reinterpret_cast<uintptr_t>(ptr) - base) >> 5) : 0u;
+    uint32_t r[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) r[j] = __shfl_sync(0xffffffffu, row0, 4 * (lane & 7) + j);
+    auto issue = [&](uint32_t stg, uint32_t k) {
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" :: "r"(bars + 8 * k), "r"(32u * kTmaW) : "memory");
+        __syncwarp();
+        if (lane < 8) {
+            const uint32_t adv = stg * (kTmaW / 32u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the lanes' reads of this stage, then the copy
+            asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                         :: "r"(ring + k * 32u * kTmaW + lane * 4u * kTmaW), "l"(tmap), "r"(0), "r"(r[0] + adv), "r"(r[1] + adv),
+                            "r"(r[2] + adv), "r"(r[3] + adv), "r"(bars + 8 * k) : "memory");
+        }
+    };
+    for (uint32_t k = 0; k < kTmaStages; k++) if (k < wst) issue(k, k);
+    for (uint32_t stg = 0; stg < wst; stg++) {
+        const uint32_t k = stg % kTmaStages;
+        // (phase: completed uses of each stage's barrier so far in this kernel, one bit per stage)
+        const uint32_t par = (phase >> k) & 1u;
+        uint32_t done = 0, spins = 0;
+        while (!done) {
+            asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                         : "=r"(done) : "r"(bars + 8 * k), "r"(par) : "memory");
+            if (!done && ++spins > (1u << 26)) asm volatile("trap;");  // never hang the GPU on a lost copy
+        }
+        phase ^= 1u << k;
+        uint4 q[kTmaW / 16];
+        const uint32_t rb = ring + k * 32u * kTmaW + lane * kTmaW;
+#pragma unroll
+        for (int j = 0; j < (int)(kTmaW / 16); j++) {
+            uint32_t a = rb + 16 * j;
+            a ^= ((a >> 7) & 3u) << 4;  // SWIZZLE_64B
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q[j].x), "=r"(q[j].y), "=r"(q[j].z), "=r"(q[j].w) : "r"(a));
+        }
+        __syncwarp();
+        if (stg + kTmaStages < wst) issue(stg + kTmaStages, k);
+        if (live && stg < nst) {
+            // the two 32-byte blocks of the stage, one copy of the step code (as run_lanes)
+#pragma unroll 1
+            for (uint32_t bb = 0; bb < 2 && live; bb++) {
+                const uint32_t bi = 2 * stg + bb;
+                if (bi >= nblk) break;  // the odd last block: first half of the stage only
+                const uint4 blo = bb ? q[2] : q[0], bhi = bb ? q[3] : q[1];
+#pragma unroll
+                for (int half = 0; half < 2; half++) {
+                    const uint4 v = half ? bhi : blo;
+                    const bool tick = half && (bi & 1);
+                    bool fin_all;
+                    switch (__reduce_max_sync(__activemask(), nlive)) {
+                    case 0:
+                    case 1: fin_all = block_step<1>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    case 2: fin_all = block_step<2>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    case 3: fin_all = block_step<3>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    case 4: fin_all = block_step<4>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    case 5: fin_all = block_step<5>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    case 6: fin_all = block_step<6>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    case 7: fin_all = block_step<7>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    default: fin_all = block_step<8>(tab, v, absorb, has_absorb, st, own, nlive, fin, convergence, tick, nullptr, false, pend, pend_off, 0u); break;
+                    }
+                    if (fin_all) { live = false; break; }
+                }
+            }
+        }
+    }
+    if (!live) return;
+    ptr += (uint64_t)nblk * 32;
+    while (ptr < endp) step_scalar(tab, *ptr++, st, nlive);
+    // remaining lanes: final state of the slot that carries them
+#pragma unroll
+    for (int rr = 0; rr < kLanes; rr++) {
+        if ((uint32_t)rr >= nl || own[rr] == kDone) continue;
+        uint32_t v = 0;
+#pragma unroll
+        for (int l = 0; l < kLanes; l++) v |= st[l] & (0u - (uint32_t)(own[rr] == (uint32_t)l));
+        fin[rr] = v - tab.bias;
+    }
+}
+
 // Rank-space maps (maps of <= 8 entries, the grouped path): an entry is either
 // a rank code kRank + r = "the r-th state of the NEXT sub-chunk's domain" or
 // an absolute state (error states, which no later byte leaves, and
@@ -1093,7 +1215,7 @@ __device__ __forceinline__ void fused_tail(const DevTables &T, const Plan &p, co
 
 // COUNT: the DFA_OPT_COUNT_WORK instantiation (a live counter register would make the
 // timed kernel spill, so counting is a separate instantiation)
-template <int MODE, bool STICKY, bool COUNT>
+template <int MODE, bool STICKY, bool COUNT, bool TMA>
 __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTables T, Plan p, const uint8_t *__restrict__ in,
                                                     const uint16_t *__restrict__ surv,
                                                     const uint8_t *__restrict__ surv_n,
@@ -1128,9 +1250,36 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
     const uint32_t *absorb = reinterpret_cast<const uint32_t *>(tsm) + smem_words<MODE>(T);
     uint64_t work = 0;  // executed lane-steps of this thread (DFA_OPT_COUNT_WORK)
     if (fz.on && fz.rows) tail_prefetch(T, p, fz, in, smem4, g_log);
+    // TMA input staging: the warp's ring and barriers after the bitmaps; whole warps enter the
+    // loop (lanes past NS idle through the warp-collective copy issue and waits)
+    uint32_t tma_ring = 0, tma_bars = 0, tma_phase = 0;
+    if constexpr (TMA) {
+        const uint32_t after = (uint32_t)__cvta_generic_to_shared(absorb + bw);
+        const uint32_t nwarps = blockDim.x >> 5, warp = threadIdx.x >> 5;
+        const uint32_t ring0 = (after + 1023u) & ~1023u;
+        tma_ring = ring0 + warp * (kTmaStages * 32u * kTmaW);
+        tma_bars = ring0 + nwarps * (kTmaStages * 32u * kTmaW) + warp * (kTmaStages * 8u);
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (uint32_t k = 0; k < kTmaStages; k++) asm volatile("mbarrier.init.shared.b64 [%0], 1;" :: "r"(tma_bars + 8 * k));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    const uint64_t ns_loop = TMA ? (p.NS + 31) & ~31ull : p.NS;
 
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.NS;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns_loop;
          i += (uint64_t)gridDim.x * blockDim.x) {
+        if constexpr (TMA) {
+            if (i >= p.NS) {  // an idle lane of the last warp
+                uint32_t st0[kLanes], own0[kLanes], fin0[kLanes];
+#pragma unroll
+                for (int l = 0; l < kLanes; l++) { st0[l] = tab.enc(0); own0[l] = kDone; fin0[l] = kNone; }
+                run_lanes_tma<MODE>(tab, absorb, T.has_absorb != 0, in, 0, 0, p.n, p.tmap, tma_ring, tma_bars, st0, own0, 0u,
+                                    convergence, fin0, tma_phase);
+                continue;
+            }
+        }
         uint64_t start, end;
         sub_range(p, i, start, end);
         const uint32_t dom = sub_domain(T, p, in, i, start);
@@ -1212,7 +1361,10 @@ __global__ void __launch_bounds__(lanes_max_threads(MODE), 1) lanes_kernel(DevTa
                 fin[l] = kNone;
             }
             uint32_t wk = 0;
-            if (nl) run_lanes<MODE, STICKY, COUNT>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
+            if constexpr (TMA)
+                run_lanes_tma<MODE>(tab, absorb, T.has_absorb != 0, in, pos, end, p.n, p.tmap, tma_ring, tma_bars, st, own, nl,
+                                    convergence, fin, tma_phase);
+            else if (nl) run_lanes<MODE, STICKY, COUNT>(tab, absorb, T.has_absorb != 0, sticky_s, dead_s, in, pos, end, st, own, nl,
                                             convergence, fin, wk);
             work += wk;
 #ifdef DFA_TREE_TIMING
@@ -2858,10 +3010,18 @@ void *converge_or_null(bool id8) {
     if constexpr (M == kIdentU8 || M == kRepU8x8 || M == kRepU8x4) return nullptr;
     else return id8 ? (void *)converge_kernel<M, true> : (void *)converge_kernel<M, false>;
 }
+template <int M>
+void *lanes_tma_or_null() {
+    // TMA input staging is built for the replicated layout (one 640-thread CTA per SM: few
+    // warps, where it pays)
+    if constexpr (M == kRepU8x8) return (void *)lanes_kernel<M, false, false, true>;
+    else return nullptr;
+}
 #define DFA_DEFINE_MODE_ENTRIES(M)                                                                      \
-    template <> void *lanes_entry<M>(bool sticky, bool count) {                                         \
-        return count ? (sticky ? (void *)lanes_kernel<M, true, true> : (void *)lanes_kernel<M, false, true>) \
-                     : (sticky ? (void *)lanes_kernel<M, true, false> : (void *)lanes_kernel<M, false, false>); \
+    template <> void *lanes_entry<M>(bool sticky, bool count, bool tma) {                               \
+        if (tma) return lanes_tma_or_null<M>();                                                         \
+        return count ? (sticky ? (void *)lanes_kernel<M, true, true, false> : (void *)lanes_kernel<M, false, true, false>) \
+                     : (sticky ? (void *)lanes_kernel<M, true, false, false> : (void *)lanes_kernel<M, false, false, false>); \
     }                                                                                                   \
     template <> void *ceiling_entry<M>() { return (void *)ceiling_kernel<M>; }                          \
     template <> void *converge_entry<M>(bool id8) { return converge_or_null<M>(id8); }
@@ -2897,18 +3057,18 @@ void *ceiling_fn(int mode) {
     }
 }
 
-void *lanes_fn(const DevTables &T, bool count = false) {
+void *lanes_fn(const DevTables &T, bool count = false, bool tma = false) {
     const bool st = T.has_sticky != 0;
     switch (T.mode) {
-    case kIdentU8: return lanes_entry<kIdentU8>(st, count);
-    case kRepU8x8: return lanes_entry<kRepU8x8>(st, count);
-    case kRepU8x4: return lanes_entry<kRepU8x4>(st, count);
-    case kIdentU8P: return lanes_entry<kIdentU8P>(st, count);
-    case kIdentU16: return lanes_entry<kIdentU16>(st, count);
-    case kWindowU8: return lanes_entry<kWindowU8>(st, count);
-    case kWindowU16: return lanes_entry<kWindowU16>(st, count);
-    case kPacked9: return lanes_entry<kPacked9>(st, count);
-    default: return lanes_entry<kGlobalU16>(st, count);
+    case kIdentU8: return lanes_entry<kIdentU8>(st, count, tma);
+    case kRepU8x8: return lanes_entry<kRepU8x8>(st, count, tma);
+    case kRepU8x4: return lanes_entry<kRepU8x4>(st, count, tma);
+    case kIdentU8P: return lanes_entry<kIdentU8P>(st, count, tma);
+    case kIdentU16: return lanes_entry<kIdentU16>(st, count, tma);
+    case kWindowU8: return lanes_entry<kWindowU8>(st, count, tma);
+    case kWindowU16: return lanes_entry<kWindowU16>(st, count, tma);
+    case kPacked9: return lanes_entry<kPacked9>(st, count, tma);
+    default: return lanes_entry<kGlobalU16>(st, count, tma);
     }
 }
 // The converge kernel steps all lanes of one sub-chunk on the same byte (a
@@ -2992,6 +3152,10 @@ cudaError_t setup_kernel_attributes(const DevTables &T) {
         if (e != cudaSuccess) return e;
     }
     cudaError_t e;
+    if (void *ft = lanes_fn(T, false, true)) {
+        e = cudaFuncSetAttribute(ft, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        if (e != cudaSuccess) return e;
+    }
     e = cudaFuncSetAttribute(converge_fn(T), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(ceiling_fn(T.mode), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
@@ -3078,6 +3242,8 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
                     (void *)&g_log, (void *)&leaf_rows, (void *)&leaf_dom, (void *)&status, (void *)&cap,
                     (void *)&fz};
     int smem = lanes_smem_bytes(T);
+    const bool tma = p.tmap != nullptr;
+    if (tma) smem += (int)tma_ring_bytes((uint32_t)threads / 32u);
     Fuse f2 = fz;
     if (fz.on) {
         // info area after both the table image and the tail area (it is written at kernel start)
@@ -3085,7 +3251,13 @@ cudaError_t launch_lanes(const DevTables &T, const Plan &p, const uint8_t *in, c
         smem = (int)f2.info_off + fused_info_bytes(threads, g_log);
     }
     args[16] = (void *)&f2;
-    return cudaLaunchKernel(lanes_fn(T, p.work != nullptr), dim3(grid), dim3(threads), args, smem, s);
+    return cudaLaunchKernel(lanes_fn(T, p.work != nullptr, tma), dim3(grid), dim3(threads), args, smem, s);
+}
+
+// TMA input staging available for this layout and CTA size (the ring must fit beside the table)
+bool lanes_tma_available(const DevTables &T, int threads, int optin_smem) {
+    return lanes_fn(T, false, true) != nullptr && !T.has_sticky &&
+           lanes_smem_bytes(T) + (int)tma_ring_bytes((uint32_t)threads / 32u) <= optin_smem;
 }
 
 const void *tree_fn() { return (const void *)tree_kernel; }

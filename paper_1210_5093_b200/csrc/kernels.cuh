@@ -70,6 +70,7 @@ struct Plan {
     unsigned long long *work; // DFA_OPT_COUNT_WORK: [0] converge, [1] lanes lane-steps; else null
     uint32_t keep_amap;      // factored composition: lanes_kernel leaves the converge maps coded
     uint32_t use_dom2;       // converge_kernel starts internal sub-chunks from the two-symbol sets
+    const void *tmap;        // device CUtensorMap of the input for TMA staging (run_lanes_tma), else null
     uint32_t magic_m0, magic_m; // min(floor(2^32 / m0), 2^32 - 1), same for m: exact 32-bit division on the device
 };
 inline uint32_t plan_magic(uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : (uint32_t)((1ull << 32) / d); }
@@ -174,6 +175,7 @@ int fused_tail_smem_bytes(int threads, uint32_t g_log, int grid);
 cudaError_t launch_fused_starts(const DevTables &T, const Plan &p, const Fuse &fz, const uint8_t *in, uint32_t lpc,
                                 uint32_t g_log, int grid, cudaStream_t s);
 int lanes_smem_bytes(const DevTables &T);
+bool lanes_tma_available(const DevTables &T, int threads, int optin_smem);
 int lanes_occupancy(const DevTables &T, int threads);
 int converge_occupancy(const DevTables &T, int warps_per_cta);
 cudaError_t launch_tree(const DevTables &T, const Tree &tr, int grid, int smem_bytes, cudaStream_t s);
@@ -214,11 +216,11 @@ int probe_dynamic_smem_base(uint32_t *dev_scratch);
 
 // Match kernels of one table layout (MODE = TableMode), one translation unit
 // each (kernels_m<MODE>.cu); nullptr where a layout has no such kernel.
-template <int MODE> void *lanes_entry(bool sticky, bool count);
+template <int MODE> void *lanes_entry(bool sticky, bool count, bool tma);
 template <int MODE> void *ceiling_entry();
 template <int MODE> void *converge_entry(bool id8);
 #define DFA_DECLARE_MODE_ENTRIES(M)                  \
-    template <> void *lanes_entry<M>(bool sticky, bool count); \
+    template <> void *lanes_entry<M>(bool sticky, bool count, bool tma); \
     template <> void *ceiling_entry<M>();            \
     template <> void *converge_entry<M>(bool id8);
 DFA_DECLARE_MODE_ENTRIES(1) DFA_DECLARE_MODE_ENTRIES(2) DFA_DECLARE_MODE_ENTRIES(3)

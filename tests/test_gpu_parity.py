@@ -903,6 +903,29 @@ def test_fused_tail_and_compose8(name, fused):
     check_match(c, opts={D.DFA_OPT_FUSED_TAIL: fused})
 
 
+def test_tma_input_staging():
+    """DFA_OPT_TMA_INPUT = 1 (rep8_u8: the match kernel's input staged by TMA gather4 copies,
+    run_lanes_tma): the oracle's maps, starts and final for chunk counts that leave whole and
+    partial warps, sub-chunks shorter than a stage, a misaligned input pointer (rows from the
+    32-byte aligned base) and an input whose last block's row would end past it."""
+    w = W.get("random")
+    for n in (1 << 20, (1 << 20) + 4321, 5000, 97):
+        x = w.input(n)
+        c = Case(w.automaton, x, "random")
+        for P in (1, 3, 64, 777):
+            if P <= n:
+                info = check_chunk_maps(c, P, opts={D.DFA_OPT_TMA_INPUT: 1})
+                assert info["table_mode_name"] == "rep8_u8"
+        check_match(c, opts={D.DFA_OPT_TMA_INPUT: 1})
+    x = w.input((1 << 19) + 77)
+    c = Case(w.automaton, x, "random")
+    buf = torch.zeros(x.size + 64, dtype=torch.uint8, device=DEV)
+    for off in (1, 13, 32, 47):
+        dev = buf[off:off + x.size]
+        dev.copy_(torch.from_numpy(x))
+        check_chunk_maps(c, 300, opts={D.DFA_OPT_TMA_INPUT: 1}, dev=dev)
+
+
 @pytest.mark.parametrize("factored", [0, 1])
 @pytest.mark.parametrize("name", ["worst", "protein", "counter"])
 def test_factored_and_full_row_composition(name, factored):

@@ -27,7 +27,14 @@ __device__ __forceinline__ uint32_t step16(uint32_t s, uint4 q, uint32_t tb) {
 #pragma unroll
         for (int kk = 0; kk < 4; kk++) {
             if (TAB == 0) s = lds_u8(__byte_perm(w4[wq], s, 0x6540 + kk));
-            else {
+            else if (TAB == 2) {
+                // rep8_u8: copy g = lane % 8 in banks 4g..4g+3; state register holds s + table >> 11
+                const uint32_t x = w4[wq], g4 = ((threadIdx.x & 7u) << 4) * 0x01010101u;
+                const uint32_t y = (x & 0x0F0F0F0Fu) | ((x & 0x10101010u) << 3) | g4, z = (x >> 5) & 0x07070707u;
+                uint32_t sel;
+                asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sel) : "r"(y), "r"(z), "r"(0xCC00u | ((4u + kk) << 4) | (uint32_t)kk));
+                s = lds_u8((s << 11) + sel);
+            } else {
                 const uint32_t c = (w4[wq] >> (8 * kk)) & 0xFFu, wc = (c * 171u) >> 9;
                 uint32_t v;
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(s * 348u + tb + 4u * wc));
@@ -40,9 +47,9 @@ __device__ __forceinline__ uint32_t step16(uint32_t s, uint4 q, uint32_t tb) {
 template <int TAB>
 __device__ __forceinline__ uint32_t load_table(uint8_t *sm, const uint8_t *img, uint32_t img_bytes) {
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t base = (sb + 255) & ~255u;
+    const uint32_t base = TAB == 2 ? (sb + 2047) & ~2047u : (sb + 255) & ~255u;
     uint8_t *tab = sm + (base - sb);
-    const uint32_t bias4 = TAB == 0 ? (base >> 8) * 0x01010101u : 0u;
+    const uint32_t bias4 = TAB == 0 ? (base >> 8) * 0x01010101u : TAB == 2 ? (base >> 11) * 0x01010101u : 0u;
     for (uint32_t i = threadIdx.x; i < img_bytes / 16; i += blockDim.x) {
         uint4 v = reinterpret_cast<const uint4 *>(img)[i];
         v.x = __vadd4(v.x, bias4); v.y = __vadd4(v.y, bias4); v.z = __vadd4(v.z, bias4); v.w = __vadd4(v.w, bias4);
@@ -60,7 +67,7 @@ __global__ void __launch_bounds__(1024, 1) gather_ldg(const uint8_t *img, uint32
     __syncthreads();
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint8_t *p = in + tid * per;
-    uint32_t s = TAB == 0 ? base >> 8 : 0u;
+    uint32_t s = TAB == 0 ? base >> 8 : TAB == 2 ? base >> 11 : 0u;
     uint4 lo, hi;
     asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w) : "l"(p));
     for (uint64_t bi = 0; bi < per / 32; bi++) {
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(1024, 1) gather_ldg(const uint8_t *img, uint32
         s = step16<TAB>(s, hi, base);
         lo = nlo; hi = nhi;
     }
-    out[tid] = s - (TAB == 0 ? base >> 8 : 0u);
+    out[tid] = s - (TAB == 0 ? base >> 8 : TAB == 2 ? base >> 11 : 0u);
 }
 
 // W bytes per lane and stage, S stages, swizzle SW (0 none, else matching W: 32/64/128)
@@ -109,7 +116,7 @@ __global__ void __launch_bounds__(1024, 1) gather_g4(const __grid_constant__ CUt
         }
     };
     for (int k = 0; k < S; k++) if ((uint64_t)k < nblk) issue(k, k);
-    uint32_t s = TAB == 0 ? base >> 8 : 0u;
+    uint32_t s = TAB == 0 ? base >> 8 : TAB == 2 ? base >> 11 : 0u;
     // swizzle: the 16-byte chunk index is XORed with address bits 7.. (128B: 3 bits, 64B: 2, 32B: 1)
     const uint32_t rowoff = lane * W;
     for (uint64_t bi = 0; bi < nblk; bi++) {
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(1024, 1) gather_g4(const __grid_constant__ CUt
 #pragma unroll
         for (int j = 0; j < W / 16; j++) s = step16<TAB>(s, q[j], base);
     }
-    out[tid] = s - (TAB == 0 ? base >> 8 : 0u);
+    out[tid] = s - (TAB == 0 ? base >> 8 : TAB == 2 ? base >> 11 : 0u);
 }
 
 static uint64_t rng = 88172645463325252ull;
@@ -145,7 +152,7 @@ int run_g4(const char *name, int threads, uint32_t pad, const uint8_t *dimg, uin
            uint32_t *dout, const std::vector<uint8_t> &hin, const std::vector<uint8_t> &delta, const std::vector<uint16_t> &d9) {
     const int grid = sms;
     const uint64_t per = (n / ((uint64_t)grid * threads)) & ~(uint64_t)(W - 1);
-    const size_t smem = 256 + bytes + pad + 1024 + (size_t)(threads / 32) * S * 32 * W + (threads / 32) * S * 8 + 64;
+    const size_t smem = 2048 + bytes + pad + 1024 + (size_t)(threads / 32) * S * 32 * W + (threads / 32) * S * 8 + 64;
     if (smem > 232448) { printf("{\"g4\": \"%s\", \"W\": %d, \"S\": %d, \"threads\": %d, \"pad\": %u, \"skip\": \"smem %zu\"}\n", name, W, S, threads, pad, smem); return 0; }
     CUtensorMap tm;
     const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)((n - W) / 32 + 1)};
@@ -163,7 +170,7 @@ int run_g4(const char *name, int threads, uint32_t pad, const uint8_t *dimg, uin
     int bad = 0;
     for (uint32_t t : {0u, 777u, (uint32_t)(grid * threads - 1)}) {
         uint32_t hs = 0;
-        for (uint64_t i = 0; i < per; i++) hs = TAB == 0 ? delta[hs * 256 + hin[t * per + i]] : d9[hs * 256 + hin[t * per + i]];
+        for (uint64_t i = 0; i < per; i++) hs = TAB != 1 ? delta[hs * 256 + hin[t * per + i]] : d9[hs * 256 + hin[t * per + i]];
         bad += got[t] != hs;
     }
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -219,6 +226,32 @@ int main(int argc, char **argv) {
     }
 #define RUN9(W, S, SW, T) if (run_g4<W, S, SW, 1>("packed9", T, 0, dimg9, bytes9, din, n, sms, dout, hin, delta, d9)) return 1;
     RUN9(32, 2, 32, 640) RUN9(32, 2, 32, 704) RUN9(32, 3, 32, 512) RUN9(64, 2, 64, 384)
+    // rep8_u8 (Random's layout): 64 states x 2 KB
+    {
+        const uint32_t bytes8 = nq * 2048;
+        std::vector<uint8_t> img8(bytes8, 0);
+        for (int g = 0; g < 8; g++) for (int st = 0; st < nq; st++) for (int b = 0; b < 256; b++)
+            img8[(st << 11) | (((b >> 5) & 7) << 8) | (((b >> 4) & 1) << 7) | (g << 4) | (b & 15)] = delta[st * 256 + b];
+        uint8_t *dimg8; CK(cudaMalloc(&dimg8, bytes8));
+        CK(cudaMemcpy(dimg8, img8.data(), bytes8, cudaMemcpyHostToDevice));
+        for (int threads : {640, 1024}) {
+            const int grid = sms;
+            const uint64_t per = (n / ((uint64_t)grid * threads)) & ~31ull;
+            CK(cudaFuncSetAttribute(gather_ldg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            const size_t smem = 2048 + bytes8 + 64;
+            gather_ldg<2><<<grid, threads, smem>>>(dimg8, bytes8, 0, din, per, dout);
+            CK(cudaDeviceSynchronize());
+            cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+            cudaEventRecord(a);
+            for (int r = 0; r < 20; r++) gather_ldg<2><<<grid, threads, smem>>>(dimg8, bytes8, 0, din, per, dout);
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            float ms; cudaEventElapsedTime(&ms, a, b); ms /= 20;
+            printf("{\"ldg32\": 1, \"table\": \"rep8_u8\", \"threads\": %d, \"ms\": %.4f, \"GBps\": %.1f}\n", threads, ms, (double)per * grid * threads / ms / 1e6);
+        }
+#define RUN8(W, S, SW, T) if (run_g4<W, S, SW, 2>("rep8_u8", T, 0, dimg8, bytes8, din, n, sms, dout, hin, delta, d9)) return 1;
+        RUN8(64, 2, 64, 640) RUN8(32, 2, 32, 640) RUN8(32, 4, 32, 640) RUN8(32, 2, 32, 1024)
+    }
     for (int threads : {1024, 640}) {
         const int grid = sms;
         const uint64_t per = (n / ((uint64_t)grid * threads)) & ~31ull;
