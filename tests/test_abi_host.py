@@ -38,6 +38,16 @@ def test_exports_every_declared_symbol():
         assert hasattr(L, n), n
 
 
+def test_binding_constants_match_header():
+    """Every DFA_OPT_* / DFA_ERR_* / DFA_CREATE_* value of include/dfa.h has the same value in the binding."""
+    src = open(os.path.join(ROOT, "include", "dfa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    consts = dict(re.findall(r"\b(DFA_(?:OPT|ERR|CREATE)_[A-Z0-9_]+)\s*=\s*(\d+)", src))
+    assert len([k for k in consts if k.startswith("DFA_OPT_")]) >= 17
+    for k, v in consts.items():
+        assert getattr(D, k) == int(v), k
+
+
 def test_sass_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", D.LIB], capture_output=True, text=True).stdout
