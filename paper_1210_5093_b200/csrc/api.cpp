@@ -441,8 +441,10 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         // converge_kernel costs ~ NS * |I_sigma| while a lanes kernel held to one CTA per SM
         // by a large table is pipe-bound at ~16 warps per SM (Worst, measured: 95k
         // sub-chunks 1499 GB/s, 151k 1388 GB/s): fewer, longer sub-chunks there
+        // (measured per layout: Worst/packed9 640 threads per SM 5.89 ms, 768: 5.98; Protein/window_u16
+        // 768 threads 1.624 ms, 640: 1.679, 1024: 1.691)
         if (h->convergence && h->T.imax > (uint32_t)kLanes && lanes_occupancy(h->T, 512) < 2)
-            target = std::min<uint64_t>(target, (uint64_t)h->sms * 1024 * 5 / 8);
+            target = std::min<uint64_t>(target, (uint64_t)h->sms * (h->T.mode == kPacked9 ? 640 : 768));
         // converge_kernel work per sub-chunk is ~|I_sigma| lanes over the first few hundred
         // bytes whatever the sub-chunk length: keep sub-chunks >= 4 KiB on average so that
         // short inputs (dfa_match_host pieces, segments) are not all convergence
@@ -471,6 +473,9 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
         // 151,552 threads, 1694 GB/s; 2072 after rounding down)
         const uint64_t slots = (uint64_t)h->sms * bps * std::min(bps >= 2 ? 512 : 1024, lanes_max_threads(h->T.mode));
         while (sp.m > 1 && (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m > slots) sp.m--;
+        // a sub-chunk stride that is a multiple of 8 KiB puts a warp's 32 streams on the same
+        // memory partitions (Protein, 1 MiB chunks in 32 parts: 1.82 ms vs 1.62 ms in 27)
+        while (sp.m > 1 && avg / sp.m >= 8192 && (avg / sp.m) % 8192 == 0 && avg % sp.m == 0) sp.m--;
         while (sp.m0 > 1 && (uint64_t)sp.m0 + (uint64_t)(P - 1) * sp.m > slots) sp.m0--;
     } else {
         // sub-chunks of >= 32 bytes; m a multiple of the largest power-of-two group

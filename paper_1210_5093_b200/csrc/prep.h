@@ -49,7 +49,8 @@ DFA_HD constexpr uint32_t rep_log_of(int mode) { return mode == kRepU8x8 ? 3u : 
 // threads for 88 registers with its sub-chunk count unchanged (6.80 vs 6.99 ms).
 // Every other layout: 1024 (64 registers).
 #ifndef DFA_WIN16_MAX_THREADS
-#define DFA_WIN16_MAX_THREADS 1024  // window_u16 (Protein) CTA bound; -D for the register-budget experiment
+#define DFA_WIN16_MAX_THREADS 896   // window_u16 (Protein) CTA bound: 73 registers; run at 768 threads behind the
+                                    // converge stage (plan_split), 1.624 ms vs 1.691 at 1024 threads / 64 registers
 #endif
 #ifndef DFA_PACKED9_MAX_THREADS
 #define DFA_PACKED9_MAX_THREADS 704  // packed9 (Worst) CTA bound; -D for the register-budget experiment
