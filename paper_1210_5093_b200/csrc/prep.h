@@ -55,8 +55,12 @@ DFA_HD constexpr uint32_t rep_log_of(int mode) { return mode == kRepU8x8 ? 3u : 
 #ifndef DFA_PACKED9_MAX_THREADS
 #define DFA_PACKED9_MAX_THREADS 704  // packed9 (Worst) CTA bound; -D for the register-budget experiment
 #endif
+#ifndef DFA_PAD_MAX_THREADS
+#define DFA_PAD_MAX_THREADS 768     // ident_u8_pad (Keyword) CTA bound: fewer, longer sub-chunks (6 instead of 9 per
+                                    // chunk at P = 16384): 0.425 ms vs 0.442 at 1024 threads (sweep in DESIGN.md section 11)
+#endif
 DFA_HD constexpr int lanes_max_threads(int mode) {
-    return mode == kRepU8x8 ? 640 : mode == kPacked9 ? DFA_PACKED9_MAX_THREADS : mode == kWindowU16 ? DFA_WIN16_MAX_THREADS : 1024;
+    return mode == kRepU8x8 ? 640 : mode == kIdentU8P ? DFA_PAD_MAX_THREADS : mode == kPacked9 ? DFA_PACKED9_MAX_THREADS : mode == kWindowU16 ? DFA_WIN16_MAX_THREADS : 1024;
 }
 
 struct Prep {
