@@ -496,6 +496,8 @@ Split plan_split(const dfa_handle *h, uint64_t n, uint32_t P, const uint64_t *hb
             const double c = (double)len0 / (double)std::max<uint64_t>(avg, 1);
             const uint64_t est = (uint64_t)((double)target / ((double)(P - 1) + c));
             sp.m = shape(std::min<uint64_t>(est, std::max<uint64_t>(1, minlen / 32)));
+            // (a stride that is a multiple of 8 KiB: see below; Keyword 64 KiB chunks in 8: 0.467 vs 0.442 ms)
+            if (sp.m > 1 && avg % sp.m == 0 && (avg / sp.m) % 8192 == 0) sp.m = shape(sp.m - 1);
             g = group_of(sp.m);
             uint64_t m0 = (uint64_t)((double)sp.m * c + 0.5);
             m0 = std::max<uint64_t>(g, m0 / g * g);

@@ -1,5 +1,5 @@
 set -x
-O=gpurun_out/r02s
+O=gpurun_out/quick
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "not slow" > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
 tail -5 $O/pytest.log
