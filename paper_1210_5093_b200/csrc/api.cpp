@@ -277,7 +277,8 @@ dfa_status upload(dfa_handle *h) {
     T.dom2 = nullptr;
     T.dom2_size = nullptr;
     T.dom2_stride = 0;
-    if (imax > (uint32_t)kLanes && !p.full_domain && nq <= 0x7F00u) {
+    if (imax > (uint32_t)kLanes && !p.full_domain && nq <= 0x7F00u &&
+        (size_t)nc * nc * imax * 4 <= (size_t)512 << 20) {  // (no point in building what cannot fit)
         std::vector<std::vector<uint32_t>> sets((size_t)nc * nc);
         std::vector<uint8_t> mark(nq);
         uint32_t smax = 0;
