@@ -302,13 +302,15 @@ struct Tab {
         } else return x;
     }
     // per input byte, shared by all lanes of the thread: the column's address
-    template <class X>
+    // PX: byte k by one PRMT (lanes_kernel: one instruction less on two bytes of four);
+    // converge_kernel keeps shift + mask (the PRMT form spills at its 64 registers)
+    template <bool PX = true, class X>
     __device__ __forceinline__ Pre bprep(X xw, int k) const {
         if constexpr (is_rep<MODE>()) {
             return {prmt_s(xw.x, xw.y, 0xCC00u | ((4u + k) << 4) | (uint32_t)k), 0u};
         } else {
         const uint32_t x = xw;
-        const uint32_t c = (x >> (8 * k)) & 0xFFu;
+        const uint32_t c = PX ? __byte_perm(x, 0u, 0x4440u | (uint32_t)k) : (x >> (8 * k)) & 0xFFu;
         if constexpr (MODE == kIdentU16) return {tb + 2u * c, 0u};
         else if constexpr (MODE == kWindowU8) return {tb + c, 0u};
         else if constexpr (MODE == kWindowU16) return {2u * c, 0u};
@@ -439,7 +441,7 @@ __device__ __forceinline__ void add_work(unsigned long long *ctr, uint64_t v) {
 // ---------------------------------------------------------------------------
 // Lanes l >= nlive of a thread do not load: a warp gather in which only some
 // threads still carry a second lane costs wavefronts for those threads only.
-template <int B, int MODE, int N>
+template <int B, int MODE, bool PX = true, int N>
 __device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t (&st)[N], uint32_t nlive) {
     static_assert(B <= N, "block16: more lanes than state registers");
     const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
@@ -471,7 +473,7 @@ __device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t 
         const auto x = tab.wprep(wds[wi]);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            const typename Tab<MODE>::Pre c = tab.bprep(x, k);
+            const typename Tab<MODE>::Pre c = tab.template bprep<PX>(x, k);
 #pragma unroll
             for (int l = 0; l < B; l++)
                 if (act[l]) st[l] = tab.look(st[l], x, k, c);
@@ -1593,9 +1595,9 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
                     // (three step variants only: the stage is instruction-fetch bound with
                     // eight, Worst: stall no_instruction 4.2 per issue)
                     switch (rows) {
-                    case 1: block16<1, MODE>(tab, v, s, nact); break;
-                    case 2: block16<2, MODE>(tab, v, s, nact); break;
-                    default: block16<kConvergeLA, MODE>(tab, v, s, nact); break;
+                    case 1: block16<1, MODE, false>(tab, v, s, nact); break;
+                    case 2: block16<2, MODE, false>(tab, v, s, nact); break;
+                    default: block16<kConvergeLA, MODE, false>(tab, v, s, nact); break;
                     }
                 } else {
                     for (uint32_t k = k0; k < k1; k++) {
@@ -1677,7 +1679,7 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
                 if (nd <= cap || pos >= end) break;
                 fetch_window();
                 if (act) {
-                    if (k0 == 0 && k1 == 16) block16<1, MODE>(tab, v, st1, 1u);
+                    if (k0 == 0 && k1 == 16) block16<1, MODE, false>(tab, v, st1, 1u);
                     else
                         for (uint32_t k = k0; k < k1; k++) {
                             const uint32_t wsel = k >> 2;
