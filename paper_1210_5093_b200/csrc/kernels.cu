@@ -459,7 +459,7 @@ __device__ __forceinline__ void block16(const Tab<MODE> &tab, uint4 v, uint32_t 
                 const uint32_t xd = (wds[wi] & tab.lo4) << 1;
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    const uint32_t a = (xd >> (8 * k)) & 0xFFu;
+                    const uint32_t a = PX ? __byte_perm(xd, 0u, 0x4440u | (uint32_t)k) : (xd >> (8 * k)) & 0xFFu;
 #pragma unroll
                     for (int l = 0; l < B; l++)
                         if (act[l]) st[l] = tab.lds_u16(st[l] * tab.rowb + a);
