@@ -37,7 +37,11 @@
  *
  * Ownership: dfa_create copies the table and bitmap (the caller may free
  * them on return).  The handle owns its device copies and scratch, freed by
- * dfa_destroy.  Every dev_* pointer is caller-owned device memory, borrowed
+ * dfa_destroy.  Device footprint of a handle: the tables (|Q| x 256 uint16, the
+ * I_sigma lists and rank tables over the byte classes), for I_max > 8 the
+ * two-symbol sets of Eq.istatesm (classes^2 x max |I_{s1 s2}| x 4 bytes, built
+ * only up to 128 MiB), and scratch that grows with the largest call (about
+ * 2 x I_max bytes per execution sub-chunk, ~10^5 sub-chunks).  Every dev_* pointer is caller-owned device memory, borrowed
  * for the stream-ordered lifetime of the call.
  *
  * Errors: every call returns a dfa_status; nothing is thrown across the

@@ -48,6 +48,31 @@ def test_binding_constants_match_header():
         assert getattr(D, k) == int(v), k
 
 
+def test_plan_division_magic_is_exact():
+    """The device's 32-bit sub-chunk arithmetic (kernels.cu udiv_magic / split_range, magics from
+    kernels.cuh plan_magic): umulhi(n, floor(2^32 / d)) is floor(n / d) or one less, so one
+    correction is exact; and floor(len j / m) = q j + floor(r j / m) with len = q m + r."""
+    rng = np.random.default_rng(5)
+    ds = [1, 2, 3, 5, 7, 22, 23, 27, 37, 640, 65535, 65536, 65537, (1 << 31) - 1, 1 << 31, (1 << 32) - 1]
+    ds += [int(v) for v in rng.integers(1, 1 << 32, 200)]
+    for d in ds:
+        magic = 0xFFFFFFFF if d <= 1 else (1 << 32) // d
+        ns = [0, 1, d - 1, d, d + 1, 2 * d - 1, (1 << 32) - 1, (1 << 32) - d] + [int(v) for v in rng.integers(0, 1 << 32, 50)]
+        for n in ns:
+            n &= 0xFFFFFFFF
+            q = (n * magic) >> 32
+            assert n // d - 1 <= q <= n // d
+            if n - q * d >= d:
+                q += 1
+            assert q == n // d, (n, d)
+    for _ in range(2000):
+        m = int(rng.integers(1, 65537))
+        ln = int(rng.integers(0, 1 << 32))
+        j = int(rng.integers(0, m + 1))
+        q, r = divmod(ln, m)
+        assert r * j < (1 << 32) and ln * j // m == q * j + (r * j) // m
+
+
 def test_sass_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", D.LIB], capture_output=True, text=True).stdout
