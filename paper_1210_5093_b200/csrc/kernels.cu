@@ -1523,6 +1523,9 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
         const uint64_t ab0 = start - ((reinterpret_cast<uintptr_t>(in) + start) & 15u);
         const uint64_t pb = ab0 + 16ull * lane;
         const uint4 pre = pb + 16 <= p.n ? ldg16(reinterpret_cast<const uint4 *>(in + pb)) : make_uint4(0, 0, 0, 0);
+        // (the byte two before the sub-chunk is loaded beside the one before it: one latency, not two)
+        const bool two = p.use_dom2 && T.dom2 && jsub != 0 && start >= cb0 + 2;
+        const uint32_t c1 = two ? (uint32_t)T.byte_class[__ldg(in + start - 2)] : 0u;
         const uint32_t dom = sub_domain(T, p, in, i, start);
         const uint32_t u = T.dom_size[dom];
         const uint16_t *dl = T.dom_list + (uint64_t)dom * T.rs;
@@ -1537,8 +1540,8 @@ __global__ void __launch_bounds__(1024, 1) converge_kernel(DevTables T, Plan p, 
         // stay ranks in I_s2, so the map and the composition do not change; the entries of
         // unreachable ranks are kNone and never looked up.
         const uint32_t *dl2 = nullptr;
-        if (p.use_dom2 && T.dom2 && jsub != 0 && start >= cb0 + 2) {
-            const uint32_t pair = (uint32_t)T.byte_class[__ldg(in + start - 2)] * T.nclass + dom;
+        if (two) {
+            const uint32_t pair = c1 * T.nclass + dom;
             dl2 = T.dom2 + (uint64_t)pair * T.dom2_stride;
             np = T.dom2_size[pair];
             DFA_CHECK(dom < T.nclass && np <= u, "converge: two-symbol set");
